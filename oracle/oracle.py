@@ -1,0 +1,425 @@
+"""ctypes bindings for the CPU oracle (liboracle.so) and the compiled reference (_ref/libtgf_ref.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs -- as the checker or the CPU baseline, never as the
+product path.  The product (paper_2409_05477_b200, libtgfx.so) never imports this module.
+
+Array conventions follow the reference (proj/include/tgformer/*.hpp): ids int64, times
+float64, events as the 32-byte TemporalEvent record (event_stream.hpp:13-18).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libtgf_ref.so")
+
+EVENT_DTYPE = np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_U64 = C.c_uint64
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def build_oracle():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+_orc = None
+_ref = None
+
+
+def lib():
+    """The C restatement (oracle.c)."""
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORACLE_SO):
+            build_oracle()
+        L = C.CDLL(ORACLE_SO)
+        L.orc_mix64.restype = _U64
+        L.orc_mix64.argtypes = [_U64]
+        L.orc_rng_state.restype = _U64
+        L.orc_rng_state.argtypes = [_U64, _U64]
+        L.orc_rng_draw.restype = _U64
+        L.orc_rng_draw.argtypes = [_U64, _U64]
+        L.orc_mulhi64.restype = _U64
+        L.orc_mulhi64.argtypes = [_U64, _U64]
+        L.orc_make_random_stream.argtypes = [_I64, _I64, _U64, C.c_double, _P]
+        L.orc_zipf_cdf.argtypes = [_I64, C.c_double, _P]
+        L.orc_build.argtypes = [_P, _I64, _I64, C.c_int, _P, _P, _P, _P, _P]
+        L.orc_validate.argtypes = [_I64, _I64, _I64, _P, _P, _P, _P]
+        L.orc_prefix_end.restype = _I64
+        L.orc_prefix_end.argtypes = [_P, _P, _I64, C.c_double]
+        L.orc_sample_batch.argtypes = [_I64, _P, _P, _P, _P, _P, _P, _I64, _I64, C.c_int, _U64,
+                                       _U64, _P, _P, _P, _P, _P]
+        L.orc_build_sequence_batch.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64,
+                                               _P, _P, _P, _P, _P]
+        L.orc_build_mask.argtypes = [_I64, _I64, _P, _P, C.c_int, _P]
+        L.orc_make_queries.argtypes = [_P, _I64, _I64, _I64, _I64, _U64, _P, _P]
+        _orc = L
+    return _orc
+
+
+def ref_available():
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    """The reference's own hot path (compiled from /root/reference by oracle/Makefile)."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise RuntimeError(f"reference build {REF_SO} missing (run make -C oracle)")
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_make_random_stream.argtypes = [_I64, _I64, _U64, C.c_double, _P]
+        L.ref_stream_create.restype = _P
+        L.ref_stream_create.argtypes = [_P, _I64, _I64]
+        L.ref_stream_free.argtypes = [_P]
+        L.ref_build.argtypes = [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_double)]
+        L.ref_build_parallel_raw.argtypes = [_P, C.c_int, C.c_int, C.POINTER(_P)]
+        L.ref_graph_free.argtypes = [_P]
+        L.ref_graph_info.argtypes = [_P, _P]
+        L.ref_graph_export.argtypes = [_P, _P, _P, _P, _P]
+        L.ref_graph_validate.argtypes = [_P]
+        L.ref_sample_batch.argtypes = [_P, _P, _P, _I64, _I64, C.c_int, _U64, C.c_int, _P, _P, _P,
+                                       _P, C.POINTER(C.c_double)]
+        L.ref_sample_random.argtypes = [_P, _I64, C.c_double, _I64, _U64, _U64, _P, _P, _P, _P]
+        L.ref_sample_assemble.argtypes = [_P, _P, _P, _I64, _I64, C.c_int, _U64, C.c_int, _I64,
+                                          _I64, _P, _P, _P, _P, C.POINTER(C.c_double)]
+        L.ref_build_sequence_batch.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P,
+                                               _P, _P, _P, _P]
+        L.ref_build_mask.argtypes = [_I64, _I64, _P, _P, C.c_int, _P]
+        _ref = L
+    return _ref
+
+
+class OracleError(Exception):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+# --------------------------------------------------------------------------- restatement
+
+def mix64(x):
+    return lib().orc_mix64(x)
+
+
+def make_random_stream(num_edges, num_nodes, seed, zipf=1.2):
+    ev = np.zeros(num_edges, dtype=EVENT_DTYPE)
+    rc = lib().orc_make_random_stream(num_edges, num_nodes, seed, zipf, _ptr(ev))
+    if rc:
+        raise OracleError(1, "bad stream dimensions")
+    return ev
+
+
+def zipf_cdf(num_nodes, zipf=1.2):
+    cdf = np.zeros(num_nodes, dtype=np.float64)
+    lib().orc_zipf_cdf(num_nodes, zipf, _ptr(cdf))
+    return cdf
+
+
+def events_from(src, dst, ts, eid=None):
+    n = len(src)
+    ev = np.zeros(n, dtype=EVENT_DTYPE)
+    ev["edge_id"] = np.arange(n) if eid is None else eid
+    ev["src"], ev["dst"], ev["timestamp"] = src, dst, ts
+    return ev
+
+
+def build(events, num_nodes, reverse=True):
+    """build_sequential (tcsr.cpp:83-105) -> dict(indptr, nbr, eid, ts)."""
+    events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    n = len(events)
+    m = n * (2 if reverse else 1)
+    indptr = np.zeros(num_nodes + 1, dtype=np.int64)
+    nbr = np.zeros(max(m, 1), dtype=np.int64)
+    eid = np.zeros(max(m, 1), dtype=np.int64)
+    ts = np.zeros(max(m, 1), dtype=np.float64)
+    bad = np.zeros(1, dtype=np.int64)
+    rc = lib().orc_build(_ptr(events), n, num_nodes, 1 if reverse else 0, _ptr(indptr), _ptr(nbr),
+                         _ptr(eid), _ptr(ts), _ptr(bad))
+    if rc:
+        raise OracleError(1, f"event {int(bad[0])} endpoint out of range")
+    return dict(num_nodes=num_nodes, num_edges=n, reverse=bool(reverse), indptr=indptr,
+                nbr=nbr[:m], eid=eid[:m], ts=ts[:m])
+
+
+def validate(g):
+    rc = lib().orc_validate(g["num_nodes"], g["num_edges"], len(g["nbr"]), _ptr(g["indptr"]),
+                            _ptr(g["nbr"]), _ptr(g["eid"]), _ptr(g["ts"]))
+    return rc == 0
+
+
+def sample_batch(g, nodes, times, k, strategy="recent", seed=0, stream_base=0):
+    """sample_batch (sampler.cpp:84-104) -> (counts[Q], nbr[Q,k], eid[Q,k], ts[Q,k])."""
+    nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+    times = np.ascontiguousarray(times, dtype=np.float64)
+    q = len(nodes)
+    kp = max(k, 1)
+    counts = np.zeros(q, dtype=np.int64)
+    nb = np.zeros(q * kp, dtype=np.int64)
+    ed = np.zeros(q * kp, dtype=np.int64)
+    tt = np.zeros(q * kp, dtype=np.float64)
+    bad = np.zeros(1, dtype=np.int64)
+    rc = lib().orc_sample_batch(g["num_nodes"], _ptr(g["indptr"]), _ptr(g["nbr"]), _ptr(g["eid"]),
+                                _ptr(g["ts"]), _ptr(nodes), _ptr(times), q, k,
+                                0 if strategy == "recent" else 1, seed, stream_base, _ptr(counts),
+                                _ptr(nb), _ptr(ed), _ptr(tt), _ptr(bad))
+    if rc == 1:
+        raise OracleError(1, f"query node {int(bad[0])} out of range")
+    if rc == 2:
+        raise OracleError(1, "k must be at least 1")
+    return counts, nb.reshape(q, kp), ed.reshape(q, kp), tt.reshape(q, kp)
+
+
+def build_sequence_batch(counts, nbr, eid, ts, qnodes, qtimes, l, self_edge_index):
+    """build_sequence_batch (sequence.cpp:55-86) -> dict of int64/float64 arrays."""
+    q, kp = nbr.shape
+    ni = np.zeros(q * l, dtype=np.int64)
+    ei = np.zeros(q * l, dtype=np.int64)
+    dt = np.zeros(q * l, dtype=np.float64)
+    vl = np.zeros(q, dtype=np.int64)
+    tr = np.zeros(q, dtype=np.int64)
+    c = [np.ascontiguousarray(a) for a in (counts, nbr, eid, ts)]
+    qn = np.ascontiguousarray(qnodes, dtype=np.int64)
+    qt = np.ascontiguousarray(qtimes, dtype=np.float64)
+    rc = lib().orc_build_sequence_batch(q, kp, _ptr(c[0]), _ptr(c[1]), _ptr(c[2]), _ptr(c[3]),
+                                        _ptr(qn), _ptr(qt), l, self_edge_index, _ptr(ni), _ptr(ei),
+                                        _ptr(dt), _ptr(vl), _ptr(tr))
+    if rc:
+        raise OracleError(1, "sequence length must be at least 2")
+    return dict(node_index=ni.reshape(q, l), edge_index=ei.reshape(q, l),
+                time_delta=dt.reshape(q, l), valid_len=vl, target_row=tr)
+
+
+def sample_assemble(g, nodes, times, k, strategy, seed, l, self_edge_index, stream_base=0):
+    counts, nb, ed, tt = sample_batch(g, nodes, times, k, strategy, seed, stream_base)
+    return build_sequence_batch(counts, nb, ed, tt, nodes, times, l, self_edge_index)
+
+
+def build_mask(valid_len, target_row, l, kind):
+    kinds = {"causal": 0, "tgat": 1, "self_loop": 2}
+    q = len(valid_len)
+    mask = np.zeros(q * l * l, dtype=np.float64)
+    vl = np.ascontiguousarray(valid_len, dtype=np.int64)
+    tr = np.ascontiguousarray(target_row, dtype=np.int64)
+    lib().orc_build_mask(q, l, _ptr(vl), _ptr(tr), kinds[kind], _ptr(mask))
+    return mask.reshape(q * l, l)
+
+
+def make_queries(events, e0, e1, batch, num_nodes, neg_seed=7):
+    events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    n = 3 * (e1 - e0)
+    nodes = np.zeros(n, dtype=np.int64)
+    times = np.zeros(n, dtype=np.float64)
+    lib().orc_make_queries(_ptr(events), e0, e1, batch, num_nodes, neg_seed, _ptr(nodes),
+                           _ptr(times))
+    return nodes, times
+
+
+def two_hop(g, roots, rtimes, k1, k2, strategy, seed, l, self_edge_index, seed2=None):
+    """2-hop composition defined over reference calls:
+
+    hop-1 = sample_batch(roots, k1); hop-2 query for hop-1 entry j of root q is
+    (nbr_j, ts_j) sampled with k2 (recent) or sample_random(seed2, stream = q*k1 + j).
+    Returns hop-1 rows [Q, l] and hop-2 rows [Q, k1, l] (absent slots zero, valid_len 0).
+    """
+    q = len(roots)
+    c1, n1, e1, t1 = sample_batch(g, roots, rtimes, k1, strategy, seed)
+    hop1 = build_sequence_batch(c1, n1, e1, t1, roots, rtimes, l, self_edge_index)
+    ni = np.zeros((q, k1, l), np.int64)
+    ei = np.zeros((q, k1, l), np.int64)
+    dt = np.zeros((q, k1, l), np.float64)
+    vl = np.zeros((q, k1), np.int64)
+    qi, ji = np.nonzero(np.arange(k1)[None, :] < c1[:, None])
+    if len(qi):
+        hn = n1[qi, ji]
+        ht = t1[qi, ji]
+        if strategy == "recent":
+            c2, n2, e2, t2 = sample_batch(g, hn, ht, k2, "recent", 0)
+        else:
+            s2 = seed if seed2 is None else seed2
+            c2 = np.zeros(len(qi), np.int64)
+            n2 = np.zeros((len(qi), k2), np.int64)
+            e2 = np.zeros((len(qi), k2), np.int64)
+            t2 = np.zeros((len(qi), k2), np.float64)
+            for r in range(len(qi)):
+                cc, a, b, c = sample_batch(g, hn[r:r + 1], ht[r:r + 1], k2, "random", s2,
+                                           stream_base=int(qi[r]) * k1 + int(ji[r]))
+                c2[r], n2[r], e2[r], t2[r] = cc[0], a[0], b[0], c[0]
+        h2 = build_sequence_batch(c2, n2, e2, t2, hn, ht, l, self_edge_index)
+        ni[qi, ji] = h2["node_index"]
+        ei[qi, ji] = h2["edge_index"]
+        dt[qi, ji] = h2["time_delta"]
+        vl[qi, ji] = h2["valid_len"]
+    return hop1, dict(node_index=ni, edge_index=ei, time_delta=dt, valid_len=vl)
+
+
+# --------------------------------------------------------------------------- reference
+
+class RefGraph:
+    """A tgf::TCsr built by the compiled reference."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_graph_free(self.h)
+            self.h = None
+
+    def info(self):
+        out = np.zeros(4, np.int64)
+        ref().ref_graph_info(self.h, _ptr(out))
+        return dict(num_nodes=int(out[0]), num_edges=int(out[1]), num_entries=int(out[2]),
+                    reverse=bool(out[3]))
+
+    def export(self):
+        inf = self.info()
+        m = inf["num_entries"]
+        indptr = np.zeros(inf["num_nodes"] + 1, np.int64)
+        nbr = np.zeros(max(m, 1), np.int64)
+        eid = np.zeros(max(m, 1), np.int64)
+        ts = np.zeros(max(m, 1), np.float64)
+        ref().ref_graph_export(self.h, _ptr(indptr), _ptr(nbr), _ptr(eid), _ptr(ts))
+        return dict(num_nodes=inf["num_nodes"], num_edges=inf["num_edges"],
+                    reverse=inf["reverse"], indptr=indptr, nbr=nbr[:m], eid=eid[:m], ts=ts[:m])
+
+
+def _ref_err(rc):
+    msg = ref().ref_last_error().decode()
+    raise OracleError(rc, msg)
+
+
+def ref_make_random_stream(num_edges, num_nodes, seed, zipf=1.2):
+    ev = np.zeros(num_edges, dtype=EVENT_DTYPE)
+    rc = ref().ref_make_random_stream(num_edges, num_nodes, seed, zipf, _ptr(ev))
+    if rc:
+        _ref_err(rc)
+    return ev
+
+
+class RefStream:
+    def __init__(self, events, num_nodes):
+        self.events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+        self.h = ref().ref_stream_create(_ptr(self.events), len(self.events), num_nodes)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_stream_free(self.h)
+            self.h = None
+
+    def build(self, reverse=True, threads=0):
+        """threads <= 0: build_sequential; else build_parallel(threads). -> (RefGraph, secs)."""
+        g = C.c_void_p()
+        s = C.c_double()
+        rc = ref().ref_build(self.h, 1 if reverse else 0, threads, C.byref(g), C.byref(s))
+        if rc:
+            _ref_err(rc)
+        return RefGraph(g.value), s.value
+
+    def build_parallel_raw(self, reverse, threads):
+        g = C.c_void_p()
+        rc = ref().ref_build_parallel_raw(self.h, 1 if reverse else 0, threads, C.byref(g))
+        if rc:
+            _ref_err(rc)
+        return RefGraph(g.value)
+
+
+def ref_sample_batch(rg, nodes, times, k, strategy="recent", seed=0, threads=0):
+    nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+    times = np.ascontiguousarray(times, dtype=np.float64)
+    q = len(nodes)
+    kp = max(k, 1)
+    counts = np.zeros(q, np.int64)
+    nb = np.zeros(q * kp, np.int64)
+    ed = np.zeros(q * kp, np.int64)
+    tt = np.zeros(q * kp, np.float64)
+    s = C.c_double()
+    rc = ref().ref_sample_batch(rg.h, _ptr(nodes), _ptr(times), q, k,
+                                0 if strategy == "recent" else 1, seed, threads, _ptr(counts),
+                                _ptr(nb), _ptr(ed), _ptr(tt), C.byref(s))
+    if rc:
+        _ref_err(rc)
+    return (counts, nb.reshape(q, kp), ed.reshape(q, kp), tt.reshape(q, kp)), s.value
+
+
+def ref_sample_random(rg, u, t, k, seed, stream):
+    cnt = np.zeros(1, np.int64)
+    nb = np.zeros(max(k, 1), np.int64)
+    ed = np.zeros(max(k, 1), np.int64)
+    tt = np.zeros(max(k, 1), np.float64)
+    rc = ref().ref_sample_random(rg.h, u, t, k, seed, stream, _ptr(cnt), _ptr(nb), _ptr(ed),
+                                 _ptr(tt))
+    if rc:
+        _ref_err(rc)
+    c = int(cnt[0])
+    return nb[:c], ed[:c], tt[:c]
+
+
+def ref_sample_assemble(rg, nodes, times, k, strategy, seed, l, self_edge_index, threads=0,
+                        want_outputs=True):
+    nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+    times = np.ascontiguousarray(times, dtype=np.float64)
+    q = len(nodes)
+    if want_outputs:
+        ni = np.zeros(q * l, np.int64)
+        ei = np.zeros(q * l, np.int64)
+        dt = np.zeros(q * l, np.float64)
+        vl = np.zeros(q, np.int64)
+    else:
+        ni = ei = dt = vl = None
+    s = C.c_double()
+    rc = ref().ref_sample_assemble(rg.h, _ptr(nodes), _ptr(times), q, k,
+                                   0 if strategy == "recent" else 1, seed, threads, l,
+                                   self_edge_index, _ptr(ni), _ptr(ei), _ptr(dt), _ptr(vl),
+                                   C.byref(s))
+    if rc:
+        _ref_err(rc)
+    out = None
+    if want_outputs:
+        out = dict(node_index=ni.reshape(q, l), edge_index=ei.reshape(q, l),
+                   time_delta=dt.reshape(q, l), valid_len=vl)
+    return out, s.value
+
+
+def ref_build_sequence_batch(counts, nbr, eid, ts, qnodes, qtimes, l, self_edge_index):
+    q, kp = nbr.shape
+    ni = np.zeros(q * l, np.int64)
+    ei = np.zeros(q * l, np.int64)
+    dt = np.zeros(q * l, np.float64)
+    vl = np.zeros(q, np.int64)
+    tr = np.zeros(q, np.int64)
+    c = [np.ascontiguousarray(a) for a in (counts, nbr, eid, ts)]
+    qn = np.ascontiguousarray(qnodes, dtype=np.int64)
+    qt = np.ascontiguousarray(qtimes, dtype=np.float64)
+    rc = ref().ref_build_sequence_batch(q, kp, _ptr(c[0]), _ptr(c[1]), _ptr(c[2]), _ptr(c[3]),
+                                        _ptr(qn), _ptr(qt), l, self_edge_index, _ptr(ni),
+                                        _ptr(ei), _ptr(dt), _ptr(vl), _ptr(tr))
+    if rc:
+        _ref_err(rc)
+    return dict(node_index=ni.reshape(q, l), edge_index=ei.reshape(q, l),
+                time_delta=dt.reshape(q, l), valid_len=vl, target_row=tr)
+
+
+def ref_build_mask(valid_len, target_row, l, kind):
+    kinds = {"causal": 0, "tgat": 1, "self_loop": 2}
+    q = len(valid_len)
+    mask = np.zeros(q * l * l, np.float64)
+    vl = np.ascontiguousarray(valid_len, dtype=np.int64)
+    tr = np.ascontiguousarray(target_row, dtype=np.int64)
+    rc = ref().ref_build_mask(q, l, _ptr(vl), _ptr(tr), kinds[kind], _ptr(mask))
+    if rc:
+        _ref_err(rc)
+    return mask.reshape(q * l, l)
