@@ -1,0 +1,188 @@
+/*
+ * tgfx.h -- C ABI of the B200-native T-CSR builder, temporal sampler and sequence assembler.
+ *
+ * Drop-in boundary for the reference hot path (tgformer, arXiv 2409.05477; paths below are
+ * relative to the reference tree).  Every entry point cites the reference interface it
+ * replaces.  Plain pointers and sizes only (no C++ / torch types).  All compute runs on the
+ * current CUDA device in hand-written sm_100a kernels; there is no CPU fallback: without a
+ * usable device every call fails with TGFX_ECUDA.
+ *
+ * Conventions
+ *   - Host-buffer calls (no _device suffix) are synchronous, like the reference functions:
+ *     inputs are uploaded, computed on the GPU and results copied back before returning.
+ *     Nothing is written to caller outputs when an error is returned.
+ *   - *_device calls take device pointers and a cudaStream_t (passed as void*, NULL = legacy
+ *     default stream).  With flags & TGFX_TRUSTED they skip input validation and do not
+ *     synchronise (fully asynchronous); otherwise they validate, synchronise and report.
+ *   - Errors: return code (TGFX_E*), message via tgfx_last_error() (thread-local), with the
+ *     reference's exception texts (proj/include/tgformer/common.hpp:15-27 error classes).
+ *   - Ids are int64 and times double, as proj/include/tgformer/common.hpp:10-12.
+ */
+#ifndef TGFX_H
+#define TGFX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGFX_ABI_VERSION 1
+
+/* status codes; the C++ shim (include/tgfx/tgformer.hpp) rethrows the reference types */
+#define TGFX_OK 0
+#define TGFX_EVALIDATION 1  /* tgf::ValidationError */
+#define TGFX_EFORMAT 2      /* tgf::FormatError */
+#define TGFX_ECUDA 3        /* CUDA runtime / no device (std::runtime_error) */
+#define TGFX_ENOMEM 4       /* device or host allocation failed (std::bad_alloc) */
+#define TGFX_EUNSUPPORTED 5 /* e.g. ids that do not fit the requested int32 outputs */
+
+/* sampling strategy: proj/include/tgformer/sampler.hpp:26 (SampleStrategy) */
+#define TGFX_RECENT 0
+#define TGFX_RANDOM 1
+
+/* mask kinds: proj/include/tgformer/sequence.hpp:38 (MaskKind) */
+#define TGFX_MASK_CAUSAL 0
+#define TGFX_MASK_TGAT 1
+#define TGFX_MASK_SELF_LOOP 2
+
+/* flags for *_device calls */
+#define TGFX_TRUSTED 1u   /* inputs known valid: no validation pass, no synchronisation */
+#define TGFX_INDEX64 2u   /* sample_assemble: node/edge index and valid_len are int64 */
+
+/* proj/include/tgformer/event_stream.hpp:13-18 (TemporalEvent), byte-identical, so
+ * stream.events.data() is passed without repacking. */
+typedef struct tgfx_event {
+  int64_t edge_id;
+  int64_t src;
+  int64_t dst;
+  double timestamp;
+} tgfx_event;
+
+/* Opaque device-resident T-CSR (proj/include/tgformer/tcsr.hpp:20-33 TCsr). */
+typedef struct tgfx_graph tgfx_graph;
+
+/* ---------------------------------------------------------------- runtime */
+const char* tgfx_last_error(void);
+int tgfx_abi_version(void);
+/* number of kernel launches issued by this library so far (process-wide counter) */
+uint64_t tgfx_launch_count(void);
+/* bytes of device memory currently held by tgfx graphs + workspaces */
+int64_t tgfx_device_bytes(void);
+
+/* ---------------------------------------------------------------- T-CSR build */
+/* replaces tgf::build_sequential (proj/include/tgformer/tcsr.hpp:37, tcsr.cpp:83-105) */
+int tgfx_build_sequential(const tgfx_event* events, int64_t n, int64_t num_nodes, int reverse,
+                          tgfx_graph** out);
+/* replaces tgf::build_parallel (tcsr.hpp:43, tcsr.cpp:107-151).  num_threads < 1 is a
+ * ValidationError as in tcsr.cpp:108; otherwise it is accepted and ignored (the grid is
+ * sized for the device); the result is element-for-element identical. */
+int tgfx_build_parallel(const tgfx_event* events, int64_t n, int64_t num_nodes, int reverse,
+                        int num_threads, tgfx_graph** out);
+/* device-resident events (n x 32 bytes); builds into a new graph. */
+int tgfx_build_device(const tgfx_event* d_events, int64_t n, int64_t num_nodes, int reverse,
+                      void* stream, unsigned flags, tgfx_graph** out);
+/* rebuild an existing graph in place from device events with the same (n, num_nodes,
+ * reverse); reuses its buffers and workspace (no allocation), for repeated builds. */
+int tgfx_rebuild_device(tgfx_graph* g, const tgfx_event* d_events, void* stream,
+                        unsigned flags);
+/* import a host T-CSR (e.g. from load_tcsr, tcsr.cpp:176-197) to the device. */
+int tgfx_graph_from_host(int64_t num_nodes, int64_t num_edges, int reverse, int64_t m,
+                         const int64_t* indptr, const int64_t* nbr, const int64_t* eid,
+                         const double* ts, tgfx_graph** out);
+int tgfx_graph_info(const tgfx_graph* g, int64_t* num_nodes, int64_t* num_edges,
+                    int64_t* num_entries, int* reverse);
+/* copy the T-CSR columns to host: indptr[num_nodes+1], nbr/eid/ts[num_entries] */
+int tgfx_graph_export(const tgfx_graph* g, int64_t* indptr, int64_t* nbr, int64_t* eid,
+                      double* ts);
+int tgfx_graph_device_arrays(const tgfx_graph* g, const int64_t** indptr, const int64_t** nbr,
+                             const int64_t** eid, const double** ts);
+/* replaces TCsr::validate (tcsr.cpp:54-81), run on the device */
+int tgfx_graph_validate(const tgfx_graph* g);
+int tgfx_graph_free(tgfx_graph* g);
+/* path the last build took: 0 presorted fast path, 1 general (re-sort), 2 large-V path */
+int tgfx_graph_build_path(const tgfx_graph* g);
+
+/* ---------------------------------------------------------------- sampling */
+/* replaces tgf::sample_batch (sampler.hpp:42-45, sampler.cpp:84-104) [and sample_recent /
+ * sample_random for q = 1, sampler.hpp:32-38].  Query i uses RNG stream stream_base + i
+ * (stream_base = 0 is the reference).  Outputs padded [q, k]: counts[q] and nbr/eid/ts
+ * [q*k] in ascending (t, eid) order, unused slots zero. */
+int tgfx_sample_batch(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                      int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
+                      int64_t* counts, int64_t* nbr, int64_t* eid, double* ts);
+int tgfx_sample_batch_device(const tgfx_graph* g, const int64_t* d_nodes,
+                             const double* d_times, int64_t q, int64_t k, int strategy,
+                             uint64_t seed, uint64_t stream_base, int64_t* d_counts,
+                             int64_t* d_nbr, int64_t* d_eid, double* d_ts, void* stream,
+                             unsigned flags);
+
+/* sample_batch fused with build_sequence_batch (sequence.cpp:55-86), i.e. the pair
+ * forward_concat runs (training.cpp:211-214), without materialising NeighborSamples.
+ * Outputs [q, l] row-major: node_index / edge_index int32 (ids + 1, 0 = padding),
+ * dt32 = float(t_q - ts) rounded from the fp64 difference, dt64 the exact fp64 delta
+ * (either may be NULL), valid_len[q] int32 (target_row = valid_len - 1).
+ * ids must satisfy num_nodes < 2^31 - 1 and edge_id + 1, self_edge_index < 2^31, else
+ * TGFX_EUNSUPPORTED (use the _device variant with TGFX_INDEX64). */
+int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                         int64_t q, int64_t k, int strategy, uint64_t seed,
+                         uint64_t stream_base, int64_t l, int64_t self_edge_index,
+                         int32_t* node_index, int32_t* edge_index, float* dt32, double* dt64,
+                         int32_t* valid_len);
+/* device variant; with TGFX_INDEX64 the node_index / edge_index / valid_len pointers are
+ * int64_t* (the reference's SequenceBatch types). */
+int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                const double* d_times, int64_t q, int64_t k, int strategy,
+                                uint64_t seed, uint64_t stream_base, int64_t l,
+                                int64_t self_edge_index, void* d_node_index, void* d_edge_index,
+                                float* d_dt32, double* d_dt64, void* d_valid_len, void* stream,
+                                unsigned flags);
+
+/* 2-hop composition (not in the reference): hop-1 = sample_batch(roots,
+ * k1) rows [q, l]; hop-2 rows [q, k1, l]: slot j of root r holds the row of the query
+ * (nbr_j, ts_j) of hop-1 entry j (recent-k2, or sample_random(seed2, stream = r*k1 + j));
+ * absent slots are all zero with valid_len 0. */
+int tgfx_sample_two_hop_device(const tgfx_graph* g, const int64_t* d_roots,
+                               const double* d_times, int64_t q, int64_t k1, int64_t k2,
+                               int strategy, uint64_t seed, uint64_t seed2, int64_t l,
+                               int64_t self_edge_index, int32_t* d_hop1_node,
+                               int32_t* d_hop1_edge, float* d_hop1_dt, int32_t* d_hop1_len,
+                               int32_t* d_hop2_node, int32_t* d_hop2_edge, float* d_hop2_dt,
+                               int32_t* d_hop2_len, void* stream, unsigned flags);
+int tgfx_sample_two_hop(const tgfx_graph* g, const int64_t* roots, const double* times,
+                        int64_t q, int64_t k1, int64_t k2, int strategy, uint64_t seed,
+                        uint64_t seed2, int64_t l, int64_t self_edge_index,
+                        int32_t* hop1_node, int32_t* hop1_edge, float* hop1_dt,
+                        int32_t* hop1_len, int32_t* hop2_node, int32_t* hop2_edge,
+                        float* hop2_dt, int32_t* hop2_len);
+
+/* ---------------------------------------------------------------- sequences */
+/* replaces tgf::build_sequence_batch (sequence.hpp:45-46, sequence.cpp:55-86) over padded
+ * samples [q, kpad] (counts[q] valid entries each), in the reference's types. */
+int tgfx_assemble(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
+                  const int64_t* eid, const double* ts, const int64_t* query_nodes,
+                  const double* query_times, int64_t l, int64_t self_edge_index,
+                  int64_t* node_index, int64_t* edge_index, double* time_delta,
+                  int64_t* valid_len, int64_t* target_row);
+/* replaces tgf::build_mask (sequence.hpp:50, sequence.cpp:93-111): (q*l) x l doubles */
+int tgfx_build_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
+                    int kind, double* mask);
+
+/* ---------------------------------------------------------------- synthetic inputs */
+/* bit-identical to tgf::make_random_stream (synthetic.hpp:17-18, synthetic.cpp:12-43);
+ * the Zipf CDF is computed on the host with glibc pow as the reference does. */
+int tgfx_make_random_stream(int64_t num_edges, int64_t num_nodes, uint64_t seed,
+                            double zipf_exponent, tgfx_event* out);
+int tgfx_make_random_stream_device(int64_t num_edges, int64_t num_nodes, uint64_t seed,
+                                   double zipf_exponent, tgfx_event* d_out, void* stream);
+/* forward_concat query layout (training.cpp:193-209) for events [e0, e1): per batch of B
+ * events [src | dst | neg], neg_i = CounterRng(neg_seed, i).next_below(num_nodes)
+ * (index-keyed, metrics.cpp:68-69).  Writes 3*(e1-e0) queries. */
+int tgfx_make_queries_device(const tgfx_event* d_events, int64_t e0, int64_t e1,
+                             int64_t batch, int64_t num_nodes, uint64_t neg_seed,
+                             int64_t* d_nodes, double* d_times, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGFX_H */

@@ -1,0 +1,620 @@
+// api.cu -- the extern "C" boundary (include/tgfx.h): argument checks with the reference's
+// error texts, host<->device staging for the synchronous host-buffer calls, and the
+// process-wide runtime bits (thread-local error, launch counter, stream-ordered pool).
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "graph.cuh"
+
+namespace tgfx {
+
+namespace {
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int64_t> g_bytes{0};
+}  // namespace
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation)
+    throw Error(TGFX_ENOMEM, std::string("out of device memory (") + what + ")");
+  throw Error(TGFX_ECUDA, std::string(cudaGetErrorString(e)) + " (" + what + ")");
+}
+
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+void after_launch(const char* name) {
+  count_launch();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error(TGFX_ECUDA, std::string("launch of ") + name + " failed: " + cudaGetErrorString(e));
+}
+
+const DeviceInfo& device_info() {
+  static thread_local DeviceInfo info;
+  static thread_local int cached_dev = -1;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev != cached_dev) {
+    cudaDeviceProp p;
+    check_cuda(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+    if (p.major < 10)
+      throw Error(TGFX_ECUDA, std::string("libtgfx needs an sm_100 device, found ") + p.name);
+    info.device = dev;
+    info.sms = p.multiProcessorCount;
+    info.smem_optin = p.sharedMemPerBlockOptin;
+    // keep freed pool memory cached so repeated builds/samples do not return it to the OS
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cached_dev = dev;
+  }
+  return info;
+}
+
+void* dmalloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+  return p;
+}
+
+void dfree(void* p, cudaStream_t s) {
+  if (p) check_cuda(cudaFreeAsync(p, s), "cudaFreeAsync");
+}
+
+namespace {
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (const Error* te = dynamic_cast<const Error*>(&e)) return te->code;
+  if (dynamic_cast<const std::bad_alloc*>(&e)) return TGFX_ENOMEM;
+  return TGFX_ECUDA;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TGFX_OK;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// RAII device buffer on a stream
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DBuf(size_t bytes, cudaStream_t st) : s(st) { p = dmalloc(bytes, s); }
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+  if (bytes) TGFX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+}
+void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+  if (bytes && h) TGFX_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+}
+
+void check_graph(const tgfx_graph* g) {
+  if (!g) throw Error(TGFX_EVALIDATION, "null graph");
+}
+
+void check_k(int64_t k) {
+  if (k < 1) throw Error(TGFX_EVALIDATION, "k must be at least 1");  // sampler.cpp:25
+}
+
+void check_l(int64_t l) {
+  if (l < 2) throw Error(TGFX_EVALIDATION, "sequence length must be at least 2");  // sequence.cpp:57
+}
+
+void check_queries(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64_t k,
+                   cudaStream_t s) {
+  // sampler.cpp:88-93: every query validated before any sampling (node first, then k)
+  if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
+  if (q == 0) return;
+  // first failing check in query order: query 0's node, then k (checked with query 0)
+  const int64_t bad = find_bad_query(g, d_nodes, k < 1 ? 1 : q, s);
+  if (bad >= 0) {
+    int64_t u = 0;
+    TGFX_CUDA(cudaMemcpyAsync(&u, d_nodes + bad, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    throw Error(TGFX_EVALIDATION, "query node " + std::to_string(u) + " out of range");
+  }
+  check_k(k);
+}
+
+void check_int32_outputs(const tgfx_graph* g, int64_t self_edge_index) {
+  const int64_t lim = INT32_MAX;
+  if (g->V >= lim || g->max_eid + 1 > lim || g->min_eid + 1 < INT32_MIN ||
+      self_edge_index > lim || self_edge_index < INT32_MIN)
+    throw Error(TGFX_EUNSUPPORTED,
+                "ids do not fit int32 outputs (use tgfx_sample_assemble_device with TGFX_INDEX64)");
+}
+
+tgfx_graph* new_graph(int64_t n, int64_t V, int reverse, cudaStream_t s) {
+  if (n < 0) throw Error(TGFX_EVALIDATION, "negative event count");
+  if (V < 0) throw Error(TGFX_EVALIDATION, "negative num_nodes");
+  const DeviceInfo& di = device_info();
+  tgfx_graph* g = new tgfx_graph();
+  g->device = di.device;
+  g->V = V;
+  g->n = n;
+  g->reverse = reverse ? 1 : 0;
+  try {
+    graph_alloc(g, s);
+  } catch (...) {
+    graph_release(g);
+    delete g;
+    throw;
+  }
+  g_bytes.fetch_add(static_cast<int64_t>(sizeof(int64_t) * (V + 1) + 24 * g->m));
+  return g;
+}
+
+void free_graph(tgfx_graph* g) {
+  if (!g) return;
+  g_bytes.fetch_sub(static_cast<int64_t>(sizeof(int64_t) * (g->V + 1) + 24 * g->m));
+  graph_release(g);
+  delete g;
+}
+
+int build_host(const tgfx_event* events, int64_t n, int64_t V, int reverse, tgfx_graph** out) {
+  tgfx_graph* g = nullptr;
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    cudaStream_t s = 0;
+    device_info();
+    DBuf dev(sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 1)), s);
+    h2d(dev.p, events, sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 0)), s);
+    g = new_graph(n, V, reverse, s);
+    try {
+      build_graph(g, dev.as<tgfx_event>(), s, false);
+      TGFX_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+}  // namespace
+}  // namespace tgfx
+
+using namespace tgfx;
+
+extern "C" {
+
+const char* tgfx_last_error(void) { return g_err.c_str(); }
+int tgfx_abi_version(void) { return TGFX_ABI_VERSION; }
+uint64_t tgfx_launch_count(void) { return g_launches.load(); }
+int64_t tgfx_device_bytes(void) { return g_bytes.load(); }
+
+int tgfx_build_sequential(const tgfx_event* events, int64_t n, int64_t num_nodes, int reverse,
+                          tgfx_graph** out) {
+  return build_host(events, n, num_nodes, reverse, out);
+}
+
+int tgfx_build_parallel(const tgfx_event* events, int64_t n, int64_t num_nodes, int reverse,
+                        int num_threads, tgfx_graph** out) {
+  if (num_threads < 1) {  // tcsr.cpp:108
+    g_err = "num_threads must be at least 1";
+    if (out) *out = nullptr;
+    return TGFX_EVALIDATION;
+  }
+  return build_host(events, n, num_nodes, reverse, out);
+}
+
+int tgfx_build_device(const tgfx_event* d_events, int64_t n, int64_t num_nodes, int reverse,
+                      void* stream, unsigned flags, tgfx_graph** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    cudaStream_t s = as_stream(stream);
+    tgfx_graph* g = new_graph(n, num_nodes, reverse, s);
+    try {
+      build_graph(g, d_events, s, (flags & TGFX_TRUSTED) != 0);
+      if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tgfx_rebuild_device(tgfx_graph* g, const tgfx_event* d_events, void* stream, unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = as_stream(stream);
+    build_graph(g, d_events, s, (flags & TGFX_TRUSTED) != 0);
+    if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_graph_from_host(int64_t num_nodes, int64_t num_edges, int reverse, int64_t m,
+                         const int64_t* indptr, const int64_t* nbr, const int64_t* eid,
+                         const double* ts, tgfx_graph** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    if (m != num_edges * (reverse ? 2 : 1))
+      throw Error(TGFX_EVALIDATION, "column arrays disagree in length");
+    cudaStream_t s = 0;
+    tgfx_graph* g = new_graph(num_edges, num_nodes, reverse, s);
+    try {
+      h2d(g->indptr, indptr, sizeof(int64_t) * (num_nodes + 1), s);
+      h2d(g->nbr, nbr, sizeof(int64_t) * m, s);
+      h2d(g->eid, eid, sizeof(int64_t) * m, s);
+      h2d(g->ts, ts, sizeof(double) * m, s);
+      int64_t mx = -1, mn = 0;
+      for (int64_t i = 0; i < m; ++i) {
+        mx = i == 0 ? eid[i] : std::max(mx, eid[i]);
+        mn = i == 0 ? eid[i] : std::min(mn, eid[i]);
+      }
+      g->max_eid = mx;
+      g->min_eid = mn;
+      TGFX_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tgfx_graph_info(const tgfx_graph* g, int64_t* num_nodes, int64_t* num_edges,
+                    int64_t* num_entries, int* reverse) {
+  return guarded([&] {
+    check_graph(g);
+    if (num_nodes) *num_nodes = g->V;
+    if (num_edges) *num_edges = g->n;
+    if (num_entries) *num_entries = g->m;
+    if (reverse) *reverse = g->reverse;
+  });
+}
+
+int tgfx_graph_build_path(const tgfx_graph* g) { return g ? g->path : -1; }
+
+int tgfx_graph_export(const tgfx_graph* g, int64_t* indptr, int64_t* nbr, int64_t* eid,
+                      double* ts) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = 0;
+    d2h(indptr, g->indptr, sizeof(int64_t) * (g->V + 1), s);
+    d2h(nbr, g->nbr, sizeof(int64_t) * g->m, s);
+    d2h(eid, g->eid, sizeof(int64_t) * g->m, s);
+    d2h(ts, g->ts, sizeof(double) * g->m, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_graph_device_arrays(const tgfx_graph* g, const int64_t** indptr, const int64_t** nbr,
+                             const int64_t** eid, const double** ts) {
+  return guarded([&] {
+    check_graph(g);
+    if (indptr) *indptr = g->indptr;
+    if (nbr) *nbr = g->nbr;
+    if (eid) *eid = g->eid;
+    if (ts) *ts = g->ts;
+  });
+}
+
+int tgfx_graph_validate(const tgfx_graph* g) {
+  return guarded([&] {
+    check_graph(g);
+    const std::string msg = validate_graph(g, 0);
+    if (!msg.empty()) throw Error(TGFX_EVALIDATION, msg);
+  });
+}
+
+int tgfx_graph_free(tgfx_graph* g) {
+  return guarded([&] { free_graph(g); });
+}
+
+int tgfx_sample_batch(const tgfx_graph* g, const int64_t* nodes, const double* times, int64_t q,
+                      int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
+                      int64_t* counts, int64_t* nbr, int64_t* eid, double* ts) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
+    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
+    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
+    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
+    check_queries(g, dn.as<int64_t>(), q, k, s);
+    if (q == 0) return;
+    const size_t qk = qb * static_cast<size_t>(k);
+    DBuf dc(sizeof(int64_t) * qb, s), en(sizeof(int64_t) * qk, s), ee(sizeof(int64_t) * qk, s),
+        et(sizeof(double) * qk, s);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = dn.as<int64_t>();
+    a.times = dt.as<double>();
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.counts = dc.as<int64_t>();
+    a.e_nbr = en.as<int64_t>();
+    a.e_eid = ee.as<int64_t>();
+    a.e_ts = et.as<double>();
+    launch_sample(a, s);
+    d2h(counts, dc.p, sizeof(int64_t) * q, s);
+    d2h(nbr, en.p, sizeof(int64_t) * q * k, s);
+    d2h(eid, ee.p, sizeof(int64_t) * q * k, s);
+    d2h(ts, et.p, sizeof(double) * q * k, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_sample_batch_device(const tgfx_graph* g, const int64_t* d_nodes, const double* d_times,
+                             int64_t q, int64_t k, int strategy, uint64_t seed,
+                             uint64_t stream_base, int64_t* d_counts, int64_t* d_nbr,
+                             int64_t* d_eid, double* d_ts, void* stream, unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = as_stream(stream);
+    if (!(flags & TGFX_TRUSTED)) check_queries(g, d_nodes, q, k, s);
+    check_k(k);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = d_nodes;
+    a.times = d_times;
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.counts = d_counts;
+    a.e_nbr = d_nbr;
+    a.e_eid = d_eid;
+    a.e_ts = d_ts;
+    launch_sample(a, s);
+    if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                const double* d_times, int64_t q, int64_t k, int strategy,
+                                uint64_t seed, uint64_t stream_base, int64_t l,
+                                int64_t self_edge_index, void* d_node_index, void* d_edge_index,
+                                float* d_dt32, double* d_dt64, void* d_valid_len, void* stream,
+                                unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = as_stream(stream);
+    if (!(flags & TGFX_TRUSTED)) check_queries(g, d_nodes, q, k, s);
+    check_k(k);
+    check_l(l);
+    const bool i64 = (flags & TGFX_INDEX64) != 0;
+    if (!i64) check_int32_outputs(g, self_edge_index);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = d_nodes;
+    a.times = d_times;
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.l = l;
+    a.self_edge_index = self_edge_index;
+    a.node_index = d_node_index;
+    a.edge_index = d_edge_index;
+    a.dt32 = d_dt32;
+    a.dt64 = d_dt64;
+    a.valid_len = d_valid_len;
+    a.index64 = i64;
+    launch_sample(a, s);
+    if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                         int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
+                         int64_t l, int64_t self_edge_index, int32_t* node_index,
+                         int32_t* edge_index, float* dt32, double* dt64, int32_t* valid_len) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
+    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
+    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
+    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
+    check_queries(g, dn.as<int64_t>(), q, k, s);
+    check_l(l);
+    check_int32_outputs(g, self_edge_index);
+    if (q == 0) return;
+    const size_t ql = qb * static_cast<size_t>(l);
+    DBuf on(sizeof(int32_t) * ql, s), oe(sizeof(int32_t) * ql, s), ov(sizeof(int32_t) * qb, s);
+    DBuf o32(dt32 ? sizeof(float) * ql : 16, s), o64(dt64 ? sizeof(double) * ql : 16, s);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = dn.as<int64_t>();
+    a.times = dt.as<double>();
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.l = l;
+    a.self_edge_index = self_edge_index;
+    a.node_index = on.p;
+    a.edge_index = oe.p;
+    a.dt32 = dt32 ? o32.as<float>() : nullptr;
+    a.dt64 = dt64 ? o64.as<double>() : nullptr;
+    a.valid_len = ov.p;
+    launch_sample(a, s);
+    d2h(node_index, on.p, sizeof(int32_t) * q * l, s);
+    d2h(edge_index, oe.p, sizeof(int32_t) * q * l, s);
+    d2h(dt32, o32.p, dt32 ? sizeof(float) * q * l : 0, s);
+    d2h(dt64, o64.p, dt64 ? sizeof(double) * q * l : 0, s);
+    d2h(valid_len, ov.p, sizeof(int32_t) * q, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_sample_two_hop_device(const tgfx_graph* g, const int64_t* d_roots, const double* d_times,
+                               int64_t q, int64_t k1, int64_t k2, int strategy, uint64_t seed,
+                               uint64_t seed2, int64_t l, int64_t self_edge_index,
+                               int32_t* d_hop1_node, int32_t* d_hop1_edge, float* d_hop1_dt,
+                               int32_t* d_hop1_len, int32_t* d_hop2_node, int32_t* d_hop2_edge,
+                               float* d_hop2_dt, int32_t* d_hop2_len, void* stream,
+                               unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = as_stream(stream);
+    if (!(flags & TGFX_TRUSTED)) check_queries(g, d_roots, q, k1, s);
+    check_k(k1);
+    check_k(k2);
+    check_l(l);
+    check_int32_outputs(g, self_edge_index);
+    launch_two_hop(g, d_roots, d_times, q, k1, k2, strategy, seed, seed2, l, self_edge_index,
+                   d_hop1_node, d_hop1_edge, d_hop1_dt, d_hop1_len, d_hop2_node, d_hop2_edge,
+                   d_hop2_dt, d_hop2_len, s);
+    if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_sample_two_hop(const tgfx_graph* g, const int64_t* roots, const double* times, int64_t q,
+                        int64_t k1, int64_t k2, int strategy, uint64_t seed, uint64_t seed2,
+                        int64_t l, int64_t self_edge_index, int32_t* hop1_node,
+                        int32_t* hop1_edge, float* hop1_dt, int32_t* hop1_len,
+                        int32_t* hop2_node, int32_t* hop2_edge, float* hop2_dt,
+                        int32_t* hop2_len) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
+    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
+    h2d(dn.p, roots, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
+    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
+    check_queries(g, dn.as<int64_t>(), q, k1, s);
+    check_k(k2);
+    check_l(l);
+    check_int32_outputs(g, self_edge_index);
+    if (q == 0) return;
+    const size_t n1 = qb * l, n2 = qb * k1 * l, c2 = qb * k1;
+    DBuf a(4 * n1, s), b(4 * n1, s), c(4 * n1, s), d(4 * qb, s);
+    DBuf e(4 * n2, s), f(4 * n2, s), h(4 * n2, s), i(4 * c2, s);
+    launch_two_hop(g, dn.as<int64_t>(), dt.as<double>(), q, k1, k2, strategy, seed, seed2, l,
+                   self_edge_index, a.as<int32_t>(), b.as<int32_t>(), c.as<float>(),
+                   d.as<int32_t>(), e.as<int32_t>(), f.as<int32_t>(), h.as<float>(),
+                   i.as<int32_t>(), s);
+    d2h(hop1_node, a.p, 4 * q * l, s);
+    d2h(hop1_edge, b.p, 4 * q * l, s);
+    d2h(hop1_dt, c.p, 4 * q * l, s);
+    d2h(hop1_len, d.p, 4 * q, s);
+    d2h(hop2_node, e.p, 4 * q * k1 * l, s);
+    d2h(hop2_edge, f.p, 4 * q * k1 * l, s);
+    d2h(hop2_dt, h.p, 4 * q * k1 * l, s);
+    d2h(hop2_len, i.p, 4 * q * k1, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_assemble(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
+                  const int64_t* eid, const double* ts, const int64_t* query_nodes,
+                  const double* query_times, int64_t l, int64_t self_edge_index,
+                  int64_t* node_index, int64_t* edge_index, double* time_delta,
+                  int64_t* valid_len, int64_t* target_row) {
+  return guarded([&] {
+    check_l(l);
+    if (q < 0 || kpad < 0) throw Error(TGFX_EVALIDATION, "bad batch shape");
+    for (int64_t b = 0; b < q; ++b)
+      if (counts[b] < 0 || counts[b] > kpad) throw Error(TGFX_EVALIDATION, "bad sample count");
+    if (q == 0) return;
+    device_info();
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(q), qk = qb * std::max<int64_t>(kpad, 1),
+                 ql = qb * static_cast<size_t>(l);
+    DBuf c(8 * qb, s), n(8 * qk, s), e(8 * qk, s), t(8 * qk, s), qn(8 * qb, s), qt(8 * qb, s);
+    DBuf on(8 * ql, s), oe(8 * ql, s), od(8 * ql, s), ov(8 * qb, s), orow(8 * qb, s);
+    h2d(c.p, counts, 8 * qb, s);
+    h2d(n.p, nbr, 8 * qb * kpad, s);
+    h2d(e.p, eid, 8 * qb * kpad, s);
+    h2d(t.p, ts, 8 * qb * kpad, s);
+    h2d(qn.p, query_nodes, 8 * qb, s);
+    h2d(qt.p, query_times, 8 * qb, s);
+    launch_assemble_entries(q, kpad, c.as<int64_t>(), n.as<int64_t>(), e.as<int64_t>(),
+                            t.as<double>(), qn.as<int64_t>(), qt.as<double>(), l, self_edge_index,
+                            on.as<int64_t>(), oe.as<int64_t>(), od.as<double>(), ov.as<int64_t>(),
+                            orow.as<int64_t>(), s);
+    d2h(node_index, on.p, 8 * ql, s);
+    d2h(edge_index, oe.p, 8 * ql, s);
+    d2h(time_delta, od.p, 8 * ql, s);
+    d2h(valid_len, ov.p, 8 * qb, s);
+    d2h(target_row, orow.p, 8 * qb, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_build_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
+                    int kind, double* mask) {
+  return guarded([&] {
+    if (kind < 0 || kind > 2) throw Error(TGFX_EVALIDATION, "unknown mask kind");
+    if (q <= 0 || l <= 0) return;
+    device_info();
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(q);
+    DBuf vl(8 * qb, s), tr(8 * qb, s), m(8 * qb * l * l, s);
+    h2d(vl.p, valid_len, 8 * qb, s);
+    h2d(tr.p, target_row, 8 * qb, s);
+    launch_mask(q, l, vl.as<int64_t>(), tr.as<int64_t>(), kind, m.as<double>(), s);
+    d2h(mask, m.p, 8 * qb * l * l, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_make_random_stream(int64_t num_edges, int64_t num_nodes, uint64_t seed,
+                            double zipf_exponent, tgfx_event* out) {
+  return guarded([&] {
+    if (num_edges < 0 || num_nodes < 1) throw Error(TGFX_EVALIDATION, "bad stream dimensions");
+    if (num_edges == 0) return;
+    device_info();
+    cudaStream_t s = 0;
+    DBuf d(sizeof(tgfx_event) * num_edges, s);
+    launch_random_stream(num_edges, num_nodes, seed, zipf_exponent, d.as<tgfx_event>(), s);
+    d2h(out, d.p, sizeof(tgfx_event) * num_edges, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_make_random_stream_device(int64_t num_edges, int64_t num_nodes, uint64_t seed,
+                                   double zipf_exponent, tgfx_event* d_out, void* stream) {
+  return guarded([&] {
+    device_info();
+    launch_random_stream(num_edges, num_nodes, seed, zipf_exponent, d_out, as_stream(stream));
+  });
+}
+
+int tgfx_make_queries_device(const tgfx_event* d_events, int64_t e0, int64_t e1, int64_t batch,
+                             int64_t num_nodes, uint64_t neg_seed, int64_t* d_nodes,
+                             double* d_times, void* stream) {
+  return guarded([&] {
+    device_info();
+    launch_make_queries(d_events, e0, e1, batch, num_nodes, neg_seed, d_nodes, d_times,
+                        as_stream(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// graph.cuh -- the device-resident T-CSR handle and the builder / sampler entry points.
+#pragma once
+
+#include "common.cuh"
+
+// Device-side build diagnostics, written by the histogram pass.
+struct BuildFlags {
+  unsigned long long bad_index;  // min stream index of an event with an endpoint out of range
+  int unsorted;                  // stream is not (t, eid)-non-decreasing (or holds NaN times)
+  int pad;
+  long long max_eid;
+  long long min_eid;
+};
+
+// proj/include/tgformer/tcsr.hpp:20-33 (TCsr), resident on one device.  SoA columns in HBM:
+//   indptr int64[V+1] | nbr int64[m] | eid int64[m] | ts f64[m]   (m = n * (1 + reverse))
+struct tgfx_graph {
+  int device = 0;
+  int64_t V = 0, n = 0, m = 0;
+  int reverse = 1;
+  int path = 0;  // 0 fast presorted, 1 general re-sort, 2 large-V radix
+  int64_t* indptr = nullptr;
+  int64_t* nbr = nullptr;
+  int64_t* eid = nullptr;
+  double* ts = nullptr;
+  int64_t max_eid = -1, min_eid = 0;
+  // build workspace, kept for rebuilds
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  BuildFlags* dflags = nullptr;
+  BuildFlags* hflags = nullptr;  // pinned host mirror
+};
+
+namespace tgfx {
+
+// max num_nodes of the shared-memory (per-chunk cursor) fast path
+int64_t fast_path_max_nodes();
+
+// Allocates the columns of g (V, n, reverse set by caller).
+void graph_alloc(tgfx_graph* g, cudaStream_t s);
+void graph_release(tgfx_graph* g);
+
+// Full build into g from device events; throws tgfx::Error on invalid input.
+void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted);
+
+// TCsr::validate on device (tcsr.cpp:54-81); returns empty string if valid.
+std::string validate_graph(const tgfx_graph* g, cudaStream_t s);
+
+// ------------------------------------------------------------------ sampling
+struct SampleArgs {
+  const tgfx_graph* g;
+  const int64_t* nodes;
+  const double* times;
+  int64_t q, k;
+  int strategy;
+  uint64_t seed, stream_base;
+  // assemble outputs (l > 0)
+  int64_t l = 0;
+  int64_t self_edge_index = 0;
+  void* node_index = nullptr;
+  void* edge_index = nullptr;
+  float* dt32 = nullptr;
+  double* dt64 = nullptr;
+  void* valid_len = nullptr;
+  bool index64 = false;
+  // entries outputs (l == 0): padded [q, k]
+  int64_t* counts = nullptr;
+  int64_t* e_nbr = nullptr;
+  int64_t* e_eid = nullptr;
+  double* e_ts = nullptr;
+  // hop-2 mode: query (nodes, times) given padded [q_roots, k1] with per-root counts
+  const int64_t* hop_counts = nullptr;
+  int64_t hop_k1 = 0;
+};
+
+// first invalid query index (or -1); validates node range on device (sampler.cpp:22-27)
+int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, cudaStream_t s);
+void launch_sample(const SampleArgs& a, cudaStream_t s);
+void launch_two_hop(const tgfx_graph* g, const int64_t* roots, const double* times, int64_t q,
+                    int64_t k1, int64_t k2, int strategy, uint64_t seed, uint64_t seed2,
+                    int64_t l, int64_t self_edge_index, int32_t* h1n, int32_t* h1e, float* h1d,
+                    int32_t* h1l, int32_t* h2n, int32_t* h2e, float* h2d, int32_t* h2l,
+                    cudaStream_t s);
+
+// ------------------------------------------------------------------ sequences / masks
+void launch_assemble_entries(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
+                             const int64_t* eid, const double* ts, const int64_t* qn,
+                             const double* qt, int64_t l, int64_t self_edge_index,
+                             int64_t* node_index, int64_t* edge_index, double* dt,
+                             int64_t* valid_len, int64_t* target_row, cudaStream_t s);
+void launch_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
+                 int kind, double* mask, cudaStream_t s);
+
+// ------------------------------------------------------------------ synthetic
+void launch_random_stream(int64_t E, int64_t V, uint64_t seed, double zipf, tgfx_event* d_out,
+                          cudaStream_t s);
+void launch_make_queries(const tgfx_event* ev, int64_t e0, int64_t e1, int64_t batch, int64_t V,
+                         uint64_t neg_seed, int64_t* nodes, double* times, cudaStream_t s);
+
+// ------------------------------------------------------------------ primitives
+// exclusive scan of n uint32 counts into int64 offsets (out has n+1 entries: out[n] = total)
+void scan_u32_to_i64(const uint32_t* in, int64_t n, int64_t* out, cudaStream_t s);
+
+}  // namespace tgfx

@@ -1,0 +1,538 @@
+// sample.cu -- temporal neighbor sampler fused with the sequence assembler (sm_100a).
+//
+// Replaces sample_batch / sample_recent / sample_random (proj/src/sampler.cpp:16-104) and
+// build_sequence_batch (proj/src/sequence.cpp:55-86) with one kernel per strategy:
+//
+//   * 32 queries per warp.  Each lane runs the strict-before-t search of its own query
+//     (lower_bound over the node's ts slice, sampler.cpp:16-20: #entries with ts < t;
+//     NaN t -> 0).  Thread-per-query searches keep one sector per probe and 32
+//     independent searches in flight per warp (a warp-cooperative k-ary probe would touch
+//     32 sectors per step).
+//   * recent-k: the kept window of the row is contiguous ([lo+m-kb, lo+m), kb =
+//     min(k, m, l-1)), so the warp assembles its 32 rows "slot-parallel": lane s handles
+//     output slot s of the warp's [32 x l] block, so gathers are near-contiguous and every
+//     output store is a fully coalesced run of 32*l elements.
+//   * uniform-k: Floyd's algorithm with the reference's counter RNG (rng.hpp:23-38,
+//     sampler.cpp:66-80), warp-cooperative per query: lane d computes draw d by O(1)
+//     skip-ahead (x_d = mix64(s0 + d*gamma)), collisions are resolved sequentially in d with
+//     one __any_sync per draw, offsets are ranked (distinct) by shuffles, and each lane
+//     writes its entry straight to its sorted column.
+//   * suffix infilling epilogue: ids + 1, self-edge token at column kb, zero padding,
+//     dt = t_q - ts in fp64 then rounded to fp32 (and/or kept as fp64).
+#include <algorithm>
+
+#include "graph.cuh"
+
+namespace tgfx {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ int64_t prefix_end(const double* __restrict__ ts, int64_t lo,
+                                              int64_t n, double t) {
+  // std::lower_bound(ts+lo, ts+lo+n, t) - (ts+lo)
+  int64_t base = lo;
+  while (n > 0) {
+    const int64_t half = n >> 1;
+    const bool lt = __ldg(ts + base + half) < t;
+    base = lt ? base + half + 1 : base;
+    n = lt ? n - half - 1 : half;
+  }
+  return base - lo;
+}
+
+template <typename T>
+__device__ __forceinline__ void st(void* p, int64_t i, T v) {
+  static_cast<T*>(p)[i] = v;
+}
+
+struct QueryIn {
+  const int64_t* nodes;
+  const double* times;
+  const int64_t* hop_counts;  // hop-2 mode: presence of virtual query qq = r*k1 + j
+  int64_t hop_k1;
+};
+
+__device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_t& u, double& t) {
+  if (in.hop_counts) {
+    const int64_t r = q / in.hop_k1, j = q - r * in.hop_k1;
+    if (j >= __ldg(reinterpret_cast<const long long*>(in.hop_counts) + r)) return false;
+  }
+  u = ldg_i64(in.nodes + q);
+  t = ldg_f64(in.times + q);
+  return true;
+}
+
+struct Outs {
+  void* node;   // int32 or int64 [Q*l]
+  void* edge;
+  float* dt32;
+  double* dt64;
+  void* vlen;   // int32 or int64 [Q]
+  int64_t* counts;  // entries mode
+  int64_t* e_nbr;
+  int64_t* e_eid;
+  double* e_ts;
+};
+
+template <bool IDX64>
+__device__ __forceinline__ void write_slot(const Outs& o, int64_t i, int64_t ni, int64_t ei,
+                                           double dt) {
+  if (IDX64) {
+    st<int64_t>(o.node, i, ni);
+    st<int64_t>(o.edge, i, ei);
+  } else {
+    st<int32_t>(o.node, i, static_cast<int32_t>(ni));
+    st<int32_t>(o.edge, i, static_cast<int32_t>(ei));
+  }
+  if (o.dt32) o.dt32[i] = __double2float_rn(dt);
+  if (o.dt64) o.dt64[i] = dt;
+}
+
+template <bool IDX64>
+__device__ __forceinline__ void write_vlen(const Outs& o, int64_t q, int64_t v) {
+  if (IDX64)
+    st<int64_t>(o.vlen, q, v);
+  else
+    st<int32_t>(o.vlen, q, static_cast<int32_t>(v));
+}
+
+// ------------------------------------------------------------------ recent-k
+// ASSEMBLE: rows [Q, l]; else entries [Q, k] + counts.
+template <bool ASSEMBLE, bool IDX64>
+__global__ void __launch_bounds__(kThreads) k_recent(
+    const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, int64_t self_idx, Outs o) {
+  __shared__ int64_t s_start[kWarps][32];
+  __shared__ int64_t s_u[kWarps][32];
+  __shared__ double s_t[kWarps][32];
+  __shared__ int s_kb[kWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int width = ASSEMBLE ? l : static_cast<int>(k);
+  const int64_t ngroups = ceil_div(Q, 32);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const int64_t q = g * 32 + lane;
+    int64_t start = 0, u = 0;
+    double t = 0.0;
+    int kb = -1;  // -1: absent (hop-2 padding) -> zero row, valid_len 0
+    if (q < Q && fetch_query(in, q, u, t)) {
+      const int64_t lo = ldg_i64(indptr + u), hi = ldg_i64(indptr + u + 1);
+      const int64_t m = prefix_end(ts, lo, hi - lo, t);
+      const int64_t take = min(k, m);
+      kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
+      start = lo + m - kb;
+    }
+    if (q < Q) {
+      if (ASSEMBLE)
+        write_vlen<IDX64>(o, q, kb + 1);
+      else
+        o.counts[q] = max(kb, 0);
+    }
+    s_start[warp][lane] = start;
+    s_u[warp][lane] = u;
+    s_t[warp][lane] = t;
+    s_kb[warp][lane] = kb;
+    __syncwarp();
+    const int64_t qbase = g * 32;
+    const int nq = static_cast<int>(min((int64_t)32, Q - qbase));
+    const int total = nq * width;
+    const int64_t obase = qbase * width;
+#pragma unroll 4
+    for (int s = lane; s < total; s += 32) {
+      const int qi = s / width;
+      const int j = s - qi * width;
+      const int kbq = s_kb[warp][qi];
+      if (ASSEMBLE) {
+        int64_t ni = 0, ei = 0;
+        double dt = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          ni = ldg_i64(nbr + p) + 1;
+          ei = ldg_i64(eid + p) + 1;
+          dt = s_t[warp][qi] - ldg_f64(ts + p);
+        } else if (j == kbq) {
+          ni = s_u[warp][qi] + 1;
+          ei = self_idx;
+        }
+        write_slot<IDX64>(o, obase + s, ni, ei, dt);
+      } else {
+        int64_t a = 0, b = 0;
+        double c = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          a = ldg_i64(nbr + p);
+          b = ldg_i64(eid + p);
+          c = ldg_f64(ts + p);
+        }
+        o.e_nbr[obase + s] = a;
+        o.e_eid[obase + s] = b;
+        o.e_ts[obase + s] = c;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ uniform-k (Floyd)
+template <int P, bool ASSEMBLE, bool IDX64>
+__global__ void __launch_bounds__(kThreads) k_random(
+    const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, Outs o) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ngroups = ceil_div(Q, 32);
+  const int kk = static_cast<int>(k);
+  const uint64_t seed_mix = mix64(seed);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const int64_t q = g * 32 + lane;
+    int64_t lo = 0, m = 0, u = 0;
+    double t = 0.0;
+    bool present = false;
+    if (q < Q && fetch_query(in, q, u, t)) {
+      present = true;
+      lo = ldg_i64(indptr + u);
+      const int64_t hi = ldg_i64(indptr + u + 1);
+      m = prefix_end(ts, lo, hi - lo, t);
+    }
+    const int nq = static_cast<int>(min((int64_t)32, Q - g * 32));
+    for (int qi = 0; qi < nq; ++qi) {
+      const int64_t qq = g * 32 + qi;
+      const bool pr = __shfl_sync(kFull, present, qi);
+      const int64_t qlo = __shfl_sync(kFull, lo, qi);
+      const int64_t qm = __shfl_sync(kFull, m, qi);
+      const int64_t qu = __shfl_sync(kFull, u, qi);
+      const double qt = __shfl_sync(kFull, t, qi);
+      if (ASSEMBLE) {
+        if (!pr) {
+          for (int j = lane; j < l; j += 32) write_slot<IDX64>(o, qq * l + j, 0, 0, 0.0);
+          if (lane == 0) write_vlen<IDX64>(o, qq, 0);
+          continue;
+        }
+      }
+      if (qm <= k) {
+        // whole prefix (sampler.cpp:59-63): contiguous
+        if (ASSEMBLE) {
+          const int kb = static_cast<int>(min(qm, (int64_t)(l - 1)));
+          const int64_t start = qlo + qm - kb;
+          for (int j = lane; j < l; j += 32) {
+            int64_t ni = 0, ei = 0;
+            double dt = 0.0;
+            if (j < kb) {
+              ni = ldg_i64(nbr + start + j) + 1;
+              ei = ldg_i64(eid + start + j) + 1;
+              dt = qt - ldg_f64(ts + start + j);
+            } else if (j == kb) {
+              ni = qu + 1;
+              ei = self_idx;
+            }
+            write_slot<IDX64>(o, qq * l + j, ni, ei, dt);
+          }
+          if (lane == 0) write_vlen<IDX64>(o, qq, kb + 1);
+        } else {
+          for (int j = lane; j < kk; j += 32) {
+            const bool h = j < qm;
+            o.e_nbr[qq * k + j] = h ? ldg_i64(nbr + qlo + j) : 0;
+            o.e_eid[qq * k + j] = h ? ldg_i64(eid + qlo + j) : 0;
+            o.e_ts[qq * k + j] = h ? ldg_f64(ts + qlo + j) : 0.0;
+          }
+          if (lane == 0) o.counts[qq] = qm;
+        }
+        continue;
+      }
+      // Floyd: for d = 0..k-1, i_d = m-k+d, j_d = next_below(i_d+1); c_d = j_d unless already
+      // chosen, then i_d.  Draws are independent of the resolution (one draw per iteration).
+      const uint64_t s0 = mix64(seed_mix ^ ((stream_base + static_cast<uint64_t>(qq)) * kStreamMul));
+      int64_t jd[P], c[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int d = p * 32 + lane;
+        const uint64_t bound = static_cast<uint64_t>(qm - kk + d) + 1;
+        jd[p] = d < kk ? static_cast<int64_t>(mulhi64(rng_draw(s0, d), bound)) : -1;
+        c[p] = -1;
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        for (int o2 = 0; o2 < 32; ++o2) {
+          const int d = p * 32 + o2;
+          if (d >= kk) break;
+          const int64_t jv = __shfl_sync(kFull, jd[p], o2);
+          bool hit = false;
+#pragma unroll
+          for (int p2 = 0; p2 <= p; ++p2) hit |= (p2 < p || lane < o2) && c[p2] == jv;
+          hit = __any_sync(kFull, hit);
+          if (lane == o2) c[p] = hit ? (qm - kk + d) : jv;
+        }
+      }
+      // ranks (offsets are distinct)
+      int rank[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) rank[p] = 0;
+#pragma unroll
+      for (int p2 = 0; p2 < P; ++p2) {
+        for (int o2 = 0; o2 < 32; ++o2) {
+          if (p2 * 32 + o2 >= kk) break;
+          const int64_t v = __shfl_sync(kFull, c[p2], o2);
+#pragma unroll
+          for (int p = 0; p < P; ++p) rank[p] += v < c[p];
+        }
+      }
+      if (ASSEMBLE) {
+        const int kb = min(kk, l - 1);
+        const int drop = kk - kb;  // keep the most recent l-1 (sequence.cpp:70-71)
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int d = p * 32 + lane;
+          if (d < kk && rank[p] >= drop) {
+            const int64_t pos = qlo + c[p];
+            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ldg_i64(nbr + pos) + 1,
+                              ldg_i64(eid + pos) + 1, qt - ldg_f64(ts + pos));
+          }
+        }
+        for (int j = kb + lane; j < l; j += 32) {
+          if (j == kb)
+            write_slot<IDX64>(o, qq * l + j, qu + 1, self_idx, 0.0);
+          else
+            write_slot<IDX64>(o, qq * l + j, 0, 0, 0.0);
+        }
+        if (lane == 0) write_vlen<IDX64>(o, qq, kb + 1);
+      } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int d = p * 32 + lane;
+          if (d < kk) {
+            const int64_t pos = qlo + c[p];
+            o.e_nbr[qq * k + rank[p]] = ldg_i64(nbr + pos);
+            o.e_eid[qq * k + rank[p]] = ldg_i64(eid + pos);
+            o.e_ts[qq * k + rank[p]] = ldg_f64(ts + pos);
+          }
+        }
+        if (lane == 0) o.counts[qq] = kk;
+      }
+    }
+  }
+}
+
+__global__ void k_find_bad(const int64_t* __restrict__ nodes, int64_t q, int64_t V,
+                           unsigned long long* first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = nodes[i];
+    if (u < 0 || u >= V) atomicMin(first, (unsigned long long)i);
+  }
+}
+
+// build_sequence_batch over padded samples, reference types (sequence.cpp:55-86)
+__global__ void k_assemble_entries(int64_t q, int64_t kpad, const int64_t* __restrict__ counts,
+                                   const int64_t* __restrict__ nbr, const int64_t* __restrict__ eid,
+                                   const double* __restrict__ ts, const int64_t* __restrict__ qn,
+                                   const double* __restrict__ qt, int64_t l, int64_t self_idx,
+                                   int64_t* node_index, int64_t* edge_index, double* dt,
+                                   int64_t* valid_len, int64_t* target_row) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q * l;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / l, j = i - b * l;
+    const int64_t total = counts[b];
+    const int64_t kb = min(total, l - 1);
+    const int64_t skip = total - kb;
+    int64_t ni = 0, ei = 0;
+    double d = 0.0;
+    if (j < kb) {
+      const int64_t s = b * kpad + skip + j;
+      ni = nbr[s] + 1;
+      ei = eid[s] + 1;
+      d = qt[b] - ts[s];
+    } else if (j == kb) {
+      ni = qn[b] + 1;
+      ei = self_idx;
+      valid_len[b] = kb + 1;
+      target_row[b] = kb;
+    }
+    node_index[i] = ni;
+    edge_index[i] = ei;
+    dt[i] = d;
+  }
+}
+
+// build_mask (sequence.cpp:93-111): (q*l) x l of {0, -inf}
+__global__ void k_mask(int64_t q, int64_t l, const int64_t* __restrict__ valid_len,
+                       const int64_t* __restrict__ target_row, int kind, double* mask) {
+  const int64_t total = q * l * l;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / l, col = i - row * l;
+    const int64_t b = row / l, r = row - b * l;
+    const int64_t len = valid_len[b], kq = target_row[b];
+    int64_t hi = 0;
+    if (kind == TGFX_MASK_CAUSAL)
+      hi = min(r + 1, len);
+    else if (r == kq)
+      hi = kind == TGFX_MASK_SELF_LOOP ? kq + 1 : kq;
+    mask[i] = col < hi ? 0.0 : __longlong_as_double(0xfff0000000000000LL);  // -inf
+  }
+}
+
+int grid_groups(int64_t Q) {
+  const int64_t groups = ceil_div(std::max<int64_t>(Q, 1), 32);
+  const int64_t blocks = ceil_div(groups, kWarps);
+  return static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(device_info().sms) * 8));
+}
+
+template <bool ASM, bool I64>
+void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& o, int grid,
+                     cudaStream_t s) {
+  const tgfx_graph* g = a.g;
+  const int l = static_cast<int>(a.l);
+#define TGFX_RANDOM_CASE(PP)                                                                 \
+  case PP:                                                                                   \
+    k_random<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q, \
+                                                     a.k, l, a.self_edge_index, a.seed,      \
+                                                     a.stream_base, o);                     \
+    break;
+  switch (P) {
+    TGFX_RANDOM_CASE(1)
+    TGFX_RANDOM_CASE(2)
+    TGFX_RANDOM_CASE(4)
+    TGFX_RANDOM_CASE(8)
+    default: throw Error(TGFX_EUNSUPPORTED, "uniform sampling supports k <= 256");
+  }
+#undef TGFX_RANDOM_CASE
+  after_launch("k_random");
+}
+
+}  // namespace
+
+int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, cudaStream_t s) {
+  if (q <= 0) return -1;
+  unsigned long long* first = static_cast<unsigned long long*>(dmalloc(8, s));
+  const unsigned long long init = ~0ull;
+  TGFX_CUDA(cudaMemcpyAsync(first, &init, 8, cudaMemcpyHostToDevice, s));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(q, 256), device_info().sms * 8));
+  k_find_bad<<<grid, 256, 0, s>>>(d_nodes, q, g->V, first);
+  after_launch("k_find_bad");
+  unsigned long long h = 0;
+  TGFX_CUDA(cudaMemcpyAsync(&h, first, 8, cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaStreamSynchronize(s));
+  dfree(first, s);
+  return h == ~0ull ? -1 : static_cast<int64_t>(h);
+}
+
+void launch_sample(const SampleArgs& a, cudaStream_t s) {
+  if (a.q <= 0) return;
+  const tgfx_graph* g = a.g;
+  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1};
+  Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
+         a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
+  const int grid = grid_groups(a.q);
+  const bool assemble = a.l > 0;
+  const int l = static_cast<int>(a.l);
+  if (a.strategy == TGFX_RECENT) {
+    if (assemble) {
+      if (a.index64)
+        k_recent<true, true><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
+                                                       a.k, l, a.self_edge_index, o);
+      else
+        k_recent<true, false><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
+                                                        a.k, l, a.self_edge_index, o);
+    } else {
+      k_recent<false, false><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
+                                                       a.k, 0, 0, o);
+    }
+    after_launch("k_recent");
+    return;
+  }
+  const int P = a.k <= 32 ? 1 : a.k <= 64 ? 2 : a.k <= 128 ? 4 : a.k <= 256 ? 8 : 0;
+  if (assemble) {
+    if (a.index64)
+      launch_random_p<true, true>(P, a, in, o, grid, s);
+    else
+      launch_random_p<true, false>(P, a, in, o, grid, s);
+  } else {
+    launch_random_p<false, false>(P, a, in, o, grid, s);
+  }
+}
+
+void launch_two_hop(const tgfx_graph* g, const int64_t* roots, const double* times, int64_t q,
+                    int64_t k1, int64_t k2, int strategy, uint64_t seed, uint64_t seed2,
+                    int64_t l, int64_t self_edge_index, int32_t* h1n, int32_t* h1e, float* h1d,
+                    int32_t* h1l, int32_t* h2n, int32_t* h2e, float* h2d, int32_t* h2l,
+                    cudaStream_t s) {
+  if (q <= 0) return;
+  // hop-1 rows
+  SampleArgs a{};
+  a.g = g;
+  a.nodes = roots;
+  a.times = times;
+  a.q = q;
+  a.k = k1;
+  a.strategy = strategy;
+  a.seed = seed;
+  a.stream_base = 0;
+  a.l = l;
+  a.self_edge_index = self_edge_index;
+  a.node_index = h1n;
+  a.edge_index = h1e;
+  a.dt32 = h1d;
+  a.valid_len = h1l;
+  launch_sample(a, s);
+  // hop-1 entries (the hop-2 queries), padded [q, k1]
+  int64_t* cnt = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * q, s));
+  int64_t* en = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * q * k1, s));
+  int64_t* ee = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * q * k1, s));
+  double* et = static_cast<double*>(dmalloc(sizeof(double) * q * k1, s));
+  SampleArgs b = a;
+  b.l = 0;
+  b.node_index = b.edge_index = b.valid_len = nullptr;
+  b.dt32 = nullptr;
+  b.counts = cnt;
+  b.e_nbr = en;
+  b.e_eid = ee;
+  b.e_ts = et;
+  launch_sample(b, s);
+  // hop-2 rows over the q*k1 virtual queries; absent slots -> zero rows, valid_len 0
+  SampleArgs c = a;
+  c.nodes = en;
+  c.times = et;
+  c.q = q * k1;
+  c.k = k2;
+  c.seed = seed2;
+  c.stream_base = 0;  // stream = r*k1 + j
+  c.node_index = h2n;
+  c.edge_index = h2e;
+  c.dt32 = h2d;
+  c.valid_len = h2l;
+  c.hop_counts = cnt;
+  c.hop_k1 = k1;
+  launch_sample(c, s);
+  dfree(cnt, s);
+  dfree(en, s);
+  dfree(ee, s);
+  dfree(et, s);
+}
+
+void launch_assemble_entries(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
+                             const int64_t* eid, const double* ts, const int64_t* qn,
+                             const double* qt, int64_t l, int64_t self_edge_index,
+                             int64_t* node_index, int64_t* edge_index, double* dt,
+                             int64_t* valid_len, int64_t* target_row, cudaStream_t s) {
+  if (q <= 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(q * l, 256), device_info().sms * 8));
+  k_assemble_entries<<<grid, 256, 0, s>>>(q, kpad, counts, nbr, eid, ts, qn, qt, l,
+                                          self_edge_index, node_index, edge_index, dt, valid_len,
+                                          target_row);
+  after_launch("k_assemble_entries");
+}
+
+void launch_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
+                 int kind, double* mask, cudaStream_t s) {
+  if (q <= 0) return;
+  const int grid =
+      static_cast<int>(std::min<int64_t>(ceil_div(q * l * l, 256), device_info().sms * 8));
+  k_mask<<<grid, 256, 0, s>>>(q, l, valid_len, target_row, kind, mask);
+  after_launch("k_mask");
+}
+
+}  // namespace tgfx

@@ -1,0 +1,149 @@
+"""GPU parity: T-CSR build (CUDA, through the C ABI) vs the reference's golden vectors and the
+CPU oracle.  Bit-exact: indptr/nbr/eid int64 equal, ts compared bit-for-bit."""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, events_of
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    from paper_2409_05477_b200 import tgformer
+    return tgformer
+
+
+def assert_same(g, want, tag=""):
+    assert np.array_equal(g.indptr, want["indptr"]), tag
+    assert np.array_equal(g.neighbor_ids, want["nbr"]), tag
+    assert np.array_equal(g.edge_ids, want["eid"]), tag
+    assert g.timestamps.view(np.uint64).tobytes() == np.asarray(want["ts"]).view(np.uint64).tobytes(), tag
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "build_*.npz"))))
+def test_build_matches_reference_golden(T, path):
+    g = dict(np.load(path))
+    ev = events_of(g["events"])
+    V = int(g["num_nodes"])
+    for rev in (0, 1):
+        want = {k: g[f"rev{rev}_{k}"] for k in ("indptr", "nbr", "eid", "ts")}
+        got = T.build_sequential(T.EventStream(ev, V), bool(rev))
+        assert_same(got, want, (path, rev))
+        got.validate()
+        gp = T.build_parallel(T.EventStream(ev, V), bool(rev), 8)
+        assert_same(gp, want, (path, rev, "parallel"))
+
+
+def test_reference_unit_known_answers(T):
+    """proj/tests/test_tcsr.cpp:50-97"""
+    three = T.EventStream(np.array([(1, 0, 2, 3.0), (2, 1, 2, 4.0), (0, 0, 1, 5.0)],
+                                   dtype=T.EVENT_DTYPE), 3)
+    g = T.build_sequential(three, False)
+    assert g.indptr.tolist() == [0, 2, 3, 3]
+    assert g.timestamps[:2].tolist() == [3.0, 5.0] and g.neighbor_ids[:2].tolist() == [2, 1]
+    g = T.build_sequential(three, True)
+    assert g.num_entries() == 6 and g.indptr.tolist() == [0, 2, 4, 6]
+    assert g.neighbor_ids[4:6].tolist() == [0, 1] and g.timestamps[4:6].tolist() == [3.0, 4.0]
+    sl = T.build_sequential(T.EventStream(np.array([(0, 1, 1, 4.0)], dtype=T.EVENT_DTYPE), 2), True)
+    assert sl.degree(0) == 0 and sl.degree(1) == 2
+    assert sl.edge_ids.tolist() == [0, 0] and sl.neighbor_ids[0] == 1
+    empty = T.build_sequential(T.EventStream(np.zeros(0, T.EVENT_DTYPE), 4), True)
+    assert empty.indptr.tolist() == [0, 0, 0, 0, 0] and empty.num_entries() == 0
+
+
+def test_build_errors_match_reference(T):
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        errs = json.load(f)
+    bad = T.EventStream(np.array([(0, 0, 7, 1.0)], dtype=T.EVENT_DTYPE), 2)
+    with pytest.raises(T.ValidationError, match=errs["bad_endpoint"]):
+        T.build_sequential(bad, False)
+    with pytest.raises(T.ValidationError, match=errs["bad_endpoint"]):
+        T.build_parallel(bad, False, 2)
+    ok = T.EventStream(np.array([(0, 0, 1, 1.0)], dtype=T.EVENT_DTYPE), 2)
+    with pytest.raises(T.ValidationError, match=errs["bad_threads"]):
+        T.build_parallel(ok, True, 0)
+    # first offending event in stream order is reported (check_endpoints, tcsr.cpp:44-50)
+    ev = np.array([(10, 0, 1, 1.0), (11, 0, 9, 2.0), (12, -1, 0, 3.0)], dtype=T.EVENT_DTYPE)
+    with pytest.raises(T.ValidationError, match="event 11 endpoint out of range"):
+        T.build_sequential(T.EventStream(ev, 2), True)
+
+
+def _acceptance_stream(O, i):
+    """proj/tests/acceptance.cpp:44-55 schedule_stream(i)"""
+    if i < 90:
+        n = 1000 + O.mix64(i) % 9000
+        v = 50 + O.mix64(i + 7) % 2000
+        return O.make_random_stream(n, v, 1000 + i), v
+    if i < 98:
+        return O.make_random_stream(100000, 20000, 2000 + i), 20000
+    return O.make_random_stream(1000000, 100000, 3000 + i), 100000
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 17, 45, 89, 90, 97, 98, 99])
+def test_acceptance_schedule_vs_oracle(T, oracle_mod, i):
+    """acceptance `builder` criterion (acceptance.cpp:63-95) on a subset of its schedule:
+    includes the 1e6-edge / 1e5-node streams, which exceed the shared-memory cursor budget and
+    take the large-V path."""
+    ev, v = _acceptance_stream(oracle_mod, i)
+    for rev in (False, True):
+        want = oracle_mod.build(ev, v, rev)
+        got = T.build_sequential(T.EventStream(ev, v), rev)
+        assert_same(got, want, (i, rev))
+        assert got.build_path == (2 if v > 45000 else 0)
+
+
+@pytest.mark.parametrize("V", [700, 120000])
+def test_unsorted_streams_take_the_general_path(T, oracle_mod, V):
+    rng = np.random.default_rng(V)
+    ev = oracle_mod.make_random_stream(60000, V, 77)
+    shuffled = ev[rng.permutation(len(ev))].copy()
+    for rev in (False, True):
+        want = oracle_mod.build(shuffled, V, rev)
+        got = T.build_sequential(T.EventStream(shuffled, V), rev)
+        assert_same(got, want, (V, rev))
+        assert got.build_path == (1 if V <= 45000 else 2)
+
+
+def test_degenerate_shapes(T, oracle_mod):
+    # one node, all self-loops; node ids at the boundary; V much larger than used
+    for ev, V in ((oracle_mod.events_from([0] * 50, [0] * 50, np.arange(50.0)), 1),
+                  (oracle_mod.events_from([4, 0, 4], [0, 4, 4], [1.0, 1.0, 1.0]), 5),
+                  (oracle_mod.events_from([3, 2], [2, 3], [0.0, 0.0]), 45000),
+                  (oracle_mod.events_from([3, 2], [2, 3], [0.0, 0.0]), 45001)):
+        for rev in (False, True):
+            assert_same(T.build_sequential(T.EventStream(ev, V), rev), oracle_mod.build(ev, V, rev))
+
+
+def test_gdelt_shape_prefix_vs_oracle(T, oracle_mod):
+    """GDELT-shaped (V = 16,682, Zipf 1.2) 8M-event prefix: full bit-exact comparison."""
+    ev = oracle_mod.make_random_stream(8_000_000, 16682, 42)
+    want = oracle_mod.build(ev, 16682, True)
+    got = T.build_sequential(T.EventStream(ev, 16682), True)
+    assert_same(got, want)
+
+
+def test_full_gdelt_size_properties():
+    """Full GDELT-shaped build (191,290,882 events, rev=1) on the device: size-independent
+    properties -- validate() (sorted slices, ranges, indptr endpoints), degree histogram equal
+    to a bincount of the endpoints, and the multiset checksum of (nbr, eid) per entry equal to
+    that of the emitted entries."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V = 191_290_882, 16682
+    ev = D.random_stream(E, V, 42)
+    g = D.build(ev, V, True)
+    g.validate()
+    ip, nb, ed, ts = D.graph_tensors(g)
+    raw = ev.view(torch.int64).view(E, 4)
+    deg = torch.bincount(raw[:, 1], minlength=V) + torch.bincount(raw[:, 2], minlength=V)
+    assert torch.equal(torch.diff(ip), deg)
+    # checksum of checksums: per-entry hash summed (order-independent), equal on both sides
+    def h(a, b):
+        return ((a * 0x9E3779B1 + b * 0x85EBCA77) & 0xFFFFFFFF).sum()
+    want = h(raw[:, 2], raw[:, 0]) + h(raw[:, 1], raw[:, 0])
+    assert int(h(nb, ed)) == int(want)

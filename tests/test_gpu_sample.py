@@ -1,0 +1,212 @@
+"""GPU parity: sampler + fused assembler (CUDA via the C ABI) vs the reference's golden vectors
+and the CPU oracle.  Indices bit-exact; fp64 deltas bit-exact; fp32 deltas equal to the fp64
+reference rounded to nearest (|rel err| <= 2^-24 < 1e-6, the north-star tolerance)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6  # north_star: fp32 time deltas within 1e-6 relative
+
+
+@pytest.fixture(scope="module")
+def T():
+    from paper_2409_05477_b200 import tgformer
+    return tgformer
+
+
+def check_rows(got, want, tag=""):
+    """got: int32/fp32 rows (+ optional fp64); want: reference int64/fp64 SequenceBatch."""
+    assert np.array_equal(got["node_index"].astype(np.int64), want["node_index"]), tag
+    assert np.array_equal(got["edge_index"].astype(np.int64), want["edge_index"]), tag
+    assert np.array_equal(got["valid_len"].astype(np.int64), want["valid_len"]), tag
+    ref = want["time_delta"]
+    d32 = got["time_delta"].astype(np.float64)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        err = np.abs(d32 - ref) / np.abs(ref)
+    assert np.all((d32 == ref) | (err <= RTOL)), (tag, float(np.nanmax(err)))
+    assert np.array_equal(got["time_delta"], ref.astype(np.float32)), tag  # fp64->fp32 RN
+    if "time_delta64" in got:
+        assert got["time_delta64"].view(np.uint64).tobytes() == ref.view(np.uint64).tobytes(), tag
+
+
+@pytest.mark.parametrize("name", ["sample_4000_150_31", "sample_3000_40_32"])
+def test_sampler_matches_reference_golden(T, oracle_mod, name):
+    g = golden(name)
+    e, v, seed = (int(x) for x in name.split("_")[1:])
+    stream = T.make_random_stream(e, v, seed)
+    graph = T.build_sequential(stream, True)
+    for strat in ("recent", "random"):
+        for k in (1, 6, 20, 40):
+            for tag, nn, tt in (("rand", g["qn"], g["qt"]), ("event", g["en"], g["et"])):
+                c, nb, ed, ts = T.sample_batch_arrays(graph, nn, tt, k, strat, 9)
+                p = f"{strat}_k{k}_{tag}"
+                assert np.array_equal(c, g[p + "_counts"]), p
+                assert np.array_equal(nb, g[p + "_nbr"]), p
+                assert np.array_equal(ed, g[p + "_eid"]), p
+                assert np.array_equal(ts, g[p + "_ts"]), p
+    for strat, k, l in (("recent", 10, 11), ("random", 20, 21), ("random", 10, 5),
+                        ("recent", 40, 33)):
+        got = T.sample_assemble(graph, g["en"], g["et"], k, strat, 9, l, e + 1, dt64=True)
+        want = {kk: g[f"asm_{strat}_k{k}_l{l}_{kk}"] for kk in
+                ("node_index", "edge_index", "time_delta", "valid_len")}
+        check_rows(got, want, (name, strat, k, l))
+
+
+def test_two_hop_matches_reference_golden(T):
+    g = golden("two_hop_6000_200_51")
+    graph = T.build_sequential(T.make_random_stream(6000, 200, 51), True)
+    for strat in ("recent", "random"):
+        h1, h2 = T.sample_two_hop(graph, g["roots"], g["rtimes"], 10, 10, strat, 9, 11, 6001,
+                                  seed2=0x5eed2)
+        check_rows(h1, {kk: g[f"{strat}_hop1_{kk}"] for kk in
+                        ("node_index", "edge_index", "time_delta", "valid_len")}, strat)
+        q = len(g["roots"])
+        flat = {kk: h2[kk].reshape(q * 10, *h2[kk].shape[2:]) for kk in h2}
+        want = {kk: g[f"{strat}_hop2_{kk}"].reshape(q * 10, *g[f"{strat}_hop2_{kk}"].shape[2:])
+                for kk in ("node_index", "edge_index", "time_delta", "valid_len")}
+        check_rows(flat, want, strat)
+
+
+def test_reference_unit_known_answers(T):
+    """proj/tests/test_sampler.cpp:32-87, 264-272"""
+    ev = np.array([(1, 0, 2, 3.0), (2, 1, 2, 4.0), (0, 0, 1, 5.0)], dtype=T.EVENT_DTYPE)
+    g = T.build_sequential(T.EventStream(ev, 3), False)
+    mid = T.sample_recent(g, 0, 4.0, 5)
+    assert [(e.neighbor, e.timestamp) for e in mid.neighbors] == [(2, 3.0)]
+    assert T.sample_recent(g, 0, 3.0, 5).neighbors == []
+    assert T.sample_recent(g, 0, 0.5, 5).neighbors == []
+    assert [e.timestamp for e in T.sample_recent(g, 0, 99.0, 5).neighbors] == [3.0, 5.0]
+    got = T.sample_recent(g, 0, 5.0, 10)  # strict inequality
+    assert [e.timestamp for e in got.neighbors] == [3.0]
+    for seed in range(20):
+        assert all(e.timestamp < 5.0 for e in T.sample_random(g, 0, 5.0, 1, seed).neighbors)
+    for seed in (0, 7, 123456):
+        assert [e.timestamp for e in T.sample_random(g, 0, 99.0, 5, seed).neighbors] == [3.0, 5.0]
+    ten = np.array([(i, 0, i + 1, float(i)) for i in range(10)], dtype=T.EVENT_DTYPE)
+    g10 = T.build_sequential(T.EventStream(ten, 12), False)
+    assert [e.timestamp for e in T.sample_recent(g10, 0, 100.0, 3).neighbors] == [7.0, 8.0, 9.0]
+
+
+def test_uniformity_over_seeds(T):
+    """proj/tests/test_sampler.cpp:144-165 and acceptance.cpp:120-147 (distributional)."""
+    ev = np.array([(i, 0, i + 1, float(i)) for i in range(100)], dtype=T.EVENT_DTYPE)
+    g = T.build_sequential(T.EventStream(ev, 101), False)
+    seeds = 10000
+    hits = np.zeros(100)
+    # one batch per seed would be slow; stream_base varies the stream instead of the seed, and
+    # a second pass varies the seed with a fixed stream
+    for s in range(0, seeds, 1000):
+        c, nb, ed, ts = T.sample_batch_arrays(g, np.zeros(1000, np.int64), np.full(1000, 1e9),
+                                              10, "random", 12345, stream_base=s)
+        assert (c == 10).all()
+        np.add.at(hits, ed.ravel(), 1)
+    share = hits / (seeds * 10)
+    appear = hits / seeds
+    assert np.abs(share - 0.01).max() <= 0.01 and np.abs(appear - 0.1).max() <= 0.02
+
+
+def test_sampler_errors_match_reference(T):
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        errs = json.load(f)
+    ev = np.array([(1, 0, 2, 3.0), (2, 1, 2, 4.0), (0, 0, 1, 5.0)], dtype=T.EVENT_DTYPE)
+    g = T.build_sequential(T.EventStream(ev, 3), False)
+    with pytest.raises(T.ValidationError, match=errs["bad_node"]):
+        T.sample_recent(g, 99, 1.0, 3)
+    with pytest.raises(T.ValidationError, match=errs["bad_k"]):
+        T.sample_recent(g, 0, 1.0, 0)
+    with pytest.raises(T.ValidationError, match="node and time lists differ in length"):
+        T.sample_batch(g, [0, 1], [1.0], 3)
+    with pytest.raises(T.ValidationError, match=errs["bad_l"]):
+        T.sample_assemble(g, [0], [1.0], 3, "recent", 0, 1, 4)
+    with pytest.raises(T.ValidationError, match="query node -1 out of range"):
+        T.sample_batch(g, [0, 1, -1, 7], [1.0] * 4, 3)
+    with pytest.raises(T.ValidationError):
+        T.parse_strategy("nope")
+
+
+def _workload(O, E, V, seed, batch, n_events=None):
+    ev = O.make_random_stream(E, V, seed)
+    e1 = E if n_events is None else n_events
+    nodes, times = O.make_queries(ev, 0, e1, batch, V)
+    return ev, nodes, times
+
+
+@pytest.mark.parametrize("strat,k,l", [("recent", 10, 11), ("random", 20, 21), ("recent", 1, 2),
+                                       ("random", 64, 33), ("random", 128, 129),
+                                       ("recent", 128, 11), ("random", 200, 40)])
+def test_wikipedia_shape_vs_oracle(T, oracle_mod, strat, k, l):
+    """Config W (9,227 nodes, 157,474 edges) event-derived queries, all events."""
+    ev, nodes, times = _workload(oracle_mod, 157474, 9227, 42, 600)
+    og = oracle_mod.build(ev, 9227, True)
+    graph = T.build_sequential(T.EventStream(ev, 9227), True)
+    for b0 in (0, 200 * 1800):
+        nn, tt = nodes[b0:b0 + 1800 * 20], times[b0:b0 + 1800 * 20]
+        want = oracle_mod.sample_assemble(og, nn, tt, k, strat, 9 + b0, l, 157475,
+                                          stream_base=b0)
+        got = T.sample_assemble(graph, nn, tt, k, strat, 9 + b0, l, 157475, stream_base=b0,
+                                dt64=True)
+        check_rows(got, want, (strat, k, l, b0))
+        cw = oracle_mod.sample_batch(og, nn, tt, k, strat, 9, stream_base=b0)
+        cg = T.sample_batch_arrays(graph, nn, tt, k, strat, 9, stream_base=b0)
+        for a, b in zip(cg, cw):
+            assert np.array_equal(a, b), (strat, k)
+
+
+def test_lastfm_shape_uniform20_vs_oracle(T, oracle_mod):
+    """Config L (1,980 nodes, 1.29M edges, heavy hub): uniform-20, batch 4,000, l = 21."""
+    ev, nodes, times = _workload(oracle_mod, 1293103, 1980, 42, 4000, n_events=40000)
+    og = oracle_mod.build(ev, 1980, True)
+    graph = T.build_sequential(T.EventStream(ev, 1980), True)
+    for b in range(0, 10):  # 10 batches of 12,000 queries, seed 9 + b, stream = index in batch
+        nn, tt = nodes[b * 12000:(b + 1) * 12000], times[b * 12000:(b + 1) * 12000]
+        want = oracle_mod.sample_assemble(og, nn, tt, 20, "random", 9 + b, 21, 1293104)
+        got = T.sample_assemble(graph, nn, tt, 20, "random", 9 + b, 21, 1293104, dt64=True)
+        check_rows(got, want, b)
+
+
+def test_edge_case_queries(T, oracle_mod):
+    ev = oracle_mod.make_random_stream(5000, 60, 5)
+    og = oracle_mod.build(ev, 60, True)
+    graph = T.build_sequential(T.EventStream(ev, 60), True)
+    rng = np.random.default_rng(1)
+    nodes = rng.integers(0, 60, 4000)
+    times = np.concatenate([np.full(500, np.nan), np.full(500, -np.inf), np.full(500, np.inf),
+                            np.full(500, 0.0), np.full(500, -0.0), ev["timestamp"][:1500],
+                            rng.uniform(0, 3000, 500)])
+    for strat, k, l in (("recent", 5, 6), ("random", 5, 3), ("random", 33, 40),
+                        ("recent", 300, 301)):
+        want = oracle_mod.sample_assemble(og, nodes, times, k, strat, 3, l, 5001)
+        got = T.sample_assemble(graph, nodes, times, k, strat, 3, l, 5001, dt64=True)
+        check_rows(got, want, (strat, k, l))
+    # empty graph and single-node graph
+    e0 = T.build_sequential(T.EventStream(np.zeros(0, T.EVENT_DTYPE), 3), True)
+    out = T.sample_assemble(e0, [0, 1, 2], [1.0, 2.0, 3.0], 4, "recent", 0, 5, 1)
+    assert out["valid_len"].tolist() == [1, 1, 1]
+    assert out["node_index"][:, 0].tolist() == [1, 2, 3]
+    out = T.sample_assemble(e0, [], [], 4, "random", 0, 5, 1)
+    assert out["valid_len"].shape == (0,)
+
+
+def test_fused_int64_outputs_and_device_api(T, oracle_mod):
+    import torch
+    from paper_2409_05477_b200 import device as D
+    ev = D.random_stream(200000, 5000, 4001)
+    g = D.build(ev, 5000, True)
+    nodes, times = D.make_queries(ev, 0, 200000, 600, 5000)
+    h_ev = oracle_mod.make_random_stream(200000, 5000, 4001)
+    hn, ht = oracle_mod.make_queries(h_ev, 0, 200000, 600, 5000)
+    assert np.array_equal(nodes.cpu().numpy(), hn) and np.array_equal(times.cpu().numpy(), ht)
+    og = oracle_mod.build(h_ev, 5000, True)
+    out = D.sample_assemble(g, nodes, times, 10, "recent", 0, 11, 200001, index64=True, dt64=True)
+    want = oracle_mod.sample_assemble(og, hn, ht, 10, "recent", 0, 11, 200001)
+    assert np.array_equal(out["node_index"].cpu().numpy(), want["node_index"])
+    assert np.array_equal(out["edge_index"].cpu().numpy(), want["edge_index"])
+    assert np.array_equal(out["valid_len"].cpu().numpy(), want["valid_len"])
+    assert np.array_equal(out["time_delta64"].cpu().numpy(), want["time_delta"])
+    torch.cuda.synchronize()
