@@ -175,7 +175,7 @@ def test_edge_case_queries(T, oracle_mod):
     og = oracle_mod.build(ev, 60, True)
     graph = T.build_sequential(T.EventStream(ev, 60), True)
     rng = np.random.default_rng(1)
-    nodes = rng.integers(0, 60, 4000)
+    nodes = rng.integers(0, 60, 4500)
     times = np.concatenate([np.full(500, np.nan), np.full(500, -np.inf), np.full(500, np.inf),
                             np.full(500, 0.0), np.full(500, -0.0), ev["timestamp"][:1500],
                             rng.uniform(0, 3000, 500)])
