@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py -- TF-TGN hot path on B200: T-CSR build + most-recent-k sampling + sequence packing.
+
+Workload (BASELINE.json configs[3], GDELT-shaped; the metric's 1/2/4/8-GPU config):
+  make_random_stream(E=191,290,882, V=16,682, seed=42, zipf=1.2) generated on the device
+  (bit-identical to the reference generator), reverse=1 T-CSR build, then recent-10
+  sampling + suffix-infill packing (l=11) of every query of every event in the
+  forward_concat layout [src | dst | neg] per batch of B=600 events (573,872,646 queries),
+  processed in chunks.  One step = one full rebuild of the T-CSR from the resident event
+  stream + sampling/packing of all queries.  value = events through the path per second
+  (edges/s); the build and sampler rates are reported beside it.
+
+Timing: CUDA events on the launching stream, W untimed warm-up steps, K timed steps bracketed
+by barrier + synchronize, max over ranks.  Inputs (6.1 GB events, 9.2 GB queries) exceed the
+126 MB L2.  `e2e` repeats the step through the C ABI's host-buffer calls (tgfx_build_parallel
++ tgfx_sample_assemble with pinned host inputs/outputs; H2D/D2H inside the timed region).
+`cpu_baseline` / --impl reference time the reference's own CPU code (oracle/_ref, compiled
+from /root/reference) on a bounded prefix sample of the same workload.
+
+Multi-GPU (torchrun): T-CSR replicated (each rank builds it from its own copy of the
+stream), queries sharded contiguously across ranks (stream_base keeps results identical to
+1 GPU); no collective in the loop; total work fixed -> "scaling": "strong".
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (E, V, strategy, k, l, B, two_hop)
+    "G": dict(E=191_290_882, V=16682, strategy="recent", k=10, l=11, B=600,
+              name="GDELT-shaped synthetic (V=16,682, E=191,290,882, Zipf 1.2)"),
+    "W": dict(E=157_474, V=9227, strategy="recent", k=10, l=11, B=600,
+              name="Wikipedia-shaped synthetic (V=9,227, E=157,474)"),
+    "L": dict(E=1_293_103, V=1980, strategy="random", k=20, l=21, B=4000,
+              name="LastFM-shaped synthetic (V=1,980, E=1,293,103)"),
+}
+SEED, NEG_SEED, ZIPF = 42, 7, 1.2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------ CPU reference
+def reference_sample(cfg, sample_events, ev_host, threads):
+    """Reference CPU path (oracle/_ref = /root/reference/proj/src compiled) on the first
+    `sample_events` events of the workload stream: build (faster of build_sequential and
+    build_parallel(threads)) + sample_batch/build_sequence_batch of all their queries in the
+    forward_concat layout, batch by batch as forward_concat calls it (seed 9 + batch index)."""
+    from oracle import oracle as O
+    ev = ev_host[:sample_events]
+    rs = O.RefStream(ev, cfg["V"])
+    _, t_seq = rs.build(True, 0)
+    rg, t_par = rs.build(True, threads)
+    t_build = min(t_seq, t_par)
+    nodes, times = O.make_queries(ev, 0, sample_events, cfg["B"], cfg["V"], NEG_SEED)
+    qb = 3 * cfg["B"]
+    # per forward_concat batch the reference is called with 3B queries; to keep the sample
+    # bounded and the per-call overhead faithful we time calls of qb queries
+    t_sample = 0.0
+    for b, s in enumerate(range(0, len(nodes), qb)):
+        _, ts = O.ref_sample_assemble(rg, nodes[s:s + qb], times[s:s + qb], cfg["k"],
+                                      cfg["strategy"], 9 + b, cfg["l"], cfg["E"] + 1,
+                                      threads=threads, want_outputs=False)
+        t_sample += ts
+    q = len(nodes)
+    return dict(build_s=t_build, build_seq_s=t_seq, build_par_s=t_par, sample_s=t_sample,
+                events=sample_events, queries=q,
+                value=sample_events / (t_build + t_sample),
+                build_edges_per_s=sample_events / t_build, sample_queries_per_s=q / t_sample)
+
+
+def host_events(cfg, n):
+    """First n events of make_random_stream(E, V, 42) -- generated on the device (bit-identical
+    to the reference generator) and copied to the host."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    ev = D.random_stream(cfg["E"], cfg["V"], SEED)
+    out = ev[: n * 32].cpu().numpy().view(_event_dtype())
+    del ev
+    torch.cuda.empty_cache()
+    return out
+
+
+def _event_dtype():
+    import numpy as np
+    return np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
+
+
+def run_reference(args, cfg):
+    ws, rank, local = dist_setup()
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    import torch
+    torch.cuda.set_device(local)
+    n = args.cpu_events
+    ev_host = host_events(cfg, n)
+    for _ in range(args.warmup):
+        reference_sample(cfg, n, ev_host, threads)
+    runs = [reference_sample(cfg, n, ev_host, threads) for _ in range(args.steps)]
+    tot = sum(r["build_s"] + r["sample_s"] for r in runs)
+    value = n * len(runs) / tot
+    sample = (f"first {n:,} events of the {cfg['name']} stream: reference build (faster of "
+              f"build_sequential / build_parallel({threads})) + sample_batch+build_sequence_batch "
+              f"of their {runs[0]['queries']:,} queries, {threads} threads")
+    line = {
+        "impl": "reference", "metric": metric_name(cfg), "value": value, "unit": "edges/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * tot / len(runs), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
+        "config": config_obj(cfg, ws),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_edges_per_s": statistics.median(r["build_edges_per_s"] for r in runs),
+        "sample_queries_per_s": statistics.median(r["sample_queries_per_s"] for r in runs),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def metric_name(cfg):
+    return ("T-CSR build edges/s + sampled queries/s (events through build + recent-k "
+            "sampling/packing per second)")
+
+
+def config_obj(cfg, ws):
+    return {"workload": cfg["name"] + f"; reverse=1 T-CSR build + {cfg['strategy']}-{cfg['k']} "
+                                      f"sampling, l={cfg['l']}, all 3E queries, batch {cfg['B']}",
+            "events": cfg["E"], "num_nodes": cfg["V"], "queries": 3 * cfg["E"], "k": cfg["k"],
+            "seq_len": cfg["l"], "batch": cfg["B"], "reverse": 1,
+            "parallelism": f"query-sharded x{ws}, T-CSR replicated",
+            "l2_flush": "inputs larger than L2 (6.1 GB events, 9.2 GB queries vs 126 MB L2)"}
+
+
+# ------------------------------------------------------------------------------ our path
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2409_05477_b200 import _lib, device as D, tgformer as T
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    E, V, k, l, B = cfg["E"], cfg["V"], cfg["k"], cfg["l"], cfg["B"]
+    strat = cfg["strategy"]
+    Q = 3 * E
+    stream = torch.cuda.current_stream()
+
+    # resident inputs: event stream (generated on device) and all queries
+    ev = D.random_stream(E, V, SEED)
+    nodes = torch.empty(Q, dtype=torch.int64, device="cuda")
+    times = torch.empty(Q, dtype=torch.float64, device="cuda")
+    # whole batches per generation call keep the [src|dst|neg] batch layout
+    step_ev = (8_000_000 // B) * B
+    for e0 in range(0, E, step_ev):
+        e1 = min(E, e0 + step_ev)
+        D.make_queries(ev, e0, e1, B, V, NEG_SEED, nodes=nodes[3 * e0:3 * e1],
+                       times=times[3 * e0:3 * e1])
+    # this rank's contiguous query range, processed in chunks of whole batches
+    per = -(-Q // ws)
+    q_lo, q_hi = min(Q, rank * per), min(Q, (rank + 1) * per)
+    chunk = args.chunk
+    chunks = [(s, min(q_hi, s + chunk)) for s in range(q_lo, q_hi, chunk)]
+    out = D.alloc_rows(min(chunk, max(q_hi - q_lo, 1)), l)
+    g = D.build(ev, V, True)
+    torch.cuda.synchronize()
+
+    def one_step(record=None, taken=None):
+        if record:
+            record["b0"].record(stream)
+        D.rebuild(g, ev, trusted=True)
+        if record:
+            record["b1"].record(stream)
+        for i, (s, e) in enumerate(chunks):
+            if record:
+                record["c"][i][0].record(stream)
+            sub = {kk: vv[: e - s] for kk, vv in out.items()}
+            D.sample_assemble(g, nodes[s:e], times[s:e], k, strat, 9, l, E + 1, out=sub,
+                              stream_base=s, trusted=True)
+            if record:
+                record["c"][i][1].record(stream)
+            if taken is not None:
+                taken.append(int(sub["valid_len"].sum().item()) - (e - s))
+
+    taken = []
+    for w in range(args.warmup):
+        one_step(taken=taken if w == 0 else None)
+    if not taken:
+        one_step(taken=taken)
+    total_taken = sum(taken)
+
+    ev_rec = [dict(b0=torch.cuda.Event(enable_timing=True), b1=torch.cuda.Event(enable_timing=True),
+                   c=[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in chunks]) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start.record(stream)
+        for s in range(args.steps):
+            one_step(record=ev_rec[s])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    total_ms = start.elapsed_time(end)
+    build_ms = [r["b0"].elapsed_time(r["b1"]) for r in ev_rec]
+    samp_launch_ms = [a.elapsed_time(b) for r in ev_rec for (a, b) in r["c"]]
+    samp_ms = [sum(a.elapsed_time(b) for (a, b) in r["c"]) for r in ev_rec]
+    # max over ranks
+    vals = torch.tensor([total_ms, statistics.median(build_ms), statistics.median(samp_ms)],
+                        dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        tk = torch.tensor([total_taken], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tk)
+        total_taken = int(tk.item())
+    total_ms, build_med, samp_med = vals.tolist()
+    ms_per_step = total_ms / args.steps
+
+    peak, peak_src = load_peaks()
+    # algorithmic bytes
+    build_bytes = 32 * E + 24 * 2 * E + 8 * (V + 1)
+    q_local = q_hi - q_lo
+    samp_bytes_all = 16 * Q + 16 * Q + 24 * total_taken + (12 * l + 4) * Q
+    samp_bytes_local = samp_bytes_all * (q_local / Q)
+    avg_launch_ms = statistics.mean(samp_launch_ms)
+    bytes_per_launch = samp_bytes_local / max(len(chunks), 1)
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    traffic = load_traffic(cfg, bytes_per_launch)
+
+    line = {
+        "metric": metric_name(cfg), "value": E / (ms_per_step * 1e-3), "unit": "edges/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int64/f64 (T-CSR), int32/fp32 (sequence tensors)",
+        "data": "synthetic (device generator, bit-identical to tgf::make_random_stream)",
+        "config": config_obj(cfg, ws),
+        "build": {"ms": build_med, "edges_per_s": E / (build_med * 1e-3),
+                  "alg_bytes": build_bytes,
+                  "achieved_gbs": build_bytes / (build_med * 1e-3) / 1e9,
+                  "frac": build_bytes / (build_med * 1e-3) / 1e9 / peak},
+        "sample": {"ms": samp_med, "queries_per_s": q_local * ws / (samp_med * 1e-3),
+                   "launches_per_step": len(chunks), "mean_taken": total_taken / Q},
+        "roofline": {"kernel": "k_recent (fused recent-k sampler + sequence packing)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": avg_launch_ms},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = run_e2e(args, cfg, ev, nodes, times, chunks, ws)
+    if rank == 0 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        ev_host = ev[: args.cpu_events * 32].cpu().numpy().view(_event_dtype())
+        r = reference_sample(cfg, args.cpu_events, ev_host, threads)
+        line["cpu_baseline"] = {
+            "value": r["value"], "unit": "edges/s", "cores": threads, "kind": "reference",
+            "sample": (f"first {r['events']:,} events of the same stream: reference build "
+                       f"({r['build_s']:.3f}s, faster of sequential {r['build_seq_s']:.3f}s / "
+                       f"parallel({threads}) {r['build_par_s']:.3f}s) + sample_batch+"
+                       f"build_sequence_batch of {r['queries']:,} queries ({r['sample_s']:.3f}s)"),
+            "build_edges_per_s": r["build_edges_per_s"],
+            "sample_queries_per_s": r["sample_queries_per_s"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def load_traffic(cfg, bytes_per_launch):
+    """DRAM bytes per k_recent launch from the committed ncu --set full summary, scaled from
+    the profiled launch's query count to this launch (null if absent)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        t = d["k_recent"]
+        return t["dram_bytes"] * bytes_per_launch / t["alg_bytes"]
+    except Exception:
+        return None
+
+
+def run_e2e(args, cfg, ev, nodes, times, chunks, ws):
+    """Same step through the C ABI with HOST buffers (pinned): tgfx_build_parallel from host
+    events, then tgfx_sample_assemble per chunk with host queries and host outputs."""
+    import numpy as np
+    import torch
+    from paper_2409_05477_b200 import _lib
+    L = _lib.lib()
+    E, V, k, l = cfg["E"], cfg["V"], cfg["k"], cfg["l"]
+    h_ev = torch.empty(ev.numel(), dtype=torch.uint8, pin_memory=True)
+    h_ev.copy_(ev)
+    lo, hi = chunks[0][0], chunks[-1][1]
+    h_nodes = torch.empty(hi - lo, dtype=torch.int64, pin_memory=True)
+    h_times = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True)
+    h_nodes.copy_(nodes[lo:hi])
+    h_times.copy_(times[lo:hi])
+    cmax = max(e - s for s, e in chunks)
+    o_n = torch.empty(cmax * l, dtype=torch.int32, pin_memory=True)
+    o_e = torch.empty(cmax * l, dtype=torch.int32, pin_memory=True)
+    o_d = torch.empty(cmax * l, dtype=torch.float32, pin_memory=True)
+    o_v = torch.empty(cmax, dtype=torch.int32, pin_memory=True)
+    strat = 0 if cfg["strategy"] == "recent" else 1
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+
+    def step():
+        h = C.c_void_p()
+        _lib.check(L.tgfx_build_parallel(P(h_ev), E, V, 1, 1, C.byref(h)))
+        for s, e in chunks:
+            _lib.check(L.tgfx_sample_assemble(
+                h, C.c_void_p(h_nodes.data_ptr() + 8 * (s - lo)),
+                C.c_void_p(h_times.data_ptr() + 8 * (s - lo)), e - s, k, strat, 9, s, l, E + 1,
+                P(o_n), P(o_e), P(o_d), None, P(o_v)))
+        _lib.check(L.tgfx_graph_free(h))
+
+    step()  # warm-up
+    n_steps = max(1, min(args.steps, args.e2e_steps))
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        step()
+    dt = (time.perf_counter() - t0) / n_steps
+    q = hi - lo
+    return {"value": E / dt, "unit": "edges/s", "ms_per_step": dt * 1e3, "steps": n_steps,
+            "h2d_bytes_per_step": 32 * E + 16 * q,
+            "d2h_bytes_per_step": (12 * l + 4) * q,
+            "path": "C ABI host-buffer calls tgfx_build_parallel + tgfx_sample_assemble "
+                    "(pinned host memory), wall clock"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="G", choices=sorted(CONFIGS))
+    ap.add_argument("--chunk", type=int, default=3 * 8_000_000)
+    ap.add_argument("--cpu-events", type=int, default=4_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: W >= 3 required by the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
