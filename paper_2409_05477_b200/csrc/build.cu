@@ -39,12 +39,7 @@ namespace tgfx {
 namespace {
 
 constexpr int kHistThreads = 512;
-constexpr int kScThreads = 256;
-constexpr int kScRounds = 4;                            // entries per lane per tile
-constexpr int kScTile = kScThreads * kScRounds;         // 1024 entries per tile
-constexpr int kSlots = 2048;                            // hash slots (load <= 0.5)
-constexpr int kLog2Slots = 11;
-constexpr size_t kScFixedSmem = kSlots * (4 + 4 + 8) + kSlots * 2 + 64;
+
 constexpr int64_t kFastMaxNodes = 45000;
 
 __global__ void k_init_flags(BuildFlags* f) {
@@ -71,41 +66,44 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
   bool unsorted = false;
   unsigned long long bad = ~0ull;
   long long mx = LLONG_MIN, mn = LLONG_MAX;
-  for (int64_t b = e0; b < e1; b += kHistThreads) {
-    const int64_t e = b + threadIdx.x;
-    const bool valid = e < e1;
-    Ev x{0, 0, 0, 0.0};
-    if (valid) x = load_event(ev, e);
-    // (t, eid) order against event e+1: from the next lane, else a direct load
-    double tn = __shfl_down_sync(kFull, x.t, 1);
-    long long en = __shfl_down_sync(kFull, (long long)x.eid, 1);
-    if (valid && e + 1 < n && (lane == 31 || e + 1 >= e1)) {
-      const Ev y = load_event(ev, e + 1);
-      tn = y.t;
-      en = y.eid;
+  constexpr int U = 4;  // events per thread in flight
+  for (int64_t b = e0; b < e1; b += U * kHistThreads) {
+    Ev xs[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = b + k * kHistThreads + threadIdx.x;
+      xs[k] = e < e1 ? load_event(ev, e) : Ev{0, 0, 0, 0.0};
     }
-    if (valid && e + 1 < n) {
-      const bool ok = (x.t < tn) || (x.t == tn && x.eid <= en);  // NaN -> not ok
-      unsorted |= !ok;
-    }
-    const bool ok_s = valid && x.src >= 0 && x.src < V;
-    const bool ok_d = valid && x.dst >= 0 && x.dst < V;
-    if (valid && !(ok_s && ok_d)) bad = min(bad, (unsigned long long)e);
-    if (valid) {
-      mx = max(mx, (long long)x.eid);
-      mn = min(mn, (long long)x.eid);
-    }
-    if (HIST) {
-      const bool ok = ok_s && ok_d;  // events with a bad endpoint are not counted
-      {
-        const unsigned key = ok ? static_cast<unsigned>(x.src) : 0xffffffffu;
-        const unsigned peers = __match_any_sync(kFull, key);
-        if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = b + k * kHistThreads + threadIdx.x;
+      const bool valid = e < e1;
+      const Ev x = xs[k];
+      // (t, eid) order against event e+1: from the next lane, else a direct load
+      double tn = __shfl_down_sync(kFull, x.t, 1);
+      long long en = __shfl_down_sync(kFull, (long long)x.eid, 1);
+      if (valid && e + 1 < n && (lane == 31 || e + 1 >= e1)) {
+        const Ev y = load_event(ev, e + 1);
+        tn = y.t;
+        en = y.eid;
       }
-      if (R == 2) {
-        const unsigned key = ok ? static_cast<unsigned>(x.dst) : 0xffffffffu;
-        const unsigned peers = __match_any_sync(kFull, key);
-        if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
+      if (valid && e + 1 < n) {
+        const bool ok = (x.t < tn) || (x.t == tn && x.eid <= en);  // NaN -> not ok
+        unsorted |= !ok;
+      }
+      const bool ok_s = valid && x.src >= 0 && x.src < V;
+      const bool ok_d = valid && x.dst >= 0 && x.dst < V;
+      if (valid && !(ok_s && ok_d)) bad = min(bad, (unsigned long long)e);
+      if (valid) {
+        mx = max(mx, (long long)x.eid);
+        mn = min(mn, (long long)x.eid);
+      }
+      if (HIST) {
+        const bool ok = ok_s && ok_d;  // events with a bad endpoint are not counted
+        if (ok) {
+          atomicAdd(&hist[static_cast<unsigned>(x.src)], 1u);
+          if (R == 2) atomicAdd(&hist[static_cast<unsigned>(x.dst)], 1u);
+        }
       }
     }
   }
@@ -147,14 +145,10 @@ __global__ void k_colsum(const uint32_t* __restrict__ cnt, int C, int32_t V, int
   deg[u] = s;
 }
 
-// K2b: exclusive scan of deg[0..V) in place into indptr[0..V] (single CTA; V <= 45000)
-__global__ void __launch_bounds__(1024) k_indptr_scan(int64_t* a, int32_t V) {
-  __shared__ int64_t wsum[32];
-  const int per = (V + 1023) / 1024;
-  const int64_t i0 = static_cast<int64_t>(threadIdx.x) * per;
-  int64_t s = 0;
-  for (int i = 0; i < per; ++i)
-    if (i0 + i < V) s += a[i0 + i];
+// K2b: exclusive scan of deg[0..V) in place into indptr[0..V] (single CTA; V <= 45000), and
+// of the cold nodes' degrees into cdelta[u] = coldbase[u] - indptr[u]: a cold entry at output
+// position p of node u has dense cold index p + cdelta[u].  *ncold = total cold entries.
+__device__ __forceinline__ int64_t block_excl_scan_1024(int64_t s, int64_t* wsum, int64_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t x = s;
 #pragma unroll
@@ -174,15 +168,43 @@ __global__ void __launch_bounds__(1024) k_indptr_scan(int64_t* a, int32_t V) {
     wsum[lane] = w;
   }
   __syncthreads();
-  int64_t run = (warp ? wsum[warp - 1] : 0) + x - s;
+  const int64_t ex = (warp ? wsum[warp - 1] : 0) + x - s;
+  *total = wsum[31];
+  __syncthreads();
+  return ex;
+}
+
+__global__ void __launch_bounds__(1024) k_indptr_scan(int64_t* a, int32_t V,
+                                                      const uint32_t* __restrict__ coldbits,
+                                                      int64_t* __restrict__ cdelta,
+                                                      int64_t* __restrict__ ncold) {
+  __shared__ int64_t wsum[32];
+  const int per = (V + 1023) / 1024;
+  const int64_t i0 = static_cast<int64_t>(threadIdx.x) * per;
+  int64_t s = 0, sc = 0;
+  for (int i = 0; i < per; ++i) {
+    if (i0 + i < V) {
+      const int64_t d = a[i0 + i];
+      s += d;
+      if ((coldbits[(i0 + i) >> 5] >> ((i0 + i) & 31)) & 1u) sc += d;
+    }
+  }
+  int64_t tot, totc;
+  int64_t run = block_excl_scan_1024(s, wsum, &tot);
+  int64_t runc = block_excl_scan_1024(sc, wsum, &totc);
   for (int i = 0; i < per; ++i) {
     if (i0 + i < V) {
       const int64_t d = a[i0 + i];
       a[i0 + i] = run;
+      cdelta[i0 + i] = runc - run;
       run += d;
+      if ((coldbits[(i0 + i) >> 5] >> ((i0 + i) & 31)) & 1u) runc += d;
     }
   }
-  if (threadIdx.x == 1023) a[V] = wsum[31];
+  if (threadIdx.x == 0) {
+    a[V] = tot;
+    *ncold = totc;
+  }
 }
 
 // K2c: starting cursor of every (chunk, node): indptr[u] + sum of earlier chunks' counts
@@ -199,138 +221,150 @@ __global__ void k_coloff(uint32_t* __restrict__ cnt, int C, int32_t V,
   }
 }
 
-__device__ __forceinline__ uint32_t byte_prefix(uint32_t w0, uint32_t w1, int warp) {
-  // sum of per-warp byte counters of warps < warp (bytes 0..3 in w0, 4..7 in w1)
-  if (warp <= 4) {
-    const uint32_t m = warp == 4 ? 0xffffffffu : ((1u << (8 * warp)) - 1u);
-    return static_cast<uint32_t>(__dp4a(w0 & m, 0x01010101u, 0u));
-  }
-  const uint32_t m = (1u << (8 * (warp - 4))) - 1u;
-  return static_cast<uint32_t>(__dp4a(w0, 0x01010101u, 0u) + __dp4a(w1 & m, 0x01010101u, 0u));
+
+// K2d: cold flags (one bit per node): entries of nodes with few entries per chunk are not
+// written by the chunked scatter -- each chunk holds its own cursor per node, so a low-degree
+// node's partially filled output sectors would sit in L2 for most of the kernel and get
+// evicted half-written (read-modify-write at DRAM).  Their (pos, nbr, eid, ts) records are
+// appended to a stream-ordered list instead and placed by k_cold in lockstep.
+__global__ void k_coldflags(const int64_t* __restrict__ deg, int32_t V, int64_t thresh,
+                            uint32_t* __restrict__ coldbits) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool cold = u < V && deg[u] < thresh;
+  const unsigned b = __ballot_sync(kFull, cold);
+  if ((threadIdx.x & 31) == 0 && u < ((V + 31) & ~31)) coldbits[u >> 5] = b;
 }
 
-// K3: stable scatter -------------------------------------------------------------------
-template <int R>
-__global__ void __launch_bounds__(kScThreads) k_scatter(const tgfx_event* __restrict__ ev,
-                                                        int64_t n, int32_t V, int64_t chunk_ev,
-                                                        const uint32_t* __restrict__ off,
-                                                        int64_t* __restrict__ nbr_out,
-                                                        int64_t* __restrict__ eid_out,
-                                                        double* __restrict__ ts_out) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  const int vpad = (V + 3) & ~3;
-  uint32_t* cursor = smem;                                   // [V]
-  uint32_t* skey = cursor + vpad;                            // [kSlots] node+1, 0 = empty
-  uint32_t* sbase = skey + kSlots;                           // [kSlots]
-  uint32_t* scnt = sbase + kSlots;                           // [kSlots][2]: 8 warp bytes
-  uint16_t* slist = reinterpret_cast<uint16_t*>(scnt + 2 * kSlots);  // [kSlots]
-  uint32_t* nused = reinterpret_cast<uint32_t*>(slist + kSlots);
-  uint8_t* scnt8 = reinterpret_cast<uint8_t*>(scnt);
-  volatile uint32_t* vkey = skey;
+// K3: stable scatter ("ticketed warps") ---------------------------------------------------
+// Each CTA owns a contiguous chunk and its per-node cursors (shared memory).  The chunk is cut
+// into warp tiles of kTkRounds x 32 consecutive entries, taken by the CTA's warps round-robin.
+// A warp loads and groups its tile (MATCH.ANY per round) with no shared state, then waits for
+// the CTA's ticket to reach its tile and runs a short critical section: for each round, the
+// leader of every node group reads and bumps that node's cursor (distinct nodes per round, so
+// one LDS/STS per group, rounds in order).  Emission order is preserved by construction.
+// Positions are written after the ticket is passed on.
+constexpr int kTkRoundsDefault = 8;  // rounds (32 entries each) per warp tile
+constexpr int kTkWarpsDefault = 8;
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int R, int kTkRounds, int kTkWarps>
+__global__ void __launch_bounds__(kTkWarps * 32) k_scatter(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+    const int64_t* __restrict__ cdelta, ulonglong2* __restrict__ cold_img,
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int vpad = (V + 31) & ~31;
+  uint32_t* cursor = smem;                 // [V]
+  uint32_t* coldbits = cursor + vpad;      // [V/32]
+
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(kFull, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
   const int64_t e1 = min(n, e0 + chunk_ev);
   if (e0 >= e1) return;
   const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
-  for (int i = threadIdx.x; i < V; i += kScThreads) cursor[i] = orow[i];
-  for (int i = threadIdx.x; i < kSlots; i += kScThreads) {
-    skey[i] = 0;
-    scnt[2 * i] = 0;
-    scnt[2 * i + 1] = 0;
-  }
-  if (threadIdx.x == 0) *nused = 0;
+  constexpr int kTkThreads = kTkWarps * 32;
+  for (int i = threadIdx.x; i < V; i += kTkThreads) cursor[i] = orow[i];
+  for (int i = threadIdx.x; i < vpad / 32; i += kTkThreads) coldbits[i] = coldbits_g[i];
   __syncthreads();
 
   const int64_t E0 = e0 * R, E1 = e1 * R;
-  for (int64_t T0 = E0; T0 < E1; T0 += kScTile) {
-    int64_t nb[kScRounds], ei[kScRounds];
-    double tt[kScRounds];
-    uint32_t node[kScRounds];
-    bool ok[kScRounds];
+  constexpr int kTile = kTkRounds * 32;
+  const int64_t ntiles = ceil_div(E1 - E0, kTile);
+  for (int64_t t = warp; t < ntiles; t += kTkWarps) {
+    const int64_t T0 = E0 + t * kTile;
+    Ev x[kTkRounds];
 #pragma unroll
-    for (int r = 0; r < kScRounds; ++r) {
-      const int64_t j = T0 + warp * (kScRounds * 32) + r * 32 + lane;
-      ok[r] = j < E1;
-      node[r] = 0xffffffffu;
-      if (ok[r]) {
-        const int64_t e = R == 2 ? (j >> 1) : j;
-        const Ev x = load_event(ev, e);
-        const bool side = R == 2 && (j & 1);
-        const int64_t u = side ? x.dst : x.src;
-        const int64_t v = side ? x.src : x.dst;
-        ok[r] = x.src >= 0 && x.src < V && x.dst >= 0 && x.dst < V;
-        node[r] = ok[r] ? static_cast<uint32_t>(u) : 0xffffffffu;
-        nb[r] = v;
-        ei[r] = x.eid;
-        tt[r] = x.t;
-      }
+    for (int r = 0; r < kTkRounds; ++r) {
+      const int64_t j = T0 + r * 32 + lane;
+      x[r] = j < E1 ? load_event(ev, R == 2 ? (j >> 1) : j) : Ev{0, -1, -1, 0.0};
     }
-    // phase 1: stable in-tile rank = (earlier rounds of this warp) + (earlier lanes)
-    uint32_t slot_rank[kScRounds];  // slot << 8 | rank within this warp's 128 entries
+    uint32_t node[kTkRounds], peers[kTkRounds];
 #pragma unroll
-    for (int r = 0; r < kScRounds; ++r) {
-      const unsigned peers = __match_any_sync(kFull, node[r]);
-      const int leader = __ffs(peers) - 1;
-      uint32_t packed = 0;
-      if (ok[r] && lane == leader) {
-        const uint32_t key = node[r] + 1;
-        uint32_t h = (node[r] * 2654435761u) >> (32 - kLog2Slots);
-        while (true) {
-          const uint32_t k = vkey[h];
-          if (k == key) break;
-          if (k == 0) {
-            const uint32_t old = atomicCAS(&skey[h], 0u, key);
-            if (old == 0) {
-              slist[atomicAdd(nused, 1u)] = static_cast<uint16_t>(h);
-              break;
-            }
-            if (old == key) break;
-          }
-          h = (h + 1) & (kSlots - 1);
-        }
-        const uint32_t prev = scnt8[h * 8 + warp];
-        scnt8[h * 8 + warp] = static_cast<uint8_t>(prev + __popc(peers));
-        packed = (h << 8) | prev;
+    for (int r = 0; r < kTkRounds; ++r) {
+      const int64_t j = T0 + r * 32 + lane;
+      const bool side = R == 2 && (j & 1);
+      const bool ok = j < E1 && x[r].src >= 0 && x[r].src < V && x[r].dst >= 0 && x[r].dst < V;
+      node[r] = ok ? static_cast<uint32_t>(side ? x[r].dst : x[r].src) : 0xffffffffu;
+      if (side) {  // keep the other endpoint in .dst, so .dst is always the neighbour
+        const int64_t a = x[r].src;
+        x[r].src = x[r].dst;
+        x[r].dst = a;
       }
-      packed = __shfl_sync(kFull, packed, leader);
-      slot_rank[r] = packed + __popc(peers & lanemask_lt());
+      peers[r] = __match_any_sync(kFull, node[r]);
+    }
+    // cold flags and cold-index offsets, fetched before the critical section so their
+    // latency overlaps the ticket wait
+    int64_t cd[kTkRounds];
+#pragma unroll
+    for (int r = 0; r < kTkRounds; ++r) {
+      const bool cold = node[r] != 0xffffffffu && ((coldbits[node[r] >> 5] >> (node[r] & 31)) & 1u);
+      cd[r] = cold ? __ldg(reinterpret_cast<const long long*>(cdelta) + node[r]) : INT64_MIN;
+    }
+    // critical section: wait until the owner of tile t-1 (the previous warp) hands over.
+    // Named barrier 1+w is warp w's inbox: the previous warp arrives, this warp syncs
+    // (hardware wait, no spinning; bar.arrive/bar.sync order the shared-memory cursors).
+    if (t > 0) named_bar_sync(1 + warp, 64);
+    uint32_t base[kTkRounds];
+#pragma unroll
+    for (int r = 0; r < kTkRounds; ++r) {
+      const bool lead = node[r] != 0xffffffffu && lane == __ffs(peers[r]) - 1;
+      uint32_t b = 0;
+      if (lead) {
+        b = cursor[node[r]];
+        cursor[node[r]] = b + __popc(peers[r]);
+      }
+      base[r] = b;
       __syncwarp();
     }
-    __syncthreads();
-    // phase 2: per distinct node of the tile, claim a run of positions from its cursor
-    const uint32_t nu = *nused;
-    for (uint32_t i = threadIdx.x; i < nu; i += kScThreads) {
-      const uint32_t s = slist[i];
-      const uint32_t u = skey[s] - 1;
-      const uint32_t tot = static_cast<uint32_t>(__dp4a(scnt[2 * s], 0x01010101u, 0u) +
-                                                 __dp4a(scnt[2 * s + 1], 0x01010101u, 0u));
-      const uint32_t b = cursor[u];
-      sbase[s] = b;
-      cursor[u] = b + tot;
-    }
-    __syncthreads();
-    // phase 3: write the SoA columns
+    if (t + 1 < ntiles) named_bar_arrive(1 + (warp + 1) % kTkWarps, 64);
+    // positions and writes, outside the critical section
 #pragma unroll
-    for (int r = 0; r < kScRounds; ++r) {
-      if (ok[r]) {
-        const uint32_t s = slot_rank[r] >> 8;
-        const uint32_t pos = sbase[s] + byte_prefix(scnt[2 * s], scnt[2 * s + 1], warp) +
-                             (slot_rank[r] & 0xff);
-        nbr_out[pos] = nb[r];
-        eid_out[pos] = ei[r];
-        ts_out[pos] = tt[r];
+    for (int r = 0; r < kTkRounds; ++r) {
+      const int leader = __ffs(peers[r]) - 1;
+      const uint32_t pos =
+          __shfl_sync(kFull, base[r], leader) + __popc(peers[r] & lanemask_lt());
+      const bool ok = node[r] != 0xffffffffu;
+      const bool cold = cd[r] != INT64_MIN;
+      if (ok && !cold) {
+        nbr_out[pos] = x[r].dst;
+        eid_out[pos] = x[r].eid;
+        ts_out[pos] = x[r].t;
+      }
+      if (cold) {
+        // dense cold index; one full 32-byte record (no partial-sector write)
+        const int64_t ci = static_cast<int64_t>(pos) + cd[r];
+        ulonglong2* rec = cold_img + 2 * ci;
+        rec[0] = make_ulonglong2(static_cast<unsigned long long>(x[r].dst),
+                                 static_cast<unsigned long long>(x[r].eid));
+        rec[1] = make_ulonglong2(static_cast<unsigned long long>(__double_as_longlong(x[r].t)),
+                                 static_cast<unsigned long long>(pos));
       }
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nu; i += kScThreads) {
-      const uint32_t s = slist[i];
-      skey[s] = 0;
-      scnt[2 * s] = 0;
-      scnt[2 * s + 1] = 0;
-    }
-    if (threadIdx.x == 0) *nused = 0;
-    __syncthreads();
+  }
+}
+
+// K4: place the cold entries.  Consecutive cold indices are consecutive positions of a cold
+// node's slice, so both the 32-byte record reads and the column writes are coalesced.
+__global__ void __launch_bounds__(256) k_cold(const ulonglong2* __restrict__ img, int64_t ncold,
+                                              int64_t* __restrict__ nbr_out,
+                                              int64_t* __restrict__ eid_out,
+                                              double* __restrict__ ts_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncold;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldg(img + 2 * i);
+    const ulonglong2 b = __ldg(img + 2 * i + 1);
+    const int64_t pos = static_cast<int64_t>(b.y);
+    nbr_out[pos] = static_cast<int64_t>(a.x);
+    eid_out[pos] = static_cast<int64_t>(a.y);
+    ts_out[pos] = __longlong_as_double(static_cast<long long>(b.x));
   }
 }
 
@@ -452,22 +486,63 @@ int grid_for(int64_t work, int threads, int per_sm = 8) {
 }
 
 size_t scatter_smem(int64_t V) {
-  return static_cast<size_t>(((V + 3) & ~3LL) * 4) + kScFixedSmem;
+  const int64_t vpad = (V + 31) & ~31LL;
+  return static_cast<size_t>(vpad * 4 + vpad / 8) + 16;
+}
+
+// grow-only workspace buffer owned by the graph
+void* ws_get(void*& p, size_t& have, size_t need, cudaStream_t s) {
+  if (have < need) {
+    if (p) dfree(p, s);
+    p = dmalloc(need, s);
+    have = need;
+  }
+  return p;
+}
+
+int64_t cold_theta() {
+  // entries-per-chunk threshold below which a node's entries take the cold (deferred) path
+  static int64_t theta = [] {
+    const char* e = getenv("TGFX_COLD_THETA");
+    return e ? atoll(e) : 300LL;
+  }();
+  return theta;
+}
+
+int scatter_variant() {
+  static int v = [] {
+    const char* e = getenv("TGFX_SCATTER_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// (rounds, warps) variants of the ticketed scatter
+#define TGFX_SCATTER_VARIANTS(X) \
+  X(0, 8, 8)                     \
+  X(1, 4, 8)                     \
+  X(2, 4, 16)                    \
+  X(3, 16, 8)                    \
+  X(4, 8, 4)                     \
+  X(5, 2, 16)
+
+template <int R, int RO, int W>
+int scatter_bps(int64_t V) {
+  const size_t smem = scatter_smem(V);
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter<R, RO, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter<R, RO, W>, W * 32, smem));
+  return std::max(bps, 1);
 }
 
 int scatter_blocks_per_sm(int R, int64_t V) {
-  const size_t smem = scatter_smem(V);
-  int bps = 0;
-  if (R == 2) {
-    TGFX_CUDA(cudaFuncSetAttribute(k_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter<2>, kScThreads, smem));
-  } else {
-    TGFX_CUDA(cudaFuncSetAttribute(k_scatter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter<1>, kScThreads, smem));
-  }
-  return std::max(bps, 1);
+  const int v = scatter_variant();
+#define X(ID, RO, W) \
+  if (v == ID) return R == 2 ? scatter_bps<2, RO, W>(V) : scatter_bps<1, RO, W>(V);
+  TGFX_SCATTER_VARIANTS(X)
+#undef X
+  return R == 2 ? scatter_bps<2, 8, 8>(V) : scatter_bps<1, 8, 8>(V);
 }
 
 void read_flags(tgfx_graph* g, cudaStream_t s) {
@@ -544,23 +619,50 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   const int32_t V = static_cast<int32_t>(g->V);
   const int tb = 256;
   const int vb = static_cast<int>(ceil_div(std::max<int64_t>(V, 1), tb));
+  const int64_t vpad = (static_cast<int64_t>(V) + 31) & ~31LL;
+  // small workspace: cold bitmask [vpad/32] u32 | cdelta [V] i64 | ncold i64
+  char* small = static_cast<char*>(ws_get(g->ws_small, g->ws_small_bytes,
+                                          16 + 4 * (vpad / 32) + 8 * (vpad + 2), s));
+  uint32_t* coldbits = reinterpret_cast<uint32_t*>(small);
+  int64_t* cdelta = reinterpret_cast<int64_t*>(small + ((4 * (vpad / 32) + 15) & ~15LL));
+  int64_t* ncold_d = cdelta + vpad;
   if (V > 0) {
     k_colsum<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr);
     after_launch("k_colsum");
+    k_coldflags<<<static_cast<int>(ceil_div(vpad, tb)), tb, 0, s>>>(g->indptr, V,
+                                                                     cold_theta() * C, coldbits);
+    after_launch("k_coldflags");
   }
-  k_indptr_scan<<<1, 1024, 0, s>>>(g->indptr, V);
+  k_indptr_scan<<<1, 1024, 0, s>>>(g->indptr, V, coldbits, cdelta, ncold_d);
   after_launch("k_indptr_scan");
   if (V > 0) {
     k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr);
     after_launch("k_coloff");
   }
+  int64_t ncold = 0;
+  TGFX_CUDA(cudaMemcpyAsync(&ncold, ncold_d, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaStreamSynchronize(s));
+  ulonglong2* img = static_cast<ulonglong2*>(
+      ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
   const size_t smem = scatter_smem(V);
-  if (g->reverse)
-    k_scatter<2><<<C, kScThreads, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, g->nbr, g->eid, g->ts);
-  else
-    k_scatter<1><<<C, kScThreads, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, g->nbr, g->eid, g->ts);
+  const int v = scatter_variant();
+#define X(ID, RO, W)                                                                             \
+  if (v == ID) {                                                                                 \
+    if (g->reverse)                                                                              \
+      k_scatter<2, RO, W><<<C, W * 32, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
+                                                  img, g->nbr, g->eid, g->ts);                   \
+    else                                                                                         \
+      k_scatter<1, RO, W><<<C, W * 32, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
+                                                  img, g->nbr, g->eid, g->ts);                   \
+  }
+  TGFX_SCATTER_VARIANTS(X)
+#undef X
   after_launch("k_scatter");
+  if (ncold > 0) {
+    k_cold<<<resident_grid(k_cold, 256, 0, ncold), 256, 0, s>>>(img, ncold, g->nbr, g->eid, g->ts);
+    after_launch("k_cold");
+  }
 }
 
 void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
@@ -627,12 +729,14 @@ void graph_release(tgfx_graph* g) {
   if (g->ts) dfree(g->ts, s);
   if (g->dflags) dfree(g->dflags, s);
   if (g->ws) dfree(g->ws, s);
+  if (g->ws_small) dfree(g->ws_small, s);
+  if (g->ws_rec) dfree(g->ws_rec, s);
   if (g->hflags) cudaFreeHost(g->hflags);
   g->indptr = g->nbr = g->eid = nullptr;
   g->ts = nullptr;
   g->dflags = nullptr;
   g->hflags = nullptr;
-  g->ws = nullptr;
+  g->ws = g->ws_small = g->ws_rec = nullptr;
 }
 
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted) {

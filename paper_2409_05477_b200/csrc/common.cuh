@@ -98,6 +98,19 @@ const DeviceInfo& device_info();
 void* dmalloc(size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
 
+// Grid for a grid-stride kernel: never more blocks than can be resident at once, so every
+// thread sweeps the index space together (a second wave would revisit each output region
+// long after the first, evicting half-written sectors).
+template <typename K>
+int resident_grid(K kernel, int threads, size_t smem, int64_t work_items) {
+  int bps = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, smem),
+             "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  const int64_t need = (work_items + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(device_info().sms) * (bps > 0 ? bps : 1);
+  return static_cast<int>(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace tgfx

@@ -25,8 +25,12 @@ struct tgfx_graph {
   double* ts = nullptr;
   int64_t max_eid = -1, min_eid = 0;
   // build workspace, kept for rebuilds
-  void* ws = nullptr;
+  void* ws = nullptr;  // per-chunk node count / cursor table
   size_t ws_bytes = 0;
+  void* ws_small = nullptr;  // cold bitmask + per-chunk cold counts / offsets
+  size_t ws_small_bytes = 0;
+  void* ws_rec = nullptr;  // deferred (cold) entry records, 24 B each
+  size_t ws_rec_bytes = 0;
   BuildFlags* dflags = nullptr;
   BuildFlags* hflags = nullptr;  // pinned host mirror
 };

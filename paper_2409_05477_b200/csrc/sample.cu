@@ -99,50 +99,102 @@ __device__ __forceinline__ void write_vlen(const Outs& o, int64_t q, int64_t v) 
 }
 
 // ------------------------------------------------------------------ recent-k
+// QL queries per lane: their binary searches are interleaved step by step so each lane keeps
+// QL independent loads in flight (the search is a chain of dependent L2/HBM round trips).
+template <int QL>
+__device__ __forceinline__ void search_interleaved(const double* __restrict__ ts,
+                                                   const int64_t (&lo)[QL], int64_t (&n)[QL],
+                                                   const double (&t)[QL], int64_t (&m)[QL]) {
+  int64_t base[QL];
+#pragma unroll
+  for (int j = 0; j < QL; ++j) base[j] = lo[j];
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < QL; ++j) any |= n[j] > 0;
+    if (!any) break;
+    double v[QL];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) v[j] = n[j] > 0 ? __ldg(ts + base[j] + (n[j] >> 1)) : 0.0;
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      if (n[j] > 0) {
+        const int64_t half = n[j] >> 1;
+        const bool lt = v[j] < t[j];
+        base[j] = lt ? base[j] + half + 1 : base[j];
+        n[j] = lt ? n[j] - half - 1 : half;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QL; ++j) m[j] = base[j] - lo[j];
+}
+
+// floor(s / w) for s < 2^16 via a 32-bit multiply-high (magic = ceil(2^32 / w)), else divide
+__device__ __forceinline__ int div_slot(int s, int w, uint32_t magic) {
+  return magic ? static_cast<int>(__umulhi(static_cast<uint32_t>(s), magic)) : s / w;
+}
+
 // ASSEMBLE: rows [Q, l]; else entries [Q, k] + counts.
-template <bool ASSEMBLE, bool IDX64>
-__global__ void __launch_bounds__(kThreads) k_recent(
+template <bool ASSEMBLE, bool IDX64, int QL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_recent(
     const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, Outs o) {
-  __shared__ int64_t s_start[kWarps][32];
-  __shared__ int64_t s_u[kWarps][32];
-  __shared__ double s_t[kWarps][32];
-  __shared__ int s_kb[kWarps][32];
+    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
+  constexpr int GQ = 32 * QL;  // queries per warp group
+  __shared__ int64_t s_start[kWarps][GQ];
+  __shared__ int64_t s_u[kWarps][GQ];
+  __shared__ double s_t[kWarps][GQ];
+  __shared__ int s_kb[kWarps][GQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = ASSEMBLE ? l : static_cast<int>(k);
-  const int64_t ngroups = ceil_div(Q, 32);
+  const int64_t ngroups = ceil_div(Q, GQ);
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
        g += static_cast<int64_t>(gridDim.x) * kWarps) {
-    const int64_t q = g * 32 + lane;
-    int64_t start = 0, u = 0;
-    double t = 0.0;
-    int kb = -1;  // -1: absent (hop-2 padding) -> zero row, valid_len 0
-    if (q < Q && fetch_query(in, q, u, t)) {
-      const int64_t lo = ldg_i64(indptr + u), hi = ldg_i64(indptr + u + 1);
-      const int64_t m = prefix_end(ts, lo, hi - lo, t);
-      const int64_t take = min(k, m);
-      kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
-      start = lo + m - kb;
+    int64_t u[QL], lo[QL], n[QL], m[QL];
+    double t[QL];
+    bool pres[QL];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      u[j] = 0;
+      t[j] = 0.0;
+      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
     }
-    if (q < Q) {
-      if (ASSEMBLE)
-        write_vlen<IDX64>(o, q, kb + 1);
-      else
-        o.counts[q] = max(kb, 0);
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
+      n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
     }
-    s_start[warp][lane] = start;
-    s_u[warp][lane] = u;
-    s_t[warp][lane] = t;
-    s_kb[warp][lane] = kb;
+    search_interleaved<QL>(ts, lo, n, t, m);
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      int kb = -1;  // -1: absent (hop-2 padding) -> zero row, valid_len 0
+      if (pres[j]) {
+        const int64_t take = min(k, m[j]);
+        kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
+      }
+      if (q < Q) {
+        if (ASSEMBLE)
+          write_vlen<IDX64>(o, q, kb + 1);
+        else
+          o.counts[q] = max(kb, 0);
+      }
+      const int qi = j * 32 + lane;
+      s_start[warp][qi] = lo[j] + m[j] - kb;
+      s_u[warp][qi] = u[j];
+      s_t[warp][qi] = t[j];
+      s_kb[warp][qi] = kb;
+    }
     __syncwarp();
-    const int64_t qbase = g * 32;
-    const int nq = static_cast<int>(min((int64_t)32, Q - qbase));
+    const int64_t qbase = g * GQ;
+    const int nq = static_cast<int>(min(static_cast<int64_t>(GQ), Q - qbase));
     const int total = nq * width;
     const int64_t obase = qbase * width;
-#pragma unroll 4
+#pragma unroll 8
     for (int s = lane; s < total; s += 32) {
-      const int qi = s / width;
+      const int qi = div_slot(s, width, magic);
       const int j = s - qi * width;
       const int kbq = s_kb[warp][qi];
       if (ASSEMBLE) {
@@ -170,6 +222,120 @@ __global__ void __launch_bounds__(kThreads) k_recent(
         o.e_nbr[obase + s] = a;
         o.e_eid[obase + s] = b;
         o.e_ts[obase + s] = c;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ recent-k, split form
+// Phase A (k_recent_search): QL interleaved searches per lane, writes the kept window of each
+// query packed as (start << 8 | kb) -- kb = -1 (0xff) marks an absent hop-2 slot.
+// Phase B (k_recent_gather): streaming gather + suffix-infill packing over the packed windows;
+// no search latency on its path, so every warp keeps its loads in flight.
+template <bool ASSEMBLE, int QL>
+__global__ void __launch_bounds__(kThreads) k_recent_search(
+    const int64_t* __restrict__ indptr, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, uint64_t* __restrict__ win) {
+  constexpr int GQ = 32 * QL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ngroups = ceil_div(Q, GQ);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+    int64_t u[QL], lo[QL], n[QL], m[QL];
+    double t[QL];
+    bool pres[QL];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      u[j] = 0;
+      t[j] = 0.0;
+      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
+      n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
+    }
+    search_interleaved<QL>(ts, lo, n, t, m);
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      if (q < Q) {
+        uint64_t w = 0xffull;  // absent
+        if (pres[j]) {
+          const int64_t take = min(k, m[j]);
+          const int kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
+          w = (static_cast<uint64_t>(lo[j] + m[j] - kb) << 8) | static_cast<uint64_t>(kb);
+        }
+        win[q] = w;
+      }
+    }
+  }
+}
+
+template <bool ASSEMBLE, bool IDX64>
+__global__ void __launch_bounds__(kThreads) k_recent_gather(
+    const int64_t* __restrict__ nbr, const int64_t* __restrict__ eid,
+    const double* __restrict__ ts, QueryIn in, int64_t Q, int64_t k, int l, int64_t self_idx,
+    uint32_t magic, const uint64_t* __restrict__ win, Outs o) {
+  constexpr int GQ = 32;  // queries per warp group
+  __shared__ int64_t s_start[kWarps][GQ];
+  __shared__ int64_t s_u[kWarps][GQ];
+  __shared__ double s_t[kWarps][GQ];
+  __shared__ int s_kb[kWarps][GQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int width = ASSEMBLE ? l : static_cast<int>(k);
+  const int64_t ngroups = ceil_div(Q, GQ);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const int64_t q = g * GQ + lane;
+    if (q < Q) {
+      const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(win) + q);
+      const int kb = (w & 0xff) == 0xff ? -1 : static_cast<int>(w & 0xff);
+      s_kb[warp][lane] = kb;
+      s_start[warp][lane] = static_cast<int64_t>(w >> 8);
+      s_u[warp][lane] = kb >= 0 || ASSEMBLE ? (kb >= 0 ? ldg_i64(in.nodes + q) : 0) : 0;
+      s_t[warp][lane] = kb >= 0 ? ldg_f64(in.times + q) : 0.0;
+      if (ASSEMBLE)
+        write_vlen<IDX64>(o, q, kb + 1);
+      else
+        o.counts[q] = max(kb, 0);
+    }
+    __syncwarp();
+    const int nq = static_cast<int>(min(static_cast<int64_t>(GQ), Q - g * GQ));
+    const int total = nq * width;
+    const int64_t obase = g * GQ * width;
+#pragma unroll 4
+    for (int sl = lane; sl < total; sl += 32) {
+      const int qi = div_slot(sl, width, magic);
+      const int j = sl - qi * width;
+      const int kbq = s_kb[warp][qi];
+      if (ASSEMBLE) {
+        int64_t ni = 0, ei = 0;
+        double dt = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          ni = ldg_i64(nbr + p) + 1;
+          ei = ldg_i64(eid + p) + 1;
+          dt = s_t[warp][qi] - ldg_f64(ts + p);
+        } else if (j == kbq) {
+          ni = s_u[warp][qi] + 1;
+          ei = self_idx;
+        }
+        write_slot<IDX64>(o, obase + sl, ni, ei, dt);
+      } else {
+        int64_t a = 0, b = 0;
+        double c = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          a = ldg_i64(nbr + p);
+          b = ldg_i64(eid + p);
+          c = ldg_f64(ts + p);
+        }
+        o.e_nbr[obase + sl] = a;
+        o.e_eid[obase + sl] = b;
+        o.e_ts[obase + sl] = c;
       }
     }
     __syncwarp();
@@ -375,6 +541,29 @@ __global__ void k_mask(int64_t q, int64_t l, const int64_t* __restrict__ valid_l
   }
 }
 
+int recent_variant() {
+  static int v = [] {
+    const char* e = getenv("TGFX_RECENT_VARIANT");
+    return e ? atoi(e) : 10;
+  }();
+  return v;
+}
+
+
+// Several waves of blocks measured faster than a persistent (resident-only) grid for the
+// sampler: per-block work varies with the queried slices (hub searches), and small blocks
+// balance better.  TGFX_RECENT_WAVES overrides the blocks-per-SM cap (default: none).
+template <int QL, int MINB>
+int recent_grid(int64_t q, bool, bool) {
+  static const int64_t per_sm = [] {
+    const char* e = getenv("TGFX_RECENT_WAVES");
+    return e ? atoll(e) : (1LL << 30);  // uncapped: one 256-query group per warp
+  }();
+  const int64_t groups = ceil_div(std::max<int64_t>(q, 1), 32 * QL);
+  const int64_t blocks = ceil_div(groups, kWarps);
+  return static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(device_info().sms) * per_sm));
+}
+
 int grid_groups(int64_t Q) {
   const int64_t groups = ceil_div(std::max<int64_t>(Q, 1), 32);
   const int64_t blocks = ceil_div(groups, kWarps);
@@ -430,17 +619,56 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
   const bool assemble = a.l > 0;
   const int l = static_cast<int>(a.l);
   if (a.strategy == TGFX_RECENT) {
-    if (assemble) {
-      if (a.index64)
-        k_recent<true, true><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
-                                                       a.k, l, a.self_edge_index, o);
+    const int width = assemble ? l : static_cast<int>(a.k);
+    const uint32_t magic =
+        (width < 512) ? static_cast<uint32_t>(((1ull << 32) + width - 1) / width) : 0u;
+    const int variant = recent_variant();
+#define TGFX_RECENT_LAUNCH(QL, MINB)                                                           \
+  {                                                                                            \
+    const int rgrid = recent_grid<QL, MINB>(a.q, assemble, a.index64);                         \
+    if (assemble && a.index64)                                                                 \
+      k_recent<true, true, QL, MINB><<<rgrid, kThreads, 0, s>>>(                               \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);     \
+    else if (assemble)                                                                         \
+      k_recent<true, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                              \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);     \
+    else                                                                                       \
+      k_recent<false, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                             \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);                     \
+  }
+    const int64_t max_kb = assemble ? std::min<int64_t>(a.k, a.l - 1) : a.k;
+    if (variant >= 10 && max_kb < 255) {  // split search + gather (default)
+      constexpr int QLS = 4;
+      uint64_t* win = static_cast<uint64_t*>(dmalloc(sizeof(uint64_t) * a.q, s));
+      const int64_t sg = ceil_div(ceil_div(a.q, 32 * QLS), kWarps);
+      const int gs = static_cast<int>(std::min<int64_t>(sg, INT32_MAX));
+      if (assemble)
+        k_recent_search<true, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l, win);
       else
-        k_recent<true, false><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
-                                                        a.k, l, a.self_edge_index, o);
-    } else {
-      k_recent<false, false><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q,
-                                                       a.k, 0, 0, o);
+        k_recent_search<false, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0, win);
+      after_launch("k_recent_search");
+      const int gg = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));
+      if (assemble && a.index64)
+        k_recent_gather<true, true><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k, l,
+                                                             a.self_edge_index, magic, win, o);
+      else if (assemble)
+        k_recent_gather<true, false><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k, l,
+                                                              a.self_edge_index, magic, win, o);
+      else
+        k_recent_gather<false, false><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k,
+                                                               0, 0, magic, win, o);
+      after_launch("k_recent_gather");
+      dfree(win, s);
+      return;
     }
+    switch (variant >= 10 ? 4 : variant) {
+      case 1: TGFX_RECENT_LAUNCH(1, 4) break;
+      case 2: TGFX_RECENT_LAUNCH(2, 4) break;
+      case 3: TGFX_RECENT_LAUNCH(2, 3) break;
+      case 5: TGFX_RECENT_LAUNCH(4, 4) break;
+      default: TGFX_RECENT_LAUNCH(4, 3) break;
+    }
+#undef TGFX_RECENT_LAUNCH
     after_launch("k_recent");
     return;
   }
