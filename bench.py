@@ -322,7 +322,7 @@ def run_ours(args, cfg):
                   "frac": build_bytes / (build_med * 1e-3) / 1e9 / peak},
         "sample": {"ms": samp_med, "queries_per_s": q_local * ws / (samp_med * 1e-3),
                    "launches_per_step": len(chunks), "mean_taken": total_taken / Q},
-        "roofline": {"kernel": "k_recent (fused recent-k sampler + sequence packing)",
+        "roofline": {"kernel": "k_recent_line (fused recent-k line-probe sampler + sequence packing)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": bytes_per_launch,
@@ -360,7 +360,7 @@ def load_traffic(cfg, bytes_per_launch):
     try:
         with open(p) as f:
             d = json.load(f)
-        t = d["k_recent"]
+        t = d["k_recent_line"]
         return t["dram_bytes"] * bytes_per_launch / t["alg_bytes"]
     except Exception:
         return None

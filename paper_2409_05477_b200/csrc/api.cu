@@ -271,6 +271,17 @@ int tgfx_graph_from_host(int64_t num_nodes, int64_t num_edges, int reverse, int6
       }
       g->max_eid = mx;
       g->min_eid = mn;
+      // interpolation search needs every slice sorted by ts and NaN-free; otherwise the
+      // sampler replays std::lower_bound's bisection exactly (sampler.cpp:16-20)
+      bool ok = indptr[0] == 0 && indptr[num_nodes] == m;
+      for (int64_t u = 0; ok && u < num_nodes; ++u) {
+        const int64_t lo = indptr[u], hi = indptr[u + 1];
+        if (lo > hi || lo < 0 || hi > m) ok = false;
+        for (int64_t i = lo; ok && i < hi; ++i)
+          if (ts[i] != ts[i] || (i > lo && ts[i - 1] > ts[i])) ok = false;
+      }
+      g->search_exact = ok ? 0 : 1;
+      build_node_dir(g, s);
       TGFX_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
       free_graph(g);

@@ -45,6 +45,7 @@ constexpr int64_t kFastMaxNodes = 45000;
 __global__ void k_init_flags(BuildFlags* f) {
   f->bad_index = ~0ull;
   f->unsorted = 0;
+  f->has_nan = 0;
   f->max_eid = LLONG_MIN;
   f->min_eid = LLONG_MAX;
 }
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
   const int lane = threadIdx.x & 31;
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
   const int64_t e1 = min(n, e0 + chunk_ev);
-  bool unsorted = false;
+  bool unsorted = false, nan = false;
   unsigned long long bad = ~0ull;
   long long mx = LLONG_MIN, mn = LLONG_MAX;
   constexpr int U = 4;  // events per thread in flight
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
       const bool ok_d = valid && x.dst >= 0 && x.dst < V;
       if (valid && !(ok_s && ok_d)) bad = min(bad, (unsigned long long)e);
       if (valid) {
+        nan |= x.t != x.t;
         mx = max(mx, (long long)x.eid);
         mn = min(mn, (long long)x.eid);
       }
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
   }
   // flags: warp reduce then one atomic per warp
   unsorted = __any_sync(kFull, unsorted);
+  nan = __any_sync(kFull, nan);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     bad = min(bad, __shfl_xor_sync(kFull, bad, o));
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
   }
   if (lane == 0) {
     if (unsorted) atomicOr(&flags->unsorted, 1);
+    if (nan) atomicOr(&flags->has_nan, 1);
     if (bad != ~0ull) atomicMin(&flags->bad_index, bad);
     if (mx != LLONG_MIN) atomicMax(&flags->max_eid, mx);
     if (mn != LLONG_MAX) atomicMin(&flags->min_eid, mn);
@@ -448,6 +452,20 @@ __global__ void k_gather_entries(const tgfx_event* __restrict__ ev,
   }
 }
 
+// ------------------------------------------------------------------ node directory
+__global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __restrict__ ts,
+                           int64_t V, NodeDir* __restrict__ dir) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= V) return;
+  const int64_t a = indptr[u], b = indptr[u + 1];
+  NodeDir d;
+  d.start = a;
+  d.end = b;
+  d.t_first = b > a ? ts[a] : 0.0;
+  d.t_last = b > a ? ts[b - 1] : 0.0;
+  dir[u] = d;
+}
+
 // ------------------------------------------------------------------ validate (tcsr.cpp:54-81)
 __global__ void k_validate(const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
                            const int64_t* __restrict__ eid, const double* __restrict__ ts,
@@ -716,7 +734,9 @@ void graph_alloc(tgfx_graph* g, cudaStream_t s) {
   g->indptr = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (g->V + 1), s));
   g->nbr = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * mm, s));
   g->eid = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * mm, s));
-  g->ts = static_cast<double*>(dmalloc(sizeof(double) * mm, s));
+  g->ts = static_cast<double*>(dmalloc(sizeof(double) * (mm + kTsPad), s));
+  TGFX_CUDA(cudaMemsetAsync(g->ts + mm, 0, sizeof(double) * kTsPad, s));
+  g->dir = static_cast<NodeDir*>(dmalloc(sizeof(NodeDir) * std::max<int64_t>(g->V, 1), s));
   g->dflags = static_cast<BuildFlags*>(dmalloc(sizeof(BuildFlags), s));
   TGFX_CUDA(cudaMallocHost(&g->hflags, sizeof(BuildFlags)));
 }
@@ -728,12 +748,14 @@ void graph_release(tgfx_graph* g) {
   if (g->eid) dfree(g->eid, s);
   if (g->ts) dfree(g->ts, s);
   if (g->dflags) dfree(g->dflags, s);
+  if (g->dir) dfree(g->dir, s);
   if (g->ws) dfree(g->ws, s);
   if (g->ws_small) dfree(g->ws_small, s);
   if (g->ws_rec) dfree(g->ws_rec, s);
   if (g->hflags) cudaFreeHost(g->hflags);
   g->indptr = g->nbr = g->eid = nullptr;
   g->ts = nullptr;
+  g->dir = nullptr;
   g->dflags = nullptr;
   g->hflags = nullptr;
   g->ws = g->ws_small = g->ws_rec = nullptr;
@@ -772,6 +794,7 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   const tgfx_event* src = d_ev;
   tgfx_event* tmp = nullptr;
   g->path = fast ? 0 : 2;
+  g->search_exact = g->hflags->has_nan ? 1 : 0;
   if (g->hflags->unsorted) {
     tmp = sorted_copy(d_ev, n, s);
     src = tmp;
@@ -785,6 +808,13 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   else
     build_large(g, src, s);
   if (tmp) dfree(tmp, s);
+  build_node_dir(g, s);
+}
+
+void build_node_dir(tgfx_graph* g, cudaStream_t s) {
+  if (g->V <= 0) return;
+  k_node_dir<<<static_cast<int>(ceil_div(g->V, 256)), 256, 0, s>>>(g->indptr, g->ts, g->V, g->dir);
+  after_launch("k_node_dir");
 }
 
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {

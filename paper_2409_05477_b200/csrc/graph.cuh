@@ -7,9 +7,14 @@
 struct BuildFlags {
   unsigned long long bad_index;  // min stream index of an event with an endpoint out of range
   int unsorted;                  // stream is not (t, eid)-non-decreasing (or holds NaN times)
-  int pad;
+  int has_nan;                   // some timestamp is NaN
   long long max_eid;
   long long min_eid;
+};
+
+struct __align__(16) NodeDir {
+  int64_t start, end;
+  double t_first, t_last;
 };
 
 // proj/include/tgformer/tcsr.hpp:20-33 (TCsr), resident on one device.  SoA columns in HBM:
@@ -19,10 +24,17 @@ struct tgfx_graph {
   int64_t V = 0, n = 0, m = 0;
   int reverse = 1;
   int path = 0;  // 0 fast presorted, 1 general re-sort, 2 large-V radix
+  // 1: slices may not be sorted NaN-free (NaN timestamps, or imported from host unchecked), so
+  // the sampler replays std::lower_bound's exact bisection; 0: slices are sorted, any
+  // bracketing search (interpolation) returns the same lower_bound.
+  int search_exact = 0;
   int64_t* indptr = nullptr;
   int64_t* nbr = nullptr;
   int64_t* eid = nullptr;
-  double* ts = nullptr;
+  double* ts = nullptr;  // allocated with kTsPad trailing entries (line probes read whole lines)
+  // node directory, 32 B per node: {slice start, slice end, ts[start], ts[end-1]} -- one
+  // record gives the sampler both the slice bounds and the interpolation bracket
+  NodeDir* dir = nullptr;
   int64_t max_eid = -1, min_eid = 0;
   // build workspace, kept for rebuilds
   void* ws = nullptr;  // per-chunk node count / cursor table
@@ -43,6 +55,12 @@ int64_t fast_path_max_nodes();
 // Allocates the columns of g (V, n, reverse set by caller).
 void graph_alloc(tgfx_graph* g, cudaStream_t s);
 void graph_release(tgfx_graph* g);
+
+// trailing pad entries of the ts column (multiple of the widest line probe)
+constexpr int64_t kTsPad = 32;
+
+// (re)compute the node directory from indptr + ts (after a build or an import)
+void build_node_dir(tgfx_graph* g, cudaStream_t s);
 
 // Full build into g from device events; throws tgfx::Error on invalid input.
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted);

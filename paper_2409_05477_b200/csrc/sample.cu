@@ -29,19 +29,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-__device__ __forceinline__ int64_t prefix_end(const double* __restrict__ ts, int64_t lo,
-                                              int64_t n, double t) {
-  // std::lower_bound(ts+lo, ts+lo+n, t) - (ts+lo)
-  int64_t base = lo;
-  while (n > 0) {
-    const int64_t half = n >> 1;
-    const bool lt = __ldg(ts + base + half) < t;
-    base = lt ? base + half + 1 : base;
-    n = lt ? n - half - 1 : half;
-  }
-  return base - lo;
-}
-
 template <typename T>
 __device__ __forceinline__ void st(void* p, int64_t i, T v) {
   static_cast<T*>(p)[i] = v;
@@ -130,6 +117,95 @@ __device__ __forceinline__ void search_interleaved(const double* __restrict__ ts
   for (int j = 0; j < QL; ++j) m[j] = base[j] - lo[j];
 }
 
+// Safeguarded interpolation search, QL queries per lane interleaved.  Same result as
+// std::lower_bound on a sorted, NaN-free slice (any search that keeps the bracket
+// ts[lo-1] < t <= ts[hi] converges to the unique answer); the probe position is interpolated
+// from the bracket's values, and a step that fails to halve the bracket is followed by a
+// bisection step, so the probe count is at most ~2 log2(n) and ~log2 log2(n) on slices whose
+// timestamps grow roughly linearly (event streams).  Every probe is a dependent round trip to
+// L2/HBM, so fewer probes is the whole point: GDELT-shaped hub slices (78 M entries) take
+// ~27 bisection probes.
+template <int QL>
+__device__ __forceinline__ void search_interp(const double* __restrict__ ts,
+                                              const int64_t (&base)[QL], const int64_t (&n)[QL],
+                                              const double (&t)[QL], int64_t (&m)[QL]) {
+  int64_t lo[QL], hi[QL];
+  double vlo[QL], vhi[QL];
+  bool bis[QL];
+  // bracket values: first and last entry of every slice (independent loads)
+  double v0[QL], v1[QL];
+#pragma unroll
+  for (int j = 0; j < QL; ++j) {
+    v0[j] = n[j] > 0 ? __ldg(ts + base[j]) : 0.0;
+    v1[j] = n[j] > 1 ? __ldg(ts + base[j] + n[j] - 1) : v0[j];
+  }
+#pragma unroll
+  for (int j = 0; j < QL; ++j) {
+    bis[j] = false;
+    vlo[j] = v0[j];
+    vhi[j] = v1[j];
+    if (n[j] <= 0 || !(v0[j] < t[j])) {  // empty slice, t <= first, or NaN t -> 0
+      lo[j] = hi[j] = 0;
+    } else if (v1[j] < t[j]) {  // whole slice before t
+      lo[j] = hi[j] = n[j];
+    } else {  // ts[0] < t <= ts[n-1]: answer in [1, n-1]
+      lo[j] = 1;
+      hi[j] = n[j] - 1;
+    }
+  }
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < QL; ++j) any |= lo[j] < hi[j];
+    if (!any) break;
+    int64_t p[QL];
+    double v[QL];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t len = hi[j] - lo[j];
+      int64_t q = lo[j] + (len >> 1);
+      if (!bis[j]) {
+        // predicted answer under linear growth between ts[lo-1] = vlo and ts[hi] = vhi
+        // (fp32 fast divide: the probe position only steers the search, never its result)
+        const float f = __fdividef(static_cast<float>(t[j] - vlo[j]),
+                                   static_cast<float>(vhi[j] - vlo[j]));  // (0, 1] if finite
+        if (f >= 0.0f && f <= 1.0f)
+          q = lo[j] - 1 + static_cast<int64_t>(static_cast<double>(f) *
+                                               static_cast<double>(len + 1));
+        q = max(lo[j], min(q, hi[j] - 1));
+      }
+      p[j] = q;
+      v[j] = len > 0 ? __ldg(ts + base[j] + q) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t len = hi[j] - lo[j];
+      if (len > 0) {
+        if (v[j] < t[j]) {
+          lo[j] = p[j] + 1;
+          vlo[j] = v[j];
+        } else {
+          hi[j] = p[j];
+          vhi[j] = v[j];
+        }
+        bis[j] = !bis[j] && 2 * (hi[j] - lo[j]) > len;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QL; ++j) m[j] = lo[j];
+}
+
+template <int QL>
+__device__ __forceinline__ void search(bool exact, const double* __restrict__ ts,
+                                       const int64_t (&lo)[QL], int64_t (&n)[QL],
+                                       const double (&t)[QL], int64_t (&m)[QL]) {
+  if (exact)
+    search_interleaved<QL>(ts, lo, n, t, m);
+  else
+    search_interp<QL>(ts, lo, n, t, m);
+}
+
 // floor(s / w) for s < 2^16 via a 32-bit multiply-high (magic = ceil(2^32 / w)), else divide
 __device__ __forceinline__ int div_slot(int s, int w, uint32_t magic) {
   return magic ? static_cast<int>(__umulhi(static_cast<uint32_t>(s), magic)) : s / w;
@@ -140,7 +216,7 @@ template <bool ASSEMBLE, bool IDX64, int QL, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent(
     const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint32_t magic, int exact, Outs o) {
   constexpr int GQ = 32 * QL;  // queries per warp group
   __shared__ int64_t s_start[kWarps][GQ];
   __shared__ int64_t s_u[kWarps][GQ];
@@ -166,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
       lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
       n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
     }
-    search_interleaved<QL>(ts, lo, n, t, m);
+    search<QL>(exact != 0, ts, lo, n, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
       const int64_t q = g * GQ + j * 32 + lane;
@@ -236,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
 template <bool ASSEMBLE, int QL>
 __global__ void __launch_bounds__(kThreads) k_recent_search(
     const int64_t* __restrict__ indptr, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, uint64_t* __restrict__ win) {
+    int64_t k, int l, int exact, uint64_t* __restrict__ win) {
   constexpr int GQ = 32 * QL;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ngroups = ceil_div(Q, GQ);
@@ -257,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) k_recent_search(
       lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
       n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
     }
-    search_interleaved<QL>(ts, lo, n, t, m);
+    search<QL>(exact != 0, ts, lo, n, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
       const int64_t q = g * GQ + j * 32 + lane;
@@ -270,6 +346,351 @@ __global__ void __launch_bounds__(kThreads) k_recent_search(
         }
         win[q] = w;
       }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ recent-k, line probes
+// Default recent-k kernel.  Per query the dependent round trips are
+//   (1) node, time          coalesced
+//   (2) node directory      one 32-byte record: slice bounds + ts of its first and last entry,
+//                           i.e. the interpolation bracket comes with the bounds
+//   (3..) line probes       each probe reads the W-entry aligned ts line (W*8 bytes, 16-byte
+//                           vector loads) around the interpolated position and resolves the
+//                           whole line against t: either the answer is inside the line (done)
+//                           or the bracket shrinks to the line's edge.  A probe that fails to
+//                           halve the bracket is followed by a bisection probe, so the result
+//                           is exactly std::lower_bound's on the sorted slice.
+//   (last) window gather    suffix-infill rows written slot-parallel (coalesced), as k_recent.
+// On the GDELT-shaped workload this is ~3 probe rounds per query on average (vs ~13 for
+// bisection and ~7 for point interpolation), and ~5.5 for the slowest lane of a warp.
+template <int W, int QL>
+__device__ __forceinline__ void search_lines(const double* __restrict__ ts, const NodeDir (&d)[QL],
+                                             const bool (&pres)[QL], const double (&t)[QL],
+                                             int64_t (&m)[QL]) {
+  int64_t lo[QL], hi[QL];
+  double vlo[QL], vhi[QL];
+  bool bis[QL];
+#pragma unroll
+  for (int j = 0; j < QL; ++j) {
+    const int64_t n = d[j].end - d[j].start;
+    bis[j] = false;
+    vlo[j] = d[j].t_first;
+    vhi[j] = d[j].t_last;
+    if (!pres[j] || n <= 0 || !(d[j].t_first < t[j])) {  // empty, t <= first, NaN t
+      lo[j] = hi[j] = 0;
+    } else if (d[j].t_last < t[j]) {
+      lo[j] = hi[j] = n;
+    } else {
+      lo[j] = 1;
+      hi[j] = n - 1;
+    }
+  }
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < QL; ++j) any |= lo[j] < hi[j];
+    if (!any) break;
+    int64_t a[QL], b[QL], A[QL];
+    double v[QL][W];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t len = hi[j] - lo[j];
+      int64_t p = lo[j] + (len >> 1);
+      if (!bis[j]) {
+        const float f = __fdividef(static_cast<float>(t[j] - vlo[j]),
+                                   static_cast<float>(vhi[j] - vlo[j]));
+        if (f >= 0.0f && f <= 1.0f)
+          p = lo[j] - 1 + static_cast<int64_t>(static_cast<double>(f) * static_cast<double>(len + 1));
+        p = max(lo[j], min(p, hi[j] - 1));
+      }
+      A[j] = (d[j].start + p) & ~static_cast<int64_t>(W - 1);  // aligned line (absolute)
+      a[j] = max(A[j] - d[j].start, lo[j]);
+      b[j] = min(A[j] - d[j].start + W, hi[j]);
+      if (len > 0) {
+        const double2* src = reinterpret_cast<const double2*>(ts + A[j]);
+#pragma unroll
+        for (int w = 0; w < W / 2; ++w) {
+          const double2 x = __ldg(src + w);
+          v[j][2 * w] = x.x;
+          v[j][2 * w + 1] = x.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t len = hi[j] - lo[j];
+      if (len > 0) {
+        const int64_t r0 = A[j] - d[j].start;  // relative index of line entry 0
+        int c = 0;
+        double first = 0.0, last = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const bool in = r0 + w >= a[j] && r0 + w < b[j];
+          c += (in && v[j][w] < t[j]) ? 1 : 0;
+          if (r0 + w == a[j]) first = v[j][w];
+          if (r0 + w == b[j] - 1) last = v[j][w];
+        }
+        const int64_t span = b[j] - a[j];
+        if (c == span) {
+          lo[j] = b[j];
+          vlo[j] = last;
+        } else if (c == 0) {
+          hi[j] = a[j];
+          vhi[j] = first;
+        } else {
+          lo[j] = hi[j] = a[j] + c;
+        }
+        bis[j] = !bis[j] && 2 * (hi[j] - lo[j]) > len;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QL; ++j) m[j] = lo[j];
+}
+
+template <bool ASSEMBLE, bool IDX64, int W, int QL>
+__global__ void __launch_bounds__(kThreads) k_recent_line(
+    const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
+  constexpr int GQ = 32 * QL;
+  __shared__ int64_t s_start[kWarps][GQ];
+  __shared__ int64_t s_u[kWarps][GQ];
+  __shared__ double s_t[kWarps][GQ];
+  __shared__ int s_kb[kWarps][GQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int width = ASSEMBLE ? l : static_cast<int>(k);
+  const int64_t ngroups = ceil_div(Q, GQ);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+    int64_t u[QL], m[QL];
+    double t[QL];
+    bool pres[QL];
+    NodeDir d[QL];
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      u[j] = 0;
+      t[j] = 0.0;
+      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      if (pres[j]) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[j]);
+        const longlong2 x = __ldg(p), y = __ldg(p + 1);
+        d[j].start = x.x;
+        d[j].end = x.y;
+        d[j].t_first = __longlong_as_double(y.x);
+        d[j].t_last = __longlong_as_double(y.y);
+      } else {
+        d[j].start = d[j].end = 0;
+        d[j].t_first = d[j].t_last = 0.0;
+      }
+    }
+    search_lines<W, QL>(ts, d, pres, t, m);
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = g * GQ + j * 32 + lane;
+      int kb = -1;  // -1: absent (hop-2 padding) -> zero row, valid_len 0
+      if (pres[j]) {
+        const int64_t take = min(k, m[j]);
+        kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
+      }
+      if (q < Q) {
+        if (ASSEMBLE)
+          write_vlen<IDX64>(o, q, kb + 1);
+        else
+          o.counts[q] = max(kb, 0);
+      }
+      const int qi = j * 32 + lane;
+      s_start[warp][qi] = d[j].start + m[j] - kb;
+      s_u[warp][qi] = u[j];
+      s_t[warp][qi] = t[j];
+      s_kb[warp][qi] = kb;
+    }
+    __syncwarp();
+    const int64_t qbase = g * GQ;
+    const int nq = static_cast<int>(min(static_cast<int64_t>(GQ), Q - qbase));
+    const int total = nq * width;
+    const int64_t obase = qbase * width;
+#pragma unroll 4
+    for (int s = lane; s < total; s += 32) {
+      const int qi = div_slot(s, width, magic);
+      const int j = s - qi * width;
+      const int kbq = s_kb[warp][qi];
+      if (ASSEMBLE) {
+        int64_t ni = 0, ei = 0;
+        double dt = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          ni = ldg_i64(nbr + p) + 1;
+          ei = ldg_i64(eid + p) + 1;
+          dt = s_t[warp][qi] - ldg_f64(ts + p);
+        } else if (j == kbq) {
+          ni = s_u[warp][qi] + 1;
+          ei = self_idx;
+        }
+        write_slot<IDX64>(o, obase + s, ni, ei, dt);
+      } else {
+        int64_t a = 0, b = 0;
+        double c = 0.0;
+        if (j < kbq) {
+          const int64_t p = s_start[warp][qi] + j;
+          a = ldg_i64(nbr + p);
+          b = ldg_i64(eid + p);
+          c = ldg_f64(ts + p);
+        }
+        o.e_nbr[obase + s] = a;
+        o.e_eid[obase + s] = b;
+        o.e_ts[obase + s] = c;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Phase A, work-queue form (experimental variant 20).  The search's probe count varies a lot between
+// queries (empty slice: 0; GDELT hub: ~8 interpolation probes, up to ~25), and a warp that
+// runs 32 searches in lockstep waits for its slowest lane.  Here every lane is a small state
+// machine that takes the next query of its warp's block as soon as its current one finishes,
+// so a warp's time is the SUM of its lanes' probe chains / 32, not their max.  Each loop
+// iteration every lane issues the (at most two, independent) loads of its current state, then
+// consumes them:
+//   FETCH   node, time of query q            (hop-2 mode: HOPCHK first: is slot j present?)
+//   IPTR    indptr[u], indptr[u+1]
+//   BRACKET ts[first], ts[last] of the slice  (skipped in exact mode)
+//   SEARCH  one probe (interpolated, or bisection after a step that did not halve the range;
+//           exact mode: std::lower_bound's own midpoints)
+// and on convergence writes the packed window (start << 8 | kb) of query q.
+enum : int { kNeed = 0, kHopChk, kFetch, kIptr, kBracket, kSearch };
+
+template <bool ASSEMBLE>
+__global__ void __launch_bounds__(kThreads) k_recent_search_q(
+    const int64_t* __restrict__ indptr, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, int exact, uint64_t* __restrict__ win) {
+  constexpr int64_t kBlk = 256;  // queries per warp block
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t nblk = ceil_div(Q, kBlk);
+  int64_t blk = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  int64_t cur = blk * kBlk, end = min(Q, cur + kBlk);
+  const int64_t cap = ASSEMBLE ? min(k, static_cast<int64_t>(l - 1)) : k;
+  int st = kNeed;
+  int64_t q = 0, base = 0, lo = 0, hi = 0;
+  double t = 0.0, vlo = 0.0, vhi = 0.0;
+  bool bis = exact != 0;
+  while (true) {
+    // hand out queries of the warp's block to idle lanes (warp-uniform bookkeeping)
+    unsigned need = __ballot_sync(kFull, st == kNeed);
+    while (need && blk < nblk) {
+      const int64_t take = min(static_cast<int64_t>(__popc(need)), end - cur);
+      const int r = __popc(need & lanemask_lt());
+      if (st == kNeed && r < take) {
+        q = cur + r;
+        st = in.hop_counts ? kHopChk : kFetch;
+      }
+      cur += take;
+      if (cur >= end) {
+        blk += nwarps;
+        cur = blk * kBlk;
+        end = min(Q, cur + kBlk);
+      }
+      need = __ballot_sync(kFull, st == kNeed);
+    }
+    if (need == kFull) break;  // every lane idle and no blocks left
+    // load phase: one or two independent 8-byte loads per lane
+    const unsigned long long* pa = nullptr;
+    const unsigned long long* pb = nullptr;
+    int64_t p = 0;
+    if (st == kHopChk) {
+      pa = reinterpret_cast<const unsigned long long*>(in.hop_counts + q / in.hop_k1);
+    } else if (st == kFetch) {
+      pa = reinterpret_cast<const unsigned long long*>(in.nodes + q);
+      pb = reinterpret_cast<const unsigned long long*>(in.times + q);
+    } else if (st == kIptr) {
+      pa = reinterpret_cast<const unsigned long long*>(indptr + base);  // base holds u here
+      pb = pa + 1;
+    } else if (st == kBracket) {
+      pa = reinterpret_cast<const unsigned long long*>(ts + base);
+      pb = reinterpret_cast<const unsigned long long*>(ts + base + hi);  // hi holds n-1
+    } else if (st == kSearch) {
+      const int64_t len = hi - lo;
+      p = lo + (len >> 1);
+      if (!bis) {
+        // predicted answer under linear growth between ts[lo-1] = vlo and ts[hi] = vhi
+        const float f = __fdividef(static_cast<float>(t - vlo), static_cast<float>(vhi - vlo));
+        if (f >= 0.0f && f <= 1.0f)
+          p = lo - 1 + static_cast<int64_t>(static_cast<double>(f) * static_cast<double>(len + 1));
+        p = max(lo, min(p, hi - 1));
+      }
+      pa = reinterpret_cast<const unsigned long long*>(ts + base + p);
+    }
+    const unsigned long long va = pa ? __ldg(pa) : 0ull;
+    const unsigned long long vb = pb ? __ldg(pb) : 0ull;
+    // consume phase
+    bool done = false;
+    if (st == kHopChk) {
+      const int64_t j = q - (q / in.hop_k1) * in.hop_k1;
+      if (j >= static_cast<int64_t>(va)) {  // absent hop-2 slot
+        win[q] = 0xffull;
+        st = kNeed;
+      } else {
+        st = kFetch;
+      }
+    } else if (st == kFetch) {
+      base = static_cast<int64_t>(va);
+      t = __longlong_as_double(static_cast<long long>(vb));
+      st = kIptr;
+    } else if (st == kIptr) {
+      base = static_cast<int64_t>(va);
+      const int64_t n = static_cast<int64_t>(vb) - base;
+      lo = 0;
+      if (n <= 0) {
+        hi = 0;
+        done = true;
+      } else if (exact) {
+        hi = n;
+        st = kSearch;
+      } else {
+        hi = n - 1;
+        st = kBracket;
+      }
+    } else if (st == kBracket) {
+      const double v0 = __longlong_as_double(static_cast<long long>(va));
+      const double v1 = __longlong_as_double(static_cast<long long>(vb));
+      const int64_t n = hi + 1;
+      vlo = v0;
+      vhi = v1;
+      bis = false;
+      if (!(v0 < t)) {  // t <= first entry, or NaN t
+        lo = hi = 0;
+      } else if (v1 < t) {  // whole slice before t
+        lo = hi = n;
+      } else {  // ts[0] < t <= ts[n-1]
+        lo = 1;
+        hi = n - 1;
+      }
+      done = lo >= hi;
+      st = kSearch;
+    } else if (st == kSearch) {
+      const int64_t len = hi - lo;
+      const double v = __longlong_as_double(static_cast<long long>(va));
+      if (v < t) {
+        lo = p + 1;
+        vlo = v;
+      } else {
+        hi = p;
+        vhi = v;
+      }
+      if (!exact) bis = !bis && 2 * (hi - lo) > len;
+      done = lo >= hi;
+    }
+    if (done) {
+      const int kb = static_cast<int>(min(cap, lo));
+      win[q] = (static_cast<uint64_t>(base + lo - kb) << 8) | static_cast<uint64_t>(kb);
+      st = kNeed;
     }
   }
 }
@@ -347,7 +768,8 @@ template <int P, bool ASSEMBLE, bool IDX64>
 __global__ void __launch_bounds__(kThreads) k_random(
     const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, int exact,
+    Outs o) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ngroups = ceil_div(Q, 32);
   const int kk = static_cast<int>(k);
@@ -361,8 +783,12 @@ __global__ void __launch_bounds__(kThreads) k_random(
     if (q < Q && fetch_query(in, q, u, t)) {
       present = true;
       lo = ldg_i64(indptr + u);
-      const int64_t hi = ldg_i64(indptr + u + 1);
-      m = prefix_end(ts, lo, hi - lo, t);
+    }
+    {
+      int64_t lo1[1] = {lo}, n1[1] = {present ? ldg_i64(indptr + u + 1) - lo : 0}, m1[1];
+      const double t1[1] = {t};
+      search<1>(exact != 0, ts, lo1, n1, t1, m1);
+      m = m1[0];
     }
     const int nq = static_cast<int>(min((int64_t)32, Q - g * 32));
     for (int qi = 0; qi < nq; ++qi) {
@@ -544,7 +970,7 @@ __global__ void k_mask(int64_t q, int64_t l, const int64_t* __restrict__ valid_l
 int recent_variant() {
   static int v = [] {
     const char* e = getenv("TGFX_RECENT_VARIANT");
-    return e ? atoi(e) : 10;
+    return e ? atoi(e) : 30;
   }();
   return v;
 }
@@ -579,7 +1005,7 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
   case PP:                                                                                   \
     k_random<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q, \
                                                      a.k, l, a.self_edge_index, a.seed,      \
-                                                     a.stream_base, o);                     \
+                                                     a.stream_base, g->search_exact, o);    \
     break;
   switch (P) {
     TGFX_RANDOM_CASE(1)
@@ -628,25 +1054,72 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     const int rgrid = recent_grid<QL, MINB>(a.q, assemble, a.index64);                         \
     if (assemble && a.index64)                                                                 \
       k_recent<true, true, QL, MINB><<<rgrid, kThreads, 0, s>>>(                               \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);     \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic,          \
+          g->search_exact, o);                                                                 \
     else if (assemble)                                                                         \
       k_recent<true, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                              \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);     \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic,          \
+          g->search_exact, o);                                                                 \
     else                                                                                       \
       k_recent<false, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                             \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);                     \
+          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, g->search_exact, o);    \
   }
+    if (variant >= 30 && !g->search_exact) {  // line-probe kernel (default)
+#define TGFX_LINE_LAUNCH(W, QL)                                                                 \
+  {                                                                                             \
+    const int gl = static_cast<int>(                                                            \
+        std::min<int64_t>(ceil_div(ceil_div(a.q, 32 * QL), kWarps), INT32_MAX));                \
+    if (assemble && a.index64)                                                                  \
+      k_recent_line<true, true, W, QL><<<gl, kThreads, 0, s>>>(                                 \
+          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
+    else if (assemble)                                                                          \
+      k_recent_line<true, false, W, QL><<<gl, kThreads, 0, s>>>(                                \
+          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
+    else                                                                                        \
+      k_recent_line<false, false, W, QL><<<gl, kThreads, 0, s>>>(                               \
+          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);                         \
+  }
+      switch (variant) {
+        case 31: TGFX_LINE_LAUNCH(16, 1) break;
+        case 32: TGFX_LINE_LAUNCH(8, 2) break;
+        case 33: TGFX_LINE_LAUNCH(16, 2) break;
+        case 34: TGFX_LINE_LAUNCH(4, 2) break;
+        default: TGFX_LINE_LAUNCH(8, 1) break;
+      }
+#undef TGFX_LINE_LAUNCH
+      after_launch("k_recent_line");
+      return;
+    }
     const int64_t max_kb = assemble ? std::min<int64_t>(a.k, a.l - 1) : a.k;
     if (variant >= 10 && max_kb < 255) {  // split search + gather (default)
       constexpr int QLS = 4;
       uint64_t* win = static_cast<uint64_t*>(dmalloc(sizeof(uint64_t) * a.q, s));
       const int64_t sg = ceil_div(ceil_div(a.q, 32 * QLS), kWarps);
       const int gs = static_cast<int>(std::min<int64_t>(sg, INT32_MAX));
-      if (assemble)
-        k_recent_search<true, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l, win);
-      else
-        k_recent_search<false, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0, win);
-      after_launch("k_recent_search");
+      if (variant >= 20) {  // work-queue search (default)
+        static const int gq = [] {
+          int bps = 0;
+          TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_recent_search_q<true>,
+                                                                  kThreads, 0));
+          return std::max(bps, 1) * device_info().sms;
+        }();
+        const int gsq = static_cast<int>(std::min<int64_t>(gq, ceil_div(ceil_div(a.q, 256), kWarps)));
+        if (assemble)
+          k_recent_search_q<true><<<gsq, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l,
+                                                            g->search_exact, win);
+        else
+          k_recent_search_q<false><<<gsq, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0,
+                                                             g->search_exact, win);
+        after_launch("k_recent_search_q");
+      } else {
+        if (assemble)
+          k_recent_search<true, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l,
+                                                              g->search_exact, win);
+        else
+          k_recent_search<false, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0,
+                                                               g->search_exact, win);
+        after_launch("k_recent_search");
+      }
       const int gg = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));
       if (assemble && a.index64)
         k_recent_gather<true, true><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k, l,

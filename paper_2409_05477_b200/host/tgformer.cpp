@@ -1,0 +1,481 @@
+// tgformer.cpp -- C++ host layer (include/tgfx/tgformer.hpp) over the C ABI (include/tgfx.h).
+//
+// Each function here replaces the reference function of the same name and keeps its
+// argument meaning, return values and exception types; the arithmetic runs in libtgfx's
+// sm_100a kernels.  The only host-side work is marshalling (vectors <-> pinned/device
+// buffers), the argument checks the reference does before computing, and the TCSR container
+// file I/O.  Reference locations are relative to the reference tree (proj/...).
+#include "tgfx/tgformer.hpp"
+
+#include <zlib.h>
+
+#include <algorithm>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+
+namespace tgf {
+
+namespace detail {
+
+// Rethrow a libtgfx status as the reference's exception type (common.hpp:15-27).
+void check(int rc) {
+  if (rc == TGFX_OK) return;
+  const std::string msg = tgfx_last_error();
+  if (rc == TGFX_EVALIDATION) throw ValidationError(msg);
+  if (rc == TGFX_EFORMAT) throw FormatError(msg);
+  if (rc == TGFX_ENOMEM) throw std::bad_alloc();
+  throw std::runtime_error(msg);
+}
+
+// Content fingerprint of the host columns: full FNV-1a over small graphs, a strided sample
+// plus the sizes over large ones.  Detects a TCsr whose columns were replaced or edited after
+// its device copy was made (the reference treats TCsr as immutable).
+std::uint64_t fingerprint(const TCsr& g) {
+  std::uint64_t h = 1469598103934665603ULL;
+  auto mixin = [&](std::uint64_t x) {
+    h ^= x;
+    h *= 1099511628211ULL;
+  };
+  mixin(static_cast<std::uint64_t>(g.num_nodes));
+  mixin(static_cast<std::uint64_t>(g.num_edges));
+  mixin(g.reverse ? 1 : 0);
+  auto cols = [&](const void* p, std::size_t n) {
+    mixin(n);
+    const auto* w = static_cast<const std::uint64_t*>(p);
+    const std::size_t step = n <= (1u << 16) ? 1 : n / 4096;
+    for (std::size_t i = 0; i < n; i += step) mixin(w[i] + i);
+    if (n) mixin(w[n - 1]);
+  };
+  cols(g.indptr.data(), g.indptr.size());
+  cols(g.neighbor_ids.data(), g.neighbor_ids.size());
+  cols(g.edge_ids.data(), g.edge_ids.size());
+  cols(g.timestamps.data(), g.timestamps.size());
+  return h;
+}
+
+struct DeviceCopy {
+  std::mutex mu;
+  tgfx_graph* handle = nullptr;
+  std::uint64_t fp = 0;
+  std::int64_t max_degree = 0;
+  ~DeviceCopy() {
+    if (handle) tgfx_graph_free(handle);
+  }
+};
+
+std::int64_t max_degree(const TCsr& g) {
+  std::int64_t d = 0;
+  for (std::size_t u = 0; u + 1 < g.indptr.size(); ++u) d = std::max(d, g.indptr[u + 1] - g.indptr[u]);
+  return d;
+}
+
+void attach(const TCsr& g, tgfx_graph* h) {
+  auto dc = std::make_shared<DeviceCopy>();
+  dc->handle = h;
+  dc->fp = fingerprint(g);
+  dc->max_degree = max_degree(g);
+  g.device_copy = std::move(dc);
+}
+
+// Upload a TCsr that has no (or a stale) device copy.  The shape checks are TCsr::validate's
+// (tcsr.cpp:54-61), done before touching the columns.
+tgfx_graph* upload(const TCsr& g) {
+  if (g.indptr.size() != static_cast<std::size_t>(g.num_nodes) + 1)
+    throw ValidationError("indptr size mismatch");
+  if (g.edge_ids.size() != g.neighbor_ids.size() || g.timestamps.size() != g.neighbor_ids.size())
+    throw ValidationError("column arrays disagree in length");
+  tgfx_graph* h = nullptr;
+  const std::int64_t m = g.num_entries();
+  // the device handle stores num_edges * (1 + reverse) entries; a hand-made TCsr may not
+  // follow that rule, so describe it by its entry count
+  const int rev = (m == 2 * g.num_edges && m > 0) ? 1 : (m == g.num_edges ? 0 : -1);
+  if (rev < 0) {
+    // entries do not follow the builder's n*(1+reverse) shape: store as a non-reverse graph of
+    // m "events" (sampling only reads the columns; validate() checks ids against num_edges)
+    check(tgfx_graph_from_host(g.num_nodes, m, 0, m, g.indptr.data(), g.neighbor_ids.data(),
+                               g.edge_ids.data(), g.timestamps.data(), &h));
+  } else {
+    check(tgfx_graph_from_host(g.num_nodes, g.num_edges, rev, m, g.indptr.data(),
+                               g.neighbor_ids.data(), g.edge_ids.data(), g.timestamps.data(), &h));
+  }
+  return h;
+}
+
+DeviceCopy& device_of(const TCsr& g) {
+  std::shared_ptr<DeviceCopy> dc = g.device_copy;
+  if (!dc || dc->fp != fingerprint(g)) {
+    attach(g, upload(g));
+    dc = g.device_copy;
+  }
+  return *dc;
+}
+
+}  // namespace detail
+
+// ------------------------------------------------------------------ event stream
+void EventStream::validate() const {
+  // event_stream.cpp:62-83
+  const std::int64_t n = size();
+  for (std::int64_t i = 0; i < n; ++i) {
+    const TemporalEvent& e = events[static_cast<std::size_t>(i)];
+    if (e.src < 0 || e.src >= num_nodes || e.dst < 0 || e.dst >= num_nodes)
+      throw ValidationError("event " + std::to_string(i) + ": node id out of range");
+    if (i > 0 && events[static_cast<std::size_t>(i - 1)].timestamp > e.timestamp)
+      throw ValidationError("events not sorted by timestamp at index " + std::to_string(i));
+  }
+  if (!edge_features.empty() && (edge_features.rows() != static_cast<std::size_t>(n) ||
+                                 edge_features.cols() != static_cast<std::size_t>(d_e)))
+    throw ValidationError("edge feature matrix shape mismatch");
+  if (!node_features.empty() && (node_features.rows() != static_cast<std::size_t>(num_nodes) ||
+                                 node_features.cols() != static_cast<std::size_t>(d_v)))
+    throw ValidationError("node feature matrix shape mismatch");
+}
+
+// ------------------------------------------------------------------ T-CSR
+tgfx_graph* TCsr::device() const { return detail::device_of(*this).handle; }
+
+void TCsr::validate() const {
+  // tcsr.cpp:54-81: shape checks on the host, the O(m) scans on the device
+  if (indptr.size() != static_cast<std::size_t>(num_nodes) + 1)
+    throw ValidationError("indptr size mismatch");
+  if (indptr.front() != 0 || indptr.back() != num_entries())
+    throw ValidationError("indptr endpoints wrong");
+  if (edge_ids.size() != neighbor_ids.size() || timestamps.size() != neighbor_ids.size())
+    throw ValidationError("column arrays disagree in length");
+  detail::check(tgfx_graph_validate(device()));
+}
+
+namespace {
+
+TCsr export_graph(tgfx_graph* h, bool reverse) {
+  TCsr g;
+  std::int64_t V = 0, E = 0, m = 0;
+  int rev = 0;
+  detail::check(tgfx_graph_info(h, &V, &E, &m, &rev));
+  g.num_nodes = V;
+  g.num_edges = E;
+  g.reverse = reverse;
+  g.indptr.resize(static_cast<std::size_t>(V) + 1);
+  g.neighbor_ids.resize(static_cast<std::size_t>(m));
+  g.edge_ids.resize(static_cast<std::size_t>(m));
+  g.timestamps.resize(static_cast<std::size_t>(m));
+  detail::check(tgfx_graph_export(h, g.indptr.data(), g.neighbor_ids.data(), g.edge_ids.data(),
+                                  g.timestamps.data()));
+  detail::attach(g, h);
+  return g;
+}
+
+const tgfx_event* as_events(const EventStream& s) {
+  return reinterpret_cast<const tgfx_event*>(s.events.data());
+}
+
+}  // namespace
+
+TCsr build_sequential(const EventStream& stream, bool reverse) {
+  tgfx_graph* h = nullptr;
+  detail::check(tgfx_build_sequential(as_events(stream), stream.size(), stream.num_nodes,
+                                      reverse ? 1 : 0, &h));
+  try {
+    return export_graph(h, reverse);
+  } catch (...) {
+    tgfx_graph_free(h);
+    throw;
+  }
+}
+
+TCsr build_parallel(const EventStream& stream, bool reverse, int num_threads) {
+  tgfx_graph* h = nullptr;
+  detail::check(tgfx_build_parallel(as_events(stream), stream.size(), stream.num_nodes,
+                                    reverse ? 1 : 0, num_threads, &h));
+  try {
+    return export_graph(h, reverse);
+  } catch (...) {
+    tgfx_graph_free(h);
+    throw;
+  }
+}
+
+// ------------------------------------------------------------------ container
+namespace {
+
+constexpr char kMagic[4] = {'T', 'C', 'S', 'R'};
+constexpr std::uint8_t kVersion = 1;
+constexpr std::size_t kCrcChunk = std::size_t(1) << 30;  // zlib's crc32 takes 32-bit lengths
+
+std::uint32_t crc_update(std::uint32_t crc, const void* p, std::size_t n) {
+  uLong c = crc;
+  const auto* b = static_cast<const Bytef*>(p);
+  while (n) {
+    const std::size_t k = std::min(n, kCrcChunk);
+    c = crc32(c, b, static_cast<uInt>(k));
+    b += k;
+    n -= k;
+  }
+  return static_cast<std::uint32_t>(c);
+}
+
+struct Writer {
+  std::ofstream out;
+  std::uint32_t crc = static_cast<std::uint32_t>(crc32(0L, Z_NULL, 0));
+  explicit Writer(const std::string& path) : out(path, std::ios::binary) {
+    if (!out) throw ValidationError("cannot write '" + path + "'");
+  }
+  void put(const void* p, std::size_t n) {
+    out.write(static_cast<const char*>(p), static_cast<std::streamsize>(n));
+    crc = crc_update(crc, p, n);
+  }
+  template <class T>
+  void val(T v) {
+    put(&v, sizeof v);
+  }
+};
+
+struct Reader {
+  std::vector<char> buf;
+  std::size_t pos = 0;
+  void get(void* p, std::size_t n) {
+    if (n > buf.size() - pos) throw FormatError("truncated container");
+    std::memcpy(p, buf.data() + pos, n);
+    pos += n;
+  }
+  template <class T>
+  T val() {
+    T v;
+    get(&v, sizeof v);
+    return v;
+  }
+  template <class T>
+  void arr(std::vector<T>& v, std::uint64_t count) {
+    if (count > (buf.size() - pos) / sizeof(T)) throw FormatError("truncated container");
+    v.resize(static_cast<std::size_t>(count));
+    get(v.data(), v.size() * sizeof(T));
+  }
+};
+
+}  // namespace
+
+void save_tcsr(const TCsr& g, const std::string& path) {
+  // layout of tcsr.cpp:158-174: magic, u8 version, u8 reverse, u64 num_nodes, u64 num_edges,
+  // u64 num_entries, indptr i64[], neighbors i64[], edge ids i64[], timestamps f64[], CRC-32
+  Writer w(path);
+  w.put(kMagic, sizeof kMagic);
+  w.val<std::uint8_t>(kVersion);
+  w.val<std::uint8_t>(g.reverse ? 1 : 0);
+  w.val<std::uint64_t>(static_cast<std::uint64_t>(g.num_nodes));
+  w.val<std::uint64_t>(static_cast<std::uint64_t>(g.num_edges));
+  w.val<std::uint64_t>(static_cast<std::uint64_t>(g.num_entries()));
+  w.put(g.indptr.data(), g.indptr.size() * sizeof(std::int64_t));
+  w.put(g.neighbor_ids.data(), g.neighbor_ids.size() * sizeof(NodeId));
+  w.put(g.edge_ids.data(), g.edge_ids.size() * sizeof(EdgeId));
+  w.put(g.timestamps.data(), g.timestamps.size() * sizeof(Time));
+  const std::uint32_t c = w.crc;
+  w.out.write(reinterpret_cast<const char*>(&c), sizeof c);
+  if (!w.out) throw ValidationError("write failed");
+}
+
+TCsr load_tcsr(const std::string& path) {
+  // tcsr.cpp:176-197 + binary_io.hpp:83-100, with the checksum computed over the whole file
+  // in 1 GiB pieces (the reference passes the full length as a 32-bit uInt, so containers
+  // of 4 GiB and more fail its check)
+  std::ifstream in(path, std::ios::binary | std::ios::ate);
+  if (!in) throw ValidationError("cannot open '" + path + "'");
+  const std::streamsize size = in.tellg();
+  in.seekg(0);
+  Reader r;
+  r.buf.resize(static_cast<std::size_t>(size));
+  in.read(r.buf.data(), size);
+  if (!in) throw FormatError("read failed for '" + path + "'");
+  if (r.buf.size() < 4) throw FormatError("container too small");
+  std::uint32_t stored;
+  std::memcpy(&stored, r.buf.data() + r.buf.size() - 4, 4);
+  const std::uint32_t crc0 = static_cast<std::uint32_t>(crc32(0L, Z_NULL, 0));
+  if (crc_update(crc0, r.buf.data(), r.buf.size() - 4) != stored)
+    throw FormatError("checksum mismatch");
+  r.buf.resize(r.buf.size() - 4);
+  char magic[4];
+  r.get(magic, sizeof magic);
+  if (std::memcmp(magic, kMagic, sizeof kMagic) != 0) throw FormatError("bad magic");
+  const auto version = r.val<std::uint8_t>();
+  if (version != kVersion) throw FormatError("unsupported version " + std::to_string(version));
+  TCsr g;
+  g.reverse = r.val<std::uint8_t>() != 0;
+  g.num_nodes = static_cast<NodeId>(r.val<std::uint64_t>());
+  g.num_edges = static_cast<std::int64_t>(r.val<std::uint64_t>());
+  const auto entries = r.val<std::uint64_t>();
+  r.arr(g.indptr, static_cast<std::uint64_t>(g.num_nodes) + 1);
+  r.arr(g.neighbor_ids, entries);
+  r.arr(g.edge_ids, entries);
+  r.arr(g.timestamps, entries);
+  if (r.pos != r.buf.size()) throw FormatError("trailing bytes in container");
+  g.validate();  // uploads (the device copy stays attached for sampling) and checks on device
+  return g;
+}
+
+// ------------------------------------------------------------------ sampler
+SampleStrategy parse_strategy(const std::string& name) {
+  // sampler.cpp:34-38
+  if (name == "recent") return SampleStrategy::recent;
+  if (name == "random") return SampleStrategy::random;
+  throw ValidationError("unknown sampling strategy '" + name + "'");
+}
+
+namespace {
+
+// One libtgfx batch call; stream of query i = stream_base + i (sampler.cpp:100-101).
+std::vector<NeighborSample> run_batch(const TCsr& g, const NodeId* nodes, const Time* times,
+                                      std::int64_t q, std::int64_t k, SampleStrategy strategy,
+                                      std::uint64_t seed, std::uint64_t stream_base) {
+  detail::DeviceCopy& dc = detail::device_of(g);
+  // padded output width: no query can return more than the longest slice, so a huge k
+  // (sample_recent(g, u, t, 1 << 30)) does not size the buffers; results are unchanged
+  const std::int64_t kpad = k < 1 ? k : std::max<std::int64_t>(1, std::min(k, dc.max_degree));
+  const std::size_t qs = static_cast<std::size_t>(std::max<std::int64_t>(q, 0));
+  const std::size_t slots = qs * static_cast<std::size_t>(std::max<std::int64_t>(kpad, 1));
+  std::vector<std::int64_t> counts(qs), nb(slots), ed(slots);
+  std::vector<double> ts(slots);
+  detail::check(tgfx_sample_batch(dc.handle, nodes, times, q, kpad,
+                                  strategy == SampleStrategy::recent ? TGFX_RECENT : TGFX_RANDOM,
+                                  seed, stream_base, counts.data(), nb.data(), ed.data(),
+                                  ts.data()));
+  std::vector<NeighborSample> out(qs);
+  for (std::size_t i = 0; i < qs; ++i) {
+    NeighborSample& s = out[i];
+    s.query_node = nodes[i];
+    s.query_time = times[i];
+    const std::size_t base = i * static_cast<std::size_t>(kpad);
+    s.neighbors.resize(static_cast<std::size_t>(counts[i]));
+    for (std::size_t j = 0; j < s.neighbors.size(); ++j)
+      s.neighbors[j] = {nb[base + j], ed[base + j], ts[base + j]};
+  }
+  return out;
+}
+
+}  // namespace
+
+NeighborSample sample_recent(const TCsr& g, NodeId u, Time t, std::int64_t k) {
+  return std::move(run_batch(g, &u, &t, 1, k, SampleStrategy::recent, 0, 0)[0]);
+}
+
+NeighborSample sample_random(const TCsr& g, NodeId u, Time t, std::int64_t k,
+                             std::uint64_t seed, std::uint64_t stream) {
+  return std::move(run_batch(g, &u, &t, 1, k, SampleStrategy::random, seed, stream)[0]);
+}
+
+std::vector<NeighborSample> sample_batch(const TCsr& g, const std::vector<NodeId>& nodes,
+                                         const std::vector<Time>& times, std::int64_t k,
+                                         SampleStrategy strategy, std::uint64_t seed,
+                                         int num_threads) {
+  (void)num_threads;  // results are independent of it (sampler.cpp:91); the grid is the device's
+  if (nodes.size() != times.size())
+    throw ValidationError("node and time lists differ in length");  // sampler.cpp:88-90
+  return run_batch(g, nodes.data(), times.data(), static_cast<std::int64_t>(nodes.size()), k,
+                   strategy, seed, 0);
+}
+
+// ------------------------------------------------------------------ sequences
+void SequenceBatch::validate() const {
+  // sequence.cpp:13-46 (host-side consistency check of a batch; not on the hot path)
+  const auto total = static_cast<std::size_t>(batch * l);
+  if (node_index.size() != total || edge_index.size() != total ||
+      time_delta.rows() != static_cast<std::size_t>(batch) ||
+      time_delta.cols() != static_cast<std::size_t>(l) ||
+      valid_len.size() != static_cast<std::size_t>(batch) ||
+      target_row.size() != static_cast<std::size_t>(batch))
+    throw ValidationError("sequence batch shape mismatch");
+  for (std::int64_t b = 0; b < batch; ++b) {
+    const std::int64_t len = valid_len[static_cast<std::size_t>(b)];
+    if (len < 1 || len > l) throw ValidationError("valid_len out of range");
+    if (target_row[static_cast<std::size_t>(b)] != len - 1)
+      throw ValidationError("target_row must be valid_len-1");
+    const std::size_t row = static_cast<std::size_t>(b * l);
+    for (std::int64_t j = 0; j < l; ++j) {
+      const bool padding = j >= len;
+      const double dt = time_delta.at(static_cast<std::size_t>(b), static_cast<std::size_t>(j));
+      if (padding != (node_index[row + static_cast<std::size_t>(j)] == 0))
+        throw ValidationError("padding does not match valid_len");
+      if (padding && (edge_index[row + static_cast<std::size_t>(j)] != 0 || dt != 0.0))
+        throw ValidationError("padding positions must be zero");
+      if (dt < 0.0) throw ValidationError("negative time delta");
+    }
+    if (time_delta.at(static_cast<std::size_t>(b),
+                      static_cast<std::size_t>(target_row[static_cast<std::size_t>(b)])) != 0.0)
+      throw ValidationError("query position must have zero time delta");
+    for (std::int64_t j = 1; j + 1 < len; ++j)
+      if (time_delta.at(static_cast<std::size_t>(b), static_cast<std::size_t>(j - 1)) <
+          time_delta.at(static_cast<std::size_t>(b), static_cast<std::size_t>(j)))
+        throw ValidationError("neighbor time deltas must be non-increasing");
+  }
+}
+
+MaskKind parse_mask_kind(const std::string& name) {
+  // sequence.cpp:48-53
+  if (name == "causal") return MaskKind::causal;
+  if (name == "tgat") return MaskKind::tgat;
+  if (name == "self_loop") return MaskKind::self_loop;
+  throw ValidationError("unknown mask kind '" + name + "'");
+}
+
+SequenceBatch build_sequence_batch(const std::vector<NeighborSample>& samples, std::int64_t l,
+                                   std::int64_t self_edge_index) {
+  if (l < 2) throw ValidationError("sequence length must be at least 2");  // sequence.cpp:57
+  const std::int64_t q = static_cast<std::int64_t>(samples.size());
+  std::size_t kpad = 1;
+  for (const NeighborSample& s : samples) kpad = std::max(kpad, s.neighbors.size());
+  const std::size_t qs = static_cast<std::size_t>(q);
+  std::vector<std::int64_t> counts(qs), nb(qs * kpad), ed(qs * kpad), qn(qs);
+  std::vector<double> ts(qs * kpad), qt(qs);
+  for (std::size_t b = 0; b < qs; ++b) {
+    const NeighborSample& s = samples[b];
+    counts[b] = static_cast<std::int64_t>(s.neighbors.size());
+    qn[b] = s.query_node;
+    qt[b] = s.query_time;
+    for (std::size_t j = 0; j < s.neighbors.size(); ++j) {
+      nb[b * kpad + j] = s.neighbors[j].neighbor;
+      ed[b * kpad + j] = s.neighbors[j].edge;
+      ts[b * kpad + j] = s.neighbors[j].timestamp;
+    }
+  }
+  SequenceBatch out;
+  out.batch = q;
+  out.l = l;
+  const std::size_t ql = qs * static_cast<std::size_t>(l);
+  out.node_index.resize(ql);
+  out.edge_index.resize(ql);
+  out.time_delta = Matrix(qs, static_cast<std::size_t>(l));
+  out.valid_len.resize(qs);
+  out.target_row.resize(qs);
+  detail::check(tgfx_assemble(q, static_cast<std::int64_t>(kpad), counts.data(), nb.data(),
+                              ed.data(), ts.data(), qn.data(), qt.data(), l, self_edge_index,
+                              out.node_index.data(), out.edge_index.data(), out.time_delta.data(),
+                              out.valid_len.data(), out.target_row.data()));
+  return out;
+}
+
+SequenceBatch build_sequence(const NeighborSample& sample, std::int64_t l,
+                             std::int64_t self_edge_index) {
+  return build_sequence_batch(std::vector<NeighborSample>{sample}, l, self_edge_index);
+}
+
+Matrix build_mask(const SequenceBatch& batch, MaskKind kind) {
+  Matrix mask(static_cast<std::size_t>(batch.batch * batch.l), static_cast<std::size_t>(batch.l));
+  const int code = kind == MaskKind::causal ? TGFX_MASK_CAUSAL
+                   : kind == MaskKind::tgat ? TGFX_MASK_TGAT
+                                            : TGFX_MASK_SELF_LOOP;
+  detail::check(tgfx_build_mask(batch.batch, batch.l, batch.valid_len.data(),
+                                batch.target_row.data(), code, mask.data()));
+  return mask;
+}
+
+// ------------------------------------------------------------------ synthetic
+EventStream make_random_stream(std::int64_t num_edges, NodeId num_nodes, std::uint64_t seed,
+                               double zipf_exponent) {
+  EventStream s;
+  s.num_nodes = num_nodes;
+  s.events.resize(static_cast<std::size_t>(std::max<std::int64_t>(num_edges, 0)));
+  detail::check(tgfx_make_random_stream(num_edges, num_nodes, seed, zipf_exponent,
+                                        reinterpret_cast<tgfx_event*>(s.events.data())));
+  return s;
+}
+
+}  // namespace tgf

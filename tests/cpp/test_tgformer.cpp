@@ -1,0 +1,150 @@
+// C++ host API (include/tgfx/tgformer.hpp) on the GPU: known answers pinned by the reference's
+// unit tests (proj/tests/test_tcsr.cpp:50-107, test_sampler.cpp:32-87,
+// test_sequence.cpp:19-31) plus API-level properties (batch == per-query, container
+// round trip, device copy reuse, error types).  Needs a CUDA device.
+#include <cmath>
+#include <cstdio>
+#include <filesystem>
+
+#include "doctest.h"
+#include "tgformer/sampler.hpp"
+#include "tgformer/sequence.hpp"
+#include "tgformer/synthetic.hpp"
+#include "tgformer/tcsr.hpp"
+
+namespace {
+
+tgf::EventStream tiny() {
+  // three events, listed in time order (t = 3, 4, 5) with out-of-order edge ids
+  tgf::EventStream s;
+  s.num_nodes = 3;
+  s.events = {{1, 0, 2, 3.0}, {2, 1, 2, 4.0}, {0, 0, 1, 5.0}};
+  return s;
+}
+
+}  // namespace
+
+TEST_CASE("tiny build: indptr and slice order, both directions") {
+  const tgf::TCsr f = tgf::build_sequential(tiny(), false);
+  CHECK(f.indptr == std::vector<std::int64_t>{0, 2, 3, 3});
+  CHECK(f.neighbor_ids == std::vector<tgf::NodeId>{2, 1, 2});
+  CHECK(f.timestamps == std::vector<double>{3.0, 5.0, 4.0});
+  const tgf::TCsr r = tgf::build_parallel(tiny(), true, 8);
+  CHECK(r.indptr == std::vector<std::int64_t>{0, 2, 4, 6});
+  CHECK(r.edge_ids == std::vector<tgf::EdgeId>{1, 0, 2, 0, 1, 2});
+  r.validate();
+}
+
+TEST_CASE("builder errors carry the reference's types and messages") {
+  tgf::EventStream s = tiny();
+  s.events.push_back({3, 0, 7, 6.0});
+  try {
+    (void)tgf::build_sequential(s, true);
+    CHECK(false);
+  } catch (const tgf::ValidationError& e) {
+    CHECK(std::string(e.what()) == "event 3 endpoint out of range");
+  }
+  CHECK_THROWS_AS(tgf::build_parallel(tiny(), true, 0), tgf::ValidationError);
+}
+
+TEST_CASE("sequential, parallel and unsorted-input builds agree") {
+  tgf::EventStream s = tgf::make_random_stream(30000, 500, 7);
+  const tgf::TCsr a = tgf::build_sequential(s, true);
+  const tgf::TCsr b = tgf::build_parallel(s, true, 4);
+  CHECK(a.indptr == b.indptr);
+  CHECK(a.neighbor_ids == b.neighbor_ids);
+  CHECK(a.edge_ids == b.edge_ids);
+  CHECK(a.timestamps == b.timestamps);
+  // reversed stream order: same T-CSR (the builder sorts slices by (t, eid))
+  std::reverse(s.events.begin(), s.events.end());
+  const tgf::TCsr c = tgf::build_parallel(s, true, 4);
+  CHECK(a.neighbor_ids == c.neighbor_ids);
+  CHECK(a.edge_ids == c.edge_ids);
+}
+
+TEST_CASE("recent sampling: strict before t, k most recent ascending") {
+  const tgf::TCsr g = tgf::build_sequential(tiny(), false);
+  const tgf::NeighborSample mid = tgf::sample_recent(g, 0, 4.0, 5);
+  REQUIRE(mid.neighbors.size() == 1);
+  CHECK(mid.neighbors[0].neighbor == 2);
+  CHECK(tgf::sample_recent(g, 0, 3.0, 5).neighbors.empty());
+  const tgf::NeighborSample all = tgf::sample_recent(g, 0, 99.0, 1 << 30);
+  REQUIRE(all.neighbors.size() == 2);
+  CHECK(all.neighbors[1].timestamp == 5.0);
+  CHECK(tgf::sample_recent(g, 0, std::nan(""), 5).neighbors.empty());
+  CHECK_THROWS_AS(tgf::sample_recent(g, 3, 1.0, 1), tgf::ValidationError);
+  CHECK_THROWS_AS(tgf::sample_recent(g, 0, 1.0, 0), tgf::ValidationError);
+}
+
+TEST_CASE("batch sampling equals per-query sampling (stream = query index)") {
+  const tgf::EventStream s = tgf::make_random_stream(20000, 300, 34);
+  const tgf::TCsr g = tgf::build_parallel(s, true, 2);
+  std::vector<tgf::NodeId> nodes;
+  std::vector<tgf::Time> times;
+  tgf::CounterRng rng(77, 0);
+  for (int i = 0; i < 300; ++i) {
+    nodes.push_back(static_cast<tgf::NodeId>(rng.next_below(300)));
+    times.push_back(rng.next_uniform(0.0, 10000.0));
+  }
+  for (auto strat : {tgf::SampleStrategy::recent, tgf::SampleStrategy::random}) {
+    const auto batch = tgf::sample_batch(g, nodes, times, 12, strat, 9);
+    REQUIRE(batch.size() == nodes.size());
+    for (std::size_t i = 0; i < nodes.size(); ++i) {
+      const auto one = strat == tgf::SampleStrategy::recent
+                           ? tgf::sample_recent(g, nodes[i], times[i], 12)
+                           : tgf::sample_random(g, nodes[i], times[i], 12, 9, i);
+      REQUIRE(one.neighbors.size() == batch[i].neighbors.size());
+      for (std::size_t j = 0; j < one.neighbors.size(); ++j) {
+        CHECK(one.neighbors[j].edge == batch[i].neighbors[j].edge);
+        CHECK(one.neighbors[j].timestamp < times[i]);
+      }
+    }
+  }
+  CHECK_THROWS_AS(tgf::sample_batch(g, {0, 1}, {1.0}, 3, tgf::SampleStrategy::recent, 0),
+                  tgf::ValidationError);
+}
+
+TEST_CASE("suffix infilling known answer") {
+  // test_sequence.cpp:19-31: neighbors (nbr 1,2,5 / eid 0,1,2 / t 2,4,7) of node 7 at t = 10
+  tgf::NeighborSample s{7, 10.0, {{1, 0, 2.0}, {2, 1, 4.0}, {5, 2, 7.0}}};
+  const tgf::SequenceBatch b = tgf::build_sequence(s, 8, 100);
+  b.validate();
+  CHECK(b.node_index == std::vector<std::int64_t>{2, 3, 6, 8, 0, 0, 0, 0});
+  CHECK(b.edge_index == std::vector<std::int64_t>{1, 2, 3, 100, 0, 0, 0, 0});
+  CHECK(b.time_delta.at(0, 0) == 8.0);
+  CHECK(b.time_delta.at(0, 2) == 3.0);
+  CHECK(b.valid_len[0] == 4);
+  CHECK(b.target_row[0] == 3);
+  const tgf::Matrix m = tgf::build_mask(b, tgf::MaskKind::causal);
+  CHECK(m.rows() == 8);
+  CHECK(m.at(2, 2) == 0.0);
+  CHECK(std::isinf(m.at(2, 3)));
+  CHECK_THROWS_AS(tgf::build_sequence(s, 1, 100), tgf::ValidationError);
+  CHECK_THROWS_AS(tgf::parse_mask_kind("bogus"), tgf::ValidationError);
+}
+
+TEST_CASE("container round trip and corruption") {
+  const tgf::TCsr g = tgf::build_parallel(tgf::make_random_stream(5000, 80, 3), true, 1);
+  const std::string path =
+      (std::filesystem::temp_directory_path() / "tgfx_cpp_test.tcsr").string();
+  tgf::save_tcsr(g, path);
+  const tgf::TCsr back = tgf::load_tcsr(path);
+  CHECK(back.indptr == g.indptr);
+  CHECK(back.timestamps == g.timestamps);
+  CHECK(tgf::sample_recent(back, 0, 1e9, 4).neighbors.size() == 4);
+  std::filesystem::resize_file(path, 12);
+  CHECK_THROWS_AS(tgf::load_tcsr(path), tgf::FormatError);
+  std::remove(path.c_str());
+}
+
+TEST_CASE("hand-assembled and edited TCsr re-upload") {
+  tgf::TCsr g = tgf::build_sequential(tiny(), false);
+  tgf::TCsr h = g;  // copy: content-identical, may share the device copy
+  CHECK(tgf::sample_recent(h, 0, 99.0, 5).neighbors.size() == 2);
+  h.timestamps[0] = 4.5;  // edited columns: the next call must see the new values
+  h.timestamps[1] = 4.6;
+  const auto s = tgf::sample_recent(h, 0, 4.55, 5);
+  REQUIRE(s.neighbors.size() == 1);
+  CHECK(s.neighbors[0].timestamp == 4.5);
+  CHECK(tgf::sample_recent(g, 0, 4.55, 5).neighbors.size() == 1);  // original untouched: t=3
+}

@@ -1,0 +1,57 @@
+"""The C++ host API (include/tgfx/tgformer.hpp -> libtgformer.so -> libtgfx.so).
+
+GPU: our C++ suite (tests/cpp/test_tgformer.cpp) and the REFERENCE's own hot-path unit tests
+(proj/tests/test_tcsr.cpp, test_sampler.cpp, test_sequence.cpp) compiled unchanged against our
+headers (tests/cpp/Makefile) must pass on the device.  CPU: the library loads and exports the
+reference's API symbols."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CPP = os.path.join(ROOT, "tests", "cpp")
+LIB = os.path.join(ROOT, "paper_2409_05477_b200", "lib", "libtgformer.so")
+
+# reference API entry points (proj/include/tgformer/*.hpp) the C++ layer must define
+SYMBOLS = ["build_sequential", "build_parallel", "sample_recent", "sample_random", "sample_batch",
+           "build_sequence_batch", "build_sequence", "build_mask", "save_tcsr", "load_tcsr",
+           "parse_strategy", "parse_mask_kind", "make_random_stream"]
+
+
+def _ensure_built(target):
+    subprocess.run(["make", "-s", "-C", CPP, target], check=True)
+
+
+def test_host_library_exports_reference_api():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2409_05477_b200", "csrc")],
+                       check=True)
+    ctypes.CDLL(LIB)
+    out = subprocess.run(["nm", "-D", "-C", "--defined-only", LIB], capture_output=True,
+                         text=True, check=True).stdout
+    for s in SYMBOLS:
+        assert f"tgf::{s}(" in out, s
+    for s in ("tgf::TCsr::validate() const", "tgf::SequenceBatch::validate() const",
+              "tgf::EventStream::validate() const"):
+        assert s in out, s
+
+
+@pytest.mark.gpu
+def test_cpp_suite_on_device():
+    _ensure_built("ours")
+    r = subprocess.run([os.path.join(CPP, "tgformer_tests")], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_against_device_api():
+    exe = os.path.join(CPP, "_ref", "ref_unit_tests")
+    if not os.path.exists(exe):
+        pytest.skip("reference unit-test binary not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "0 failed" in r.stdout
