@@ -355,6 +355,364 @@ __global__ void __launch_bounds__(kTkWarps * 32) k_scatter(
   }
 }
 
+// K3' (default): tile-sorted stable scatter.
+// Each CTA owns a contiguous chunk of the stream and its V cursors (shared memory, from the
+// C x V offset table).  The chunk is streamed through shared memory in tiles of kTE events
+// by 1-D bulk copies (cp.async.bulk + mbarrier, double-buffered), and every tile is ranked
+// by node with a block-wide stable LSD radix sort of (node << 16 | entry index) keys:
+// 8-bit digits, per-warp digit counters ranked with __match_any_sync, one exclusive scan
+// over (digit, warp).  After the sort a node's entries of the tile are one contiguous run,
+// so each entry's output position is cursor[u] + (its offset in the run), the run's tail
+// bumps the cursor, and consecutive threads store consecutive positions of a run (the Zipf
+// hub's entries go out as coalesced bursts).  All warps of the CTA work on every tile --
+// no serialisation across warps -- and the tile loads overlap the ranking of the previous
+// tile.  Entries of cold nodes are written as full 32-byte records (see k_coldflags).
+constexpr int kTStages = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int kTT, int kTE>
+size_t tile_scatter_smem(int64_t V) {
+  const int64_t vpad = (V + 31) & ~31LL;
+  return static_cast<size_t>(kTStages) * kTE * 32  // event stages
+         + 2 * 2 * kTE * 4                          // key ping-pong (2 entries per event max)
+         + (kTT / 32) * 256 * 4                     // per-warp digit counters
+         + 64 * 8                                   // barriers + scan scratch
+         + vpad * 4 + (vpad / 32) * 4;              // cursors + cold bits
+}
+
+template <int R, int kTT, int kTE>
+__global__ void __launch_bounds__(kTT) k_scatter_tile(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev, int passes,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+    const int64_t* __restrict__ cdelta, ulonglong2* __restrict__ cold_img,
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
+  constexpr int kTW = kTT / 32;
+  constexpr int NE = kTE * R;       // entries per tile
+  constexpr int KPT = NE / kTT;     // keys per thread
+  static_assert(KPT * kTT == NE && KPT >= 1, "tile shape");
+  extern __shared__ __align__(128) unsigned char sm[];
+  tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
+  uint32_t* keys0 = reinterpret_cast<uint32_t*>(sm + kTStages * kTE * 32);
+  uint32_t* keys1 = keys0 + NE;
+  uint32_t* wcnt = keys0 + 2 * 2 * kTE;  // [kTW][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wcnt + kTW * 256);
+  int* scr = reinterpret_cast<int*>(bars + 8);  // 32 ints of scan scratch (+ spare)
+  const int vpad = (V + 31) & ~31;
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(bars + 64);
+  uint32_t* coldbits = cursor + vpad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  if (e0 >= e1) return;
+  const int64_t ntiles = ceil_div(e1 - e0, kTE);
+  if (tid == 0) {
+    for (int s = 0; s < kTStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kTStages && s < ntiles; ++s) {
+      const int64_t b = e0 + static_cast<int64_t>(s) * kTE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[s], bytes);
+      bulk_g2s(stage + s * kTE, ev + b, bytes, &bars[s]);
+    }
+  }
+  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
+  for (int i = tid; i < V; i += kTT) cursor[i] = orow[i];
+  for (int i = tid; i < vpad / 32; i += kTT) coldbits[i] = coldbits_g[i];
+  __syncthreads();
+
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int sidx = static_cast<int>(it % kTStages);
+    const uint32_t phase = static_cast<uint32_t>((it / kTStages) & 1);
+    const int64_t tb = e0 + it * kTE;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kTE), e1 - tb));
+    const int ent = cnt * R;
+    const tgfx_event* sev = stage + sidx * kTE;
+    mbar_wait(&bars[sidx], phase);
+
+    // keys in warp-striped order: entry j = warp*32*KPT + k*32 + lane (emission order)
+    uint32_t key[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int j = warp * 32 * KPT + k * 32 + lane;
+      uint32_t node = static_cast<uint32_t>(V);  // sentinel: sorts after every real node
+      if (j < ent) {
+        const int64_t* e = reinterpret_cast<const int64_t*>(sev + (R == 2 ? (j >> 1) : j));
+        node = static_cast<uint32_t>((R == 2 && (j & 1)) ? e[2] : e[1]);
+      }
+      key[k] = (node << 16) | static_cast<uint32_t>(j);
+    }
+    uint32_t* src_keys = keys0;
+    uint32_t* dst_keys = keys1;
+    for (int p = 0; p < passes; ++p) {
+      const int shift = 16 + 8 * p;
+      uint32_t* wc = wcnt + warp * 256;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wc[c * 32 + lane] = 0;
+      __syncwarp();
+      int rank[KPT];
+      uint32_t dig[KPT];
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        dig[k] = (key[k] >> shift) & 0xffu;
+        const unsigned peers = __match_any_sync(kFull, dig[k]);
+        const uint32_t b = wc[dig[k]];
+        __syncwarp();
+        if (lane == __ffs(peers) - 1) wc[dig[k]] = b + __popc(peers);
+        __syncwarp();
+        rank[k] = static_cast<int>(b) + __popc(peers & lanemask_lt());
+      }
+      __syncthreads();
+      // exclusive scan of the kTW x 256 counters in (digit, warp) order; thread t owns the 8
+      // consecutive (digit-major) counters t*8 .. t*8+7
+      {
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = tid * 8 + c;
+          v[c] = wcnt[(i % kTW) * 256 + i / kTW];
+          s += v[c];
+        }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) scr[warp] = static_cast<int>(x);
+        __syncthreads();
+        if (warp == 0) {
+          uint32_t w = lane < kTW ? static_cast<uint32_t>(scr[lane]) : 0u;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, w, o);
+            if (lane >= o) w += y;
+          }
+          if (lane < kTW) scr[lane] = static_cast<int>(w);
+        }
+        __syncthreads();
+        uint32_t run = (warp ? static_cast<uint32_t>(scr[warp - 1]) : 0u) + x - s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = tid * 8 + c;
+          wcnt[(i % kTW) * 256 + i / kTW] = run;
+          run += v[c];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) dst_keys[wc[dig[k]] + rank[k]] = key[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) key[k] = dst_keys[warp * 32 * KPT + k * 32 + lane];
+      uint32_t* tmp = src_keys;
+      src_keys = dst_keys;
+      dst_keys = tmp;
+    }
+    // sorted: src_keys[s], thread holds s = warp*32*KPT + k*32 + lane.  Head of each node run
+    // = last position <= s where the node changes: inclusive max-scan of head positions.
+    int hp[KPT];
+    uint32_t u[KPT];
+    {
+      int carry = 0;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const int s = warp * 32 * KPT + k * 32 + lane;
+        u[k] = key[k] >> 16;
+        const bool head = s == 0 || (src_keys[s - 1] >> 16) != u[k];
+        int x = head ? s : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x = max(x, y);
+        }
+        x = max(x, carry);
+        hp[k] = x;
+        carry = __shfl_sync(kFull, x, 31);
+      }
+      if (lane == 31) scr[warp] = carry;
+      __syncthreads();
+      int prev = 0;
+      for (int w = 0; w < warp; ++w) prev = max(prev, scr[w]);
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) hp[k] = max(hp[k], prev);
+    }
+    uint32_t pos[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int s = warp * 32 * KPT + k * 32 + lane;
+      pos[k] = u[k] < static_cast<uint32_t>(V) ? cursor[u[k]] + static_cast<uint32_t>(s - hp[k]) : 0u;
+    }
+    __syncthreads();  // every entry has read its run's cursor
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int s = warp * 32 * KPT + k * 32 + lane;
+      if (u[k] >= static_cast<uint32_t>(V)) continue;
+      const bool tail = s == NE - 1 || (src_keys[s + 1] >> 16) != u[k];
+      if (tail) cursor[u[k]] = pos[k] + 1;
+      const int j = static_cast<int>(key[k] & 0xffffu);
+      const longlong2* e = reinterpret_cast<const longlong2*>(sev + (R == 2 ? (j >> 1) : j));
+      const longlong2 a = e[0], b = e[1];  // (eid, src), (dst, t bits)
+      const bool side = R == 2 && (j & 1);
+      const long long other = side ? a.y : b.x;
+      if ((coldbits[u[k] >> 5] >> (u[k] & 31)) & 1u) {
+        const int64_t ci = static_cast<int64_t>(pos[k]) + __ldg(reinterpret_cast<const long long*>(cdelta) + u[k]);
+        ulonglong2* rec = cold_img + 2 * ci;
+        rec[0] = make_ulonglong2(static_cast<unsigned long long>(other), static_cast<unsigned long long>(a.x));
+        rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(pos[k]));
+      } else {
+        nbr_out[pos[k]] = other;
+        eid_out[pos[k]] = a.x;
+        ts_out[pos[k]] = __longlong_as_double(b.y);
+      }
+    }
+    __syncthreads();  // stage buffer consumed, cursors final for this tile
+    if (tid == 0 && it + kTStages < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t b = e0 + (it + kTStages) * kTE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[sidx], bytes);
+      bulk_g2s(stage + sidx * kTE, ev + b, bytes, &bars[sidx]);
+    }
+  }
+}
+
+// K3'' (variant 20+): ticketed warps with register prefetch.  Tiles of 64 entries (two
+// 32-entry rounds) are taken by the CTA's warps round-robin; a warp groups its rounds with
+// __match_any_sync, waits for the previous tile's warp to hand over (named barrier, no
+// spinning), bumps the shared-memory cursors of its groups (two dependent LDS/STS per group,
+// the whole critical section), hands over, then stores.  Each warp keeps the events of its
+// next D tiles in registers, loaded D tiles ahead, so the handover chain never waits on HBM;
+// only the cursors live in shared memory, so several CTAs fit per SM.
+template <int R, int W, int D>
+__global__ void __launch_bounds__(W * 32) k_scatter_pf(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+    const int64_t* __restrict__ cdelta, ulonglong2* __restrict__ cold_img,
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int vpad = (V + 31) & ~31;
+  uint32_t* cursor = smem;
+  uint32_t* coldbits = cursor + vpad;
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(kFull, static_cast<int>(threadIdx.x >> 5), 0);
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  if (e0 >= e1) return;
+  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
+  for (int i = threadIdx.x; i < V; i += W * 32) cursor[i] = orow[i];
+  for (int i = threadIdx.x; i < vpad / 32; i += W * 32) coldbits[i] = coldbits_g[i];
+  __syncthreads();
+
+  const int64_t E0 = e0 * R, E1 = e1 * R;
+  const int64_t ntiles = ceil_div(E1 - E0, 64);
+  auto load_tile = [&](int64_t t, Ev (&x)[2]) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int64_t j = E0 + t * 64 + r * 32 + lane;
+      x[r] = (t < ntiles && j < E1) ? load_event(ev, R == 2 ? (j >> 1) : j) : Ev{0, -1, -1, 0.0};
+    }
+  };
+  Ev buf[D][2];
+#pragma unroll
+  for (int d = 0; d < D; ++d) load_tile(warp + static_cast<int64_t>(d) * W, buf[d]);
+
+  for (int64_t i0 = 0;; i0 += D) {
+    bool stop = false;
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+      const int64_t t = warp + (i0 + s) * W;
+      if (t >= ntiles) {
+        stop = true;
+        break;
+      }
+      Ev x[2] = {buf[s][0], buf[s][1]};
+      load_tile(t + static_cast<int64_t>(D) * W, buf[s]);  // refill this slot D tiles ahead
+      uint32_t node[2], peers[2];
+      int64_t cd[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t j = E0 + t * 64 + r * 32 + lane;
+        const bool side = R == 2 && (j & 1);
+        const bool ok = j < E1;
+        node[r] = ok ? static_cast<uint32_t>(side ? x[r].dst : x[r].src) : 0xffffffffu;
+        if (side) {  // keep the other endpoint in .dst
+          const int64_t a = x[r].src;
+          x[r].src = x[r].dst;
+          x[r].dst = a;
+        }
+        peers[r] = __match_any_sync(kFull, node[r]);
+        const bool cold = ok && ((coldbits[node[r] >> 5] >> (node[r] & 31)) & 1u);
+        cd[r] = cold ? __ldg(reinterpret_cast<const long long*>(cdelta) + node[r]) : INT64_MIN;
+      }
+      if (t > 0) named_bar_sync(1 + warp, 64);
+      uint32_t base[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const bool lead = node[r] != 0xffffffffu && lane == __ffs(peers[r]) - 1;
+        uint32_t b = 0;
+        if (lead) {
+          b = cursor[node[r]];
+          cursor[node[r]] = b + __popc(peers[r]);
+        }
+        base[r] = b;
+        __syncwarp();
+      }
+      if (t + 1 < ntiles) named_bar_arrive(1 + (warp + 1) % W, 64);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t pos =
+            __shfl_sync(kFull, base[r], __ffs(peers[r]) - 1) + __popc(peers[r] & lanemask_lt());
+        if (node[r] == 0xffffffffu) continue;
+        if (cd[r] != INT64_MIN) {
+          const int64_t ci = static_cast<int64_t>(pos) + cd[r];
+          ulonglong2* rec = cold_img + 2 * ci;
+          rec[0] = make_ulonglong2(static_cast<unsigned long long>(x[r].dst),
+                                   static_cast<unsigned long long>(x[r].eid));
+          rec[1] = make_ulonglong2(static_cast<unsigned long long>(__double_as_longlong(x[r].t)),
+                                   static_cast<unsigned long long>(pos));
+        } else {
+          nbr_out[pos] = x[r].dst;
+          eid_out[pos] = x[r].eid;
+          ts_out[pos] = x[r].t;
+        }
+      }
+    }
+    if (stop) break;
+  }
+}
+
 // K4: place the cold entries.  Consecutive cold indices are consecutive positions of a cold
 // node's slice, so both the 32-byte record reads and the column writes are coalesced.
 __global__ void __launch_bounds__(256) k_cold(const ulonglong2* __restrict__ img, int64_t ncold,
@@ -530,9 +888,82 @@ int64_t cold_theta() {
 int scatter_variant() {
   static int v = [] {
     const char* e = getenv("TGFX_SCATTER_VARIANT");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 10;
   }();
   return v;
+}
+
+// tile-sorted scatter shapes (threads, events per tile): variant 10 (default) 256 x 256,
+// 11: 512 x 512, 12: 128 x 128, 13: 256 x 512
+#define TGFX_TILE_SHAPES(X) \
+  X(10, 256, 256)           \
+  X(11, 512, 512)           \
+  X(12, 128, 128)           \
+  X(13, 256, 512)
+
+size_t tile_smem_for(int64_t V) {
+  const int v = scatter_variant();
+#define X(ID, TT, TE) \
+  if (v == ID) return tile_scatter_smem<TT, TE>(V);
+  TGFX_TILE_SHAPES(X)
+#undef X
+  return 0;
+}
+
+bool use_tile_scatter(int64_t V) {
+  const size_t sm = tile_smem_for(V);
+  return sm > 0 && V <= 65535 && sm <= static_cast<size_t>(device_info().smem_optin);
+}
+
+template <int R, int TT, int TE>
+int tile_bps_t(int64_t V) {
+  const size_t smem = tile_scatter_smem<TT, TE>(V);
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_tile<R, TT, TE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_tile<R, TT, TE>, TT, smem));
+  return std::max(bps, 1);
+}
+
+// prefetching ticketed scatter shapes (warps per CTA, prefetch depth in tiles)
+#define TGFX_PF_SHAPES(X) \
+  X(20, 8, 4)             \
+  X(21, 12, 3)            \
+  X(22, 8, 2)             \
+  X(23, 16, 2)
+
+bool use_pf_scatter(int64_t V) {
+  const int v = scatter_variant();
+  return v >= 20 && v <= 23 && V <= 65535;
+}
+
+template <int R, int W, int D>
+int pf_bps_t(int64_t V) {
+  const size_t smem = scatter_smem(V);
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_pf<R, W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_pf<R, W, D>, W * 32, smem));
+  return std::max(bps, 1);
+}
+
+int pf_bps(int R, int64_t V) {
+  const int v = scatter_variant();
+#define X(ID, W, D) \
+  if (v == ID) return R == 2 ? pf_bps_t<2, W, D>(V) : pf_bps_t<1, W, D>(V);
+  TGFX_PF_SHAPES(X)
+#undef X
+  return 1;
+}
+
+int tile_bps(int R, int64_t V) {
+  const int v = scatter_variant();
+#define X(ID, TT, TE) \
+  if (v == ID) return R == 2 ? tile_bps_t<2, TT, TE>(V) : tile_bps_t<1, TT, TE>(V);
+  TGFX_TILE_SHAPES(X)
+#undef X
+  return 1;
 }
 
 // (rounds, warps) variants of the ticketed scatter
@@ -554,8 +985,16 @@ int scatter_bps(int64_t V) {
   return std::max(bps, 1);
 }
 
-int scatter_blocks_per_sm(int R, int64_t V) {
+// ticketed-scatter variant for graphs the tile kernel does not take (0 unless overridden)
+int ticket_variant() {
   const int v = scatter_variant();
+  return v >= 0 && v <= 5 ? v : 0;
+}
+
+int scatter_blocks_per_sm(int R, int64_t V) {
+  if (use_tile_scatter(V)) return tile_bps(R, V);
+  if (use_pf_scatter(V)) return pf_bps(R, V);
+  const int v = ticket_variant();
 #define X(ID, RO, W) \
   if (v == ID) return R == 2 ? scatter_bps<2, RO, W>(V) : scatter_bps<1, RO, W>(V);
   TGFX_SCATTER_VARIANTS(X)
@@ -663,8 +1102,55 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   ulonglong2* img = static_cast<ulonglong2*>(
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
+  if (use_tile_scatter(V)) {
+    const size_t tsm = tile_smem_for(V);
+    int bits = 1;
+    while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
+    const int passes = (bits + 7) / 8;
+    const int v = scatter_variant();
+#define X(ID, TT, TE)                                                                        \
+  if (v == ID) {                                                                             \
+    if (g->reverse)                                                                          \
+      k_scatter_tile<2, TT, TE><<<C, TT, tsm, s>>>(d_ev, g->n, V, chunk_ev, passes, cnt,     \
+                                                   coldbits, cdelta, img, g->nbr, g->eid,    \
+                                                   g->ts);                                   \
+    else                                                                                     \
+      k_scatter_tile<1, TT, TE><<<C, TT, tsm, s>>>(d_ev, g->n, V, chunk_ev, passes, cnt,     \
+                                                   coldbits, cdelta, img, g->nbr, g->eid,    \
+                                                   g->ts);                                   \
+  }
+    TGFX_TILE_SHAPES(X)
+#undef X
+    after_launch("k_scatter_tile");
+    if (ncold > 0) {
+      k_cold<<<resident_grid(k_cold, 256, 0, ncold), 256, 0, s>>>(img, ncold, g->nbr, g->eid, g->ts);
+      after_launch("k_cold");
+    }
+    return;
+  }
+  if (use_pf_scatter(V)) {
+    const size_t psm = scatter_smem(V);
+    const int v = scatter_variant();
+#define X(ID, W, D)                                                                              \
+  if (v == ID) {                                                                                 \
+    if (g->reverse)                                                                              \
+      k_scatter_pf<2, W, D><<<C, W * 32, psm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
+                                                   img, g->nbr, g->eid, g->ts);                  \
+    else                                                                                         \
+      k_scatter_pf<1, W, D><<<C, W * 32, psm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
+                                                   img, g->nbr, g->eid, g->ts);                  \
+  }
+    TGFX_PF_SHAPES(X)
+#undef X
+    after_launch("k_scatter_pf");
+    if (ncold > 0) {
+      k_cold<<<resident_grid(k_cold, 256, 0, ncold), 256, 0, s>>>(img, ncold, g->nbr, g->eid, g->ts);
+      after_launch("k_cold");
+    }
+    return;
+  }
   const size_t smem = scatter_smem(V);
-  const int v = scatter_variant();
+  const int v = ticket_variant();
 #define X(ID, RO, W)                                                                             \
   if (v == ID) {                                                                                 \
     if (g->reverse)                                                                              \
