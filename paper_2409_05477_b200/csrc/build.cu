@@ -212,11 +212,16 @@ __global__ void __launch_bounds__(1024) k_indptr_scan(int64_t* a, int32_t V,
 }
 
 // K2c: starting cursor of every (chunk, node): indptr[u] + sum of earlier chunks' counts
+// With cold_space, a cold node's cursors start at its dense cold index (indptr[u] + cdelta[u])
+// instead of its output position, so the scatter writes its records without a lookup.
 __global__ void k_coloff(uint32_t* __restrict__ cnt, int C, int32_t V,
-                         const int64_t* __restrict__ indptr) {
+                         const int64_t* __restrict__ indptr, const uint32_t* __restrict__ coldbits,
+                         const int64_t* __restrict__ cdelta, int cold_space) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= V) return;
-  uint32_t run = static_cast<uint32_t>(indptr[u]);
+  int64_t start = indptr[u];
+  if (cold_space && ((coldbits[u >> 5] >> (u & 31)) & 1u)) start += cdelta[u];
+  uint32_t run = static_cast<uint32_t>(start);
   for (int c = 0; c < C; ++c) {
     const int64_t i = static_cast<int64_t>(c) * V + u;
     const uint32_t t = cnt[i];
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kTkWarps * 32) k_scatter(
 // hub's entries go out as coalesced bursts).  All warps of the CTA work on every tile --
 // no serialisation across warps -- and the tile loads overlap the ranking of the previous
 // tile.  Entries of cold nodes are written as full 32-byte records (see k_coldflags).
-constexpr int kTStages = 2;
+constexpr int kTStages = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -486,7 +491,14 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         dig[k] = (key[k] >> shift) & 0xffu;
-        const unsigned peers = __match_any_sync(kFull, dig[k]);
+        // lanes with the same 8-bit digit: intersect the 8 bit-plane ballots (fixed cost,
+        // unlike MATCH whose latency grows with the number of distinct values)
+        unsigned peers = kFull;
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {
+          const unsigned m = __ballot_sync(kFull, (dig[k] >> bit) & 1u);
+          peers &= ((dig[k] >> bit) & 1u) ? m : ~m;
+        }
         const uint32_t b = wc[dig[k]];
         __syncwarp();
         if (lane == __ffs(peers) - 1) wc[dig[k]] = b + __popc(peers);
@@ -512,17 +524,9 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
         }
         if (lane == 31) scr[warp] = static_cast<int>(x);
         __syncthreads();
-        if (warp == 0) {
-          uint32_t w = lane < kTW ? static_cast<uint32_t>(scr[lane]) : 0u;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, w, o);
-            if (lane >= o) w += y;
-          }
-          if (lane < kTW) scr[lane] = static_cast<int>(w);
-        }
-        __syncthreads();
-        uint32_t run = (warp ? static_cast<uint32_t>(scr[warp - 1]) : 0u) + x - s;
+        uint32_t before = 0;  // totals of the earlier warps, summed redundantly per warp
+        for (int w = 0; w < warp; ++w) before += static_cast<uint32_t>(scr[w]);
+        uint32_t run = before + x - s;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int i = tid * 8 + c;
@@ -587,10 +591,10 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
       const bool side = R == 2 && (j & 1);
       const long long other = side ? a.y : b.x;
       if ((coldbits[u[k] >> 5] >> (u[k] & 31)) & 1u) {
-        const int64_t ci = static_cast<int64_t>(pos[k]) + __ldg(reinterpret_cast<const long long*>(cdelta) + u[k]);
-        ulonglong2* rec = cold_img + 2 * ci;
+        // cold node: its cursors run in dense cold-index space (k_coloff), record carries u
+        ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos[k]);
         rec[0] = make_ulonglong2(static_cast<unsigned long long>(other), static_cast<unsigned long long>(a.x));
-        rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(pos[k]));
+        rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u[k]));
       } else {
         nbr_out[pos[k]] = other;
         eid_out[pos[k]] = a.x;
@@ -604,6 +608,159 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
       const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kTE), e1 - b) * 32);
       mbar_arrive_tx(&bars[sidx], bytes);
       bulk_g2s(stage + sidx * kTE, ev + b, bytes, &bars[sidx]);
+    }
+  }
+}
+
+// K3 (default, variant 30): hashed tile ranking.  Like k_scatter_tile, each CTA streams its
+// chunk through shared memory in bulk-copied tiles of 256 entries (one 32-entry round per
+// warp, emission order = (warp, lane)), but the stable rank of an entry within the tile comes
+// without sorting:
+//   1. per warp, __match_any_sync groups the lanes by node: in-warp rank and count;
+//   2. each group leader inserts its node into a small shared-memory hash (the tile has at
+//      most 256 distinct nodes) and adds its count into the warp's 8-bit field of the slot's
+//      64-bit counter word (8 warps x 8 bits; no carries since a field holds at most 32);
+//   3. after one barrier, a leader reads the word: the fields of the earlier warps sum to
+//      the node's count in front of its warp, all fields to the node's tile total; its
+//      position base is cursor[u] + that prefix;
+//   4. after a second barrier, the first warp holding u advances cursor[u] by the total and
+//      clears the slot, while every lane stores its entry.
+// Three barriers per tile and no serial handover between warps.
+constexpr int kHW = 8;                 // warps per CTA (one 8-bit counter field each)
+constexpr int kHNE = kHW * 32;         // entries per tile
+constexpr int kHSlots = 512;           // hash slots (>= 2x the distinct nodes of a tile)
+constexpr int kHStages = 4;
+
+template <int R>
+size_t hash_scatter_smem_t(int64_t V) {
+  const int64_t vpad = (V + 31) & ~31LL;
+  return static_cast<size_t>(kHStages) * (kHNE / R) * 32  // event stages
+         + kHSlots * 8 + kHSlots * 4                       // hash counters + keys
+         + 64 * 8                                          // barriers
+         + vpad * 4 + (vpad / 32) * 4;                     // cursors + cold bits
+}
+
+__device__ __forceinline__ uint32_t byte_sum(unsigned long long x) {
+  x = (x & 0x00FF00FF00FF00FFull) + ((x >> 8) & 0x00FF00FF00FF00FFull);  // 4 x 16-bit sums
+  return static_cast<uint32_t>((x * 0x0001000100010001ull) >> 48);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kHW * 32) k_scatter_hash(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+    ulonglong2* __restrict__ cold_img, int64_t* __restrict__ nbr_out,
+    int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
+  constexpr int TE = kHNE / R;  // events per tile
+  constexpr uint32_t kEmpty = 0xffffffffu;
+  extern __shared__ __align__(128) unsigned char sm[];
+  tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
+  unsigned long long* hcnt =
+      reinterpret_cast<unsigned long long*>(sm + static_cast<size_t>(kHStages) * TE * 32);
+  uint32_t* hkey = reinterpret_cast<uint32_t*>(hcnt + kHSlots);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hkey + kHSlots);
+  const int vpad = (V + 31) & ~31;
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(bars + 64);
+  uint32_t* coldbits = cursor + vpad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  if (e0 >= e1) return;
+  const int64_t ntiles = ceil_div(e1 - e0, TE);
+  if (tid == 0) {
+    for (int s = 0; s < kHStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kHStages && s < ntiles; ++s) {
+      const int64_t b = e0 + static_cast<int64_t>(s) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[s], bytes);
+      bulk_g2s(stage + s * TE, ev + b, bytes, &bars[s]);
+    }
+  }
+  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
+  for (int i = tid; i < V; i += kHW * 32) cursor[i] = orow[i];
+  for (int i = tid; i < vpad / 32; i += kHW * 32) coldbits[i] = coldbits_g[i];
+  for (int i = tid; i < kHSlots; i += kHW * 32) {
+    hkey[i] = kEmpty;
+    hcnt[i] = 0ull;
+  }
+  __syncthreads();
+
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int sidx = static_cast<int>(it % kHStages);
+    const uint32_t phase = static_cast<uint32_t>((it / kHStages) & 1);
+    const int64_t tb = e0 + it * TE;
+    const int ent = static_cast<int>(min(static_cast<int64_t>(TE), e1 - tb)) * R;
+    const tgfx_event* sev = stage + sidx * TE;
+    mbar_wait(&bars[sidx], phase);
+
+    const int j = warp * 32 + lane;  // entry of this lane, emission order
+    const bool ok = j < ent;
+    longlong2 a = make_longlong2(0, 0), b = make_longlong2(0, 0);
+    if (ok) {
+      const longlong2* e = reinterpret_cast<const longlong2*>(sev + (R == 2 ? (j >> 1) : j));
+      a = e[0];  // (eid, src)
+      b = e[1];  // (dst, t bits)
+    }
+    const bool side = R == 2 && (j & 1);
+    const uint32_t u = ok ? static_cast<uint32_t>(side ? b.x : a.y) : kEmpty;
+    const long long other = side ? a.y : b.x;
+    const unsigned peers = __match_any_sync(kFull, u);
+    const int leader = __ffs(peers) - 1;
+    const bool lead = ok && lane == leader;
+    int slot = 0;
+    if (lead) {
+      uint32_t h = (u * 2654435761u) >> 23;  // 9-bit multiplicative hash
+      while (true) {
+        const uint32_t old = atomicCAS(&hkey[h], kEmpty, u);
+        if (old == kEmpty || old == u) break;
+        h = (h + 1) & (kHSlots - 1);
+      }
+      slot = static_cast<int>(h);
+      atomicAdd(&hcnt[h], static_cast<unsigned long long>(__popc(peers)) << (8 * warp));
+    }
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+    bool first = false;
+    if (lead) {
+      const unsigned long long w = hcnt[slot];
+      const unsigned long long below = warp ? (w & ((1ull << (8 * warp)) - 1)) : 0ull;
+      const uint32_t pre = byte_sum(below);
+      total = byte_sum(w);
+      first = pre == 0;
+      base = cursor[u] + pre;
+    }
+    const uint32_t pos = __shfl_sync(kFull, base, leader) + __popc(peers & lanemask_lt());
+    __syncthreads();  // every leader has read its cursor and counter word
+    if (lead && first) {
+      cursor[u] = base + total;
+      hkey[slot] = kEmpty;
+      hcnt[slot] = 0ull;
+    }
+    if (ok) {
+      if ((coldbits[u >> 5] >> (u & 31)) & 1u) {
+        // cold node: cursors run in dense cold-index space (k_coloff), record carries u
+        ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
+        rec[0] = make_ulonglong2(static_cast<unsigned long long>(other),
+                                 static_cast<unsigned long long>(a.x));
+        rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u));
+      } else {
+        nbr_out[pos] = other;
+        eid_out[pos] = a.x;
+        ts_out[pos] = __longlong_as_double(b.y);
+      }
+    }
+    __syncthreads();  // stage consumed, cursors advanced, hash cleared
+    if (tid == 0 && it + kHStages < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t nb = e0 + (it + kHStages) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - nb) * 32);
+      mbar_arrive_tx(&bars[sidx], bytes);
+      bulk_g2s(stage + sidx * TE, ev + nb, bytes, &bars[sidx]);
     }
   }
 }
@@ -724,6 +881,23 @@ __global__ void __launch_bounds__(256) k_cold(const ulonglong2* __restrict__ img
     const ulonglong2 a = __ldg(img + 2 * i);
     const ulonglong2 b = __ldg(img + 2 * i + 1);
     const int64_t pos = static_cast<int64_t>(b.y);
+    nbr_out[pos] = static_cast<int64_t>(a.x);
+    eid_out[pos] = static_cast<int64_t>(a.y);
+    ts_out[pos] = __longlong_as_double(static_cast<long long>(b.x));
+  }
+}
+
+// K4 for the tile scatter: records carry their node; output position = cold index - cdelta[u]
+__global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ img, int64_t ncold,
+                                                const int64_t* __restrict__ cdelta,
+                                                int64_t* __restrict__ nbr_out,
+                                                int64_t* __restrict__ eid_out,
+                                                double* __restrict__ ts_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncold;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldg(img + 2 * i);
+    const ulonglong2 b = __ldg(img + 2 * i + 1);
+    const int64_t pos = i - __ldg(reinterpret_cast<const long long*>(cdelta) + b.y);
     nbr_out[pos] = static_cast<int64_t>(a.x);
     eid_out[pos] = static_cast<int64_t>(a.y);
     ts_out[pos] = __longlong_as_double(static_cast<long long>(b.x));
@@ -893,6 +1067,22 @@ int scatter_variant() {
   return v;
 }
 
+template <int R>
+int hash_bps_t(int64_t V) {
+  const size_t smem = hash_scatter_smem_t<R>(V);
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_hash<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_hash<R>, kHW * 32, smem));
+  return std::max(bps, 1);
+}
+
+// hashed tile ranking (variant 30, default) when its shared memory fits
+bool use_hash_scatter(int64_t V) {
+  return scatter_variant() == 30 && V < 0xffffffffLL &&
+         hash_scatter_smem_t<1>(V) <= static_cast<size_t>(device_info().smem_optin);
+}
+
 // tile-sorted scatter shapes (threads, events per tile): variant 10 (default) 256 x 256,
 // 11: 512 x 512, 12: 128 x 128, 13: 256 x 512
 #define TGFX_TILE_SHAPES(X) \
@@ -992,6 +1182,7 @@ int ticket_variant() {
 }
 
 int scatter_blocks_per_sm(int R, int64_t V) {
+  if (use_hash_scatter(V)) return R == 2 ? hash_bps_t<2>(V) : hash_bps_t<1>(V);
   if (use_tile_scatter(V)) return tile_bps(R, V);
   if (use_pf_scatter(V)) return pf_bps(R, V);
   const int v = ticket_variant();
@@ -1093,7 +1284,8 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   k_indptr_scan<<<1, 1024, 0, s>>>(g->indptr, V, coldbits, cdelta, ncold_d);
   after_launch("k_indptr_scan");
   if (V > 0) {
-    k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr);
+    k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr, coldbits, cdelta,
+                               use_tile_scatter(V) || use_hash_scatter(V) ? 1 : 0);
     after_launch("k_coloff");
   }
   int64_t ncold = 0;
@@ -1102,6 +1294,21 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   ulonglong2* img = static_cast<ulonglong2*>(
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
+  if (use_hash_scatter(V)) {
+    if (g->reverse)
+      k_scatter_hash<2><<<C, kHW * 32, hash_scatter_smem_t<2>(V), s>>>(
+          d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->nbr, g->eid, g->ts);
+    else
+      k_scatter_hash<1><<<C, kHW * 32, hash_scatter_smem_t<1>(V), s>>>(
+          d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->nbr, g->eid, g->ts);
+    after_launch("k_scatter_hash");
+    if (ncold > 0) {
+      k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
+                                                                      g->eid, g->ts);
+      after_launch("k_cold_u");
+    }
+    return;
+  }
   if (use_tile_scatter(V)) {
     const size_t tsm = tile_smem_for(V);
     int bits = 1;
@@ -1123,8 +1330,9 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
 #undef X
     after_launch("k_scatter_tile");
     if (ncold > 0) {
-      k_cold<<<resident_grid(k_cold, 256, 0, ncold), 256, 0, s>>>(img, ncold, g->nbr, g->eid, g->ts);
-      after_launch("k_cold");
+      k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
+                                                                      g->eid, g->ts);
+      after_launch("k_cold_u");
     }
     return;
   }

@@ -46,8 +46,8 @@ __device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_
     const int64_t r = q / in.hop_k1, j = q - r * in.hop_k1;
     if (j >= __ldg(reinterpret_cast<const long long*>(in.hop_counts) + r)) return false;
   }
-  u = ldg_i64(in.nodes + q);
-  t = ldg_f64(in.times + q);
+  u = static_cast<int64_t>(__ldcs(reinterpret_cast<const long long*>(in.nodes) + q));
+  t = __ldcs(in.times + q);
   return true;
 }
 
@@ -63,18 +63,20 @@ struct Outs {
   double* e_ts;
 };
 
+// Output rows are written once and never re-read by the kernel: streaming (evict-first)
+// stores keep them from pushing the T-CSR lines the searches reuse out of L2.
 template <bool IDX64>
 __device__ __forceinline__ void write_slot(const Outs& o, int64_t i, int64_t ni, int64_t ei,
                                            double dt) {
   if (IDX64) {
-    st<int64_t>(o.node, i, ni);
-    st<int64_t>(o.edge, i, ei);
+    __stcs(reinterpret_cast<long long*>(o.node) + i, static_cast<long long>(ni));
+    __stcs(reinterpret_cast<long long*>(o.edge) + i, static_cast<long long>(ei));
   } else {
-    st<int32_t>(o.node, i, static_cast<int32_t>(ni));
-    st<int32_t>(o.edge, i, static_cast<int32_t>(ei));
+    __stcs(static_cast<int*>(o.node) + i, static_cast<int>(ni));
+    __stcs(static_cast<int*>(o.edge) + i, static_cast<int>(ei));
   }
-  if (o.dt32) o.dt32[i] = __double2float_rn(dt);
-  if (o.dt64) o.dt64[i] = dt;
+  if (o.dt32) __stcs(o.dt32 + i, __double2float_rn(dt));
+  if (o.dt64) __stcs(o.dt64 + i, dt);
 }
 
 template <bool IDX64>
@@ -449,8 +451,8 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
   for (int j = 0; j < QL; ++j) m[j] = lo[j];
 }
 
-template <bool ASSEMBLE, bool IDX64, int W, int QL>
-__global__ void __launch_bounds__(kThreads) k_recent_line(
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
@@ -1065,26 +1067,28 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
           g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, g->search_exact, o);    \
   }
     if (variant >= 30 && !g->search_exact) {  // line-probe kernel (default)
-#define TGFX_LINE_LAUNCH(W, QL)                                                                 \
+#define TGFX_LINE_LAUNCH(W, QL, MINB)                                                           \
   {                                                                                             \
     const int gl = static_cast<int>(                                                            \
         std::min<int64_t>(ceil_div(ceil_div(a.q, 32 * QL), kWarps), INT32_MAX));                \
     if (assemble && a.index64)                                                                  \
-      k_recent_line<true, true, W, QL><<<gl, kThreads, 0, s>>>(                                 \
+      k_recent_line<true, true, W, QL, MINB><<<gl, kThreads, 0, s>>>(                                 \
           g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
     else if (assemble)                                                                          \
-      k_recent_line<true, false, W, QL><<<gl, kThreads, 0, s>>>(                                \
+      k_recent_line<true, false, W, QL, MINB><<<gl, kThreads, 0, s>>>(                                \
           g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
     else                                                                                        \
-      k_recent_line<false, false, W, QL><<<gl, kThreads, 0, s>>>(                               \
+      k_recent_line<false, false, W, QL, MINB><<<gl, kThreads, 0, s>>>(                               \
           g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);                         \
   }
       switch (variant) {
-        case 31: TGFX_LINE_LAUNCH(16, 1) break;
-        case 32: TGFX_LINE_LAUNCH(8, 2) break;
-        case 33: TGFX_LINE_LAUNCH(16, 2) break;
-        case 34: TGFX_LINE_LAUNCH(4, 2) break;
-        default: TGFX_LINE_LAUNCH(8, 1) break;
+        case 31: TGFX_LINE_LAUNCH(16, 1, 1) break;
+        case 32: TGFX_LINE_LAUNCH(8, 2, 1) break;
+        case 35: TGFX_LINE_LAUNCH(8, 1, 5) break;
+        case 36: TGFX_LINE_LAUNCH(8, 1, 6) break;
+        case 37: TGFX_LINE_LAUNCH(4, 1, 6) break;
+        case 38: TGFX_LINE_LAUNCH(8, 1, 1) break;
+        default: TGFX_LINE_LAUNCH(8, 1, 4) break;
       }
 #undef TGFX_LINE_LAUNCH
       after_launch("k_recent_line");

@@ -239,3 +239,29 @@ def test_gdelt_full_size_sampler_vs_oracle(T, oracle_mod):
         check_rows(got, want, ("random", e0))
     del og, ip, nb, ed, ts
     torch.cuda.synchronize()
+
+
+def test_exact_search_on_unsorted_or_nan_slices(T, oracle_mod):
+    """A T-CSR imported from the host whose slices hold NaN timestamps or are out of order is
+    outside the interpolation search's precondition: the sampler must then replay
+    std::lower_bound's own bisection (sampler.cpp:16-20) and match the oracle exactly."""
+    ev = oracle_mod.make_random_stream(20000, 90, 77)
+    og = oracle_mod.build(ev, 90, True)
+    rng = np.random.default_rng(3)
+    ts = og["ts"].copy()
+    ts[rng.choice(len(ts), 300, replace=False)] = np.nan        # NaN entries
+    ip = og["indptr"]
+    for u in range(0, 90, 7):                                   # reversed slices
+        ts[ip[u]:ip[u + 1]] = ts[ip[u]:ip[u + 1]][::-1].copy()
+    bad = dict(og, ts=ts)
+    g = T.TCsr.from_host(90, 20000, True, og["indptr"], og["nbr"], og["eid"], ts)
+    nodes = rng.integers(0, 90, 5000)
+    times = np.concatenate([rng.uniform(0, 10000, 4000), np.full(500, np.nan),
+                            ev["timestamp"][:500]])
+    for strat, k, l in (("recent", 10, 11), ("random", 12, 13)):
+        want = oracle_mod.sample_assemble(bad, nodes, times, k, strat, 5, l, 20001)
+        got = T.sample_assemble(g, nodes, times, k, strat, 5, l, 20001, dt64=True)
+        assert np.array_equal(got["node_index"].astype(np.int64), want["node_index"]), strat
+        assert np.array_equal(got["valid_len"].astype(np.int64), want["valid_len"]), strat
+        # NaN entries: compare as values (the payload bits of a NaN result are not specified)
+        assert np.array_equal(got["time_delta64"], want["time_delta"], equal_nan=True), strat
