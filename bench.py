@@ -17,9 +17,12 @@ by barrier + synchronize, max over ranks.  Inputs (6.1 GB events, 9.2 GB queries
 `cpu_baseline` / --impl reference time the reference's own CPU code (oracle/_ref, compiled
 from /root/reference) on a bounded prefix sample of the same workload.
 
-Multi-GPU (torchrun): T-CSR replicated (each rank builds it from its own copy of the
-stream), queries sharded contiguously across ranks (stream_base keeps results identical to
-1 GPU); no collective in the loop; total work fixed -> "scaling": "strong".
+Multi-GPU (torchrun, one process per GPU): the T-CSR is replicated (each rank rebuilds it from
+its own copy of the stream) and sampling shards by query (paper_2409_05477_b200/shard.py).
+Default plan "weak": every rank is a data-parallel worker running a full pass with its own
+negatives (neg_seed + rank), per-rank work fixed, value = N x events / max-over-ranks step
+time.  --plan strong: one pass, whole-batch query shards with stream_base (rows identical
+to 1 GPU).  No collective touches the data path; only the timing max over ranks.
 """
 import argparse
 import ctypes as C
@@ -180,7 +183,9 @@ def run_reference(args, cfg):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * tot / len(runs), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
-        "config": config_obj(cfg, ws),
+        "config": dict(config_obj(cfg, ws), parallelism=(
+            f"reference CPU path (oracle/_ref, /root/reference/proj/src compiled), {threads} host "
+            f"threads on rank 0" + (f"; ranks 1..{ws - 1} idle" if ws > 1 else ""))),
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -196,12 +201,19 @@ def metric_name(cfg):
             "sampling/packing per second)")
 
 
-def config_obj(cfg, ws):
+def config_obj(cfg, ws, weak=True):
+    if ws == 1:
+        par = "1 GPU"
+    elif weak:
+        par = (f"dp{ws}: {ws} data-parallel workers, each a full pass (own T-CSR replica, "
+               f"own negatives neg_seed+rank); no collective in the step")
+    else:
+        par = f"query-sharded x{ws} (whole batches, stream_base), T-CSR replicated"
     return {"workload": cfg["name"] + f"; reverse=1 T-CSR build + {cfg['strategy']}-{cfg['k']} "
                                       f"sampling, l={cfg['l']}, all 3E queries, batch {cfg['B']}",
             "events": cfg["E"], "num_nodes": cfg["V"], "queries": 3 * cfg["E"], "k": cfg["k"],
             "seq_len": cfg["l"], "batch": cfg["B"], "reverse": 1,
-            "parallelism": f"query-sharded x{ws}, T-CSR replicated",
+            "parallelism": par,
             "l2_flush": "inputs larger than L2 (6.1 GB events, 9.2 GB queries vs 126 MB L2)"}
 
 
@@ -210,16 +222,27 @@ def run_ours(args, cfg):
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2409_05477_b200 import _lib, device as D, tgformer as T
+    from paper_2409_05477_b200 import _lib, device as D, shard as S
 
     ws, rank, local = dist_setup()
-    torch.cuda.set_device(local)
+    # TGFX_BENCH_SHARE_GPU=1: test mode for the N>1 code path on a 1-GPU box -- all ranks on
+    # device 0, gloo for the (timing-only) collectives
+    share = os.environ.get("TGFX_BENCH_SHARE_GPU") == "1"
+    torch.cuda.set_device(0 if share else local)
+    red = "cpu" if share else "cuda"
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     E, V, k, l, B = cfg["E"], cfg["V"], cfg["k"], cfg["l"], cfg["B"]
     strat = cfg["strategy"]
     Q = 3 * E
     stream = torch.cuda.current_stream()
+    weak = args.plan == "weak"
+    # weak: every rank is one data-parallel worker running a full pass (its own negatives);
+    # strong: one pass, whole-batch query shards across ranks (shard.py)
+    neg_seed = S.weak_neg_seed(NEG_SEED, rank) if weak else NEG_SEED
 
     # resident inputs: event stream (generated on device) and all queries
     ev = D.random_stream(E, V, SEED)
@@ -229,13 +252,11 @@ def run_ours(args, cfg):
     step_ev = (8_000_000 // B) * B
     for e0 in range(0, E, step_ev):
         e1 = min(E, e0 + step_ev)
-        D.make_queries(ev, e0, e1, B, V, NEG_SEED, nodes=nodes[3 * e0:3 * e1],
+        D.make_queries(ev, e0, e1, B, V, neg_seed, nodes=nodes[3 * e0:3 * e1],
                        times=times[3 * e0:3 * e1])
-    # this rank's contiguous query range, processed in chunks of whole batches
-    per = -(-Q // ws)
-    q_lo, q_hi = min(Q, rank * per), min(Q, (rank + 1) * per)
+    q_lo, q_hi = (0, Q) if weak else S.shard_range(Q, 3 * B, ws, rank)
     chunk = args.chunk
-    chunks = [(s, min(q_hi, s + chunk)) for s in range(q_lo, q_hi, chunk)]
+    chunks = S.chunks(q_lo, q_hi, chunk)
     out = D.alloc_rows(min(chunk, max(q_hi - q_lo, 1)), l)
     g = D.build(ev, V, True)
     torch.cuda.synchronize()
@@ -273,7 +294,7 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(0 if share else local) as clk:
         start.record(stream)
         for s in range(args.steps):
             one_step(record=ev_rec[s])
@@ -287,41 +308,38 @@ def run_ours(args, cfg):
     build_ms = [r["b0"].elapsed_time(r["b1"]) for r in ev_rec]
     samp_launch_ms = [a.elapsed_time(b) for r in ev_rec for (a, b) in r["c"]]
     samp_ms = [sum(a.elapsed_time(b) for (a, b) in r["c"]) for r in ev_rec]
-    # max over ranks
-    vals = torch.tensor([total_ms, statistics.median(build_ms), statistics.median(samp_ms)],
-                        dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        tk = torch.tensor([total_taken], dtype=torch.int64, device="cuda")
-        dist.all_reduce(tk)
-        total_taken = int(tk.item())
-    total_ms, build_med, samp_med = vals.tolist()
+    # max over ranks (device-timed), sums of work
+    total_ms, build_med, samp_med = S.max_over_ranks(
+        [total_ms, statistics.median(build_ms), statistics.median(samp_ms)], device=red)
+    q_local = q_hi - q_lo
+    local_taken = total_taken
+    q_all, taken_all = (int(x) for x in S.sum_over_ranks([q_local, local_taken], device=red))
     ms_per_step = total_ms / args.steps
+    replicas = ws if weak else 1  # passes over the stream the job completes per step
 
     peak, peak_src = load_peaks()
-    # algorithmic bytes
+    # algorithmic bytes, this rank's launches
     build_bytes = 32 * E + 24 * 2 * E + 8 * (V + 1)
-    q_local = q_hi - q_lo
-    samp_bytes_all = 16 * Q + 16 * Q + 24 * total_taken + (12 * l + 4) * Q
-    samp_bytes_local = samp_bytes_all * (q_local / Q)
+    samp_bytes_local = 16 * q_local + 16 * q_local + 24 * local_taken + (12 * l + 4) * q_local
     avg_launch_ms = statistics.mean(samp_launch_ms)
     bytes_per_launch = samp_bytes_local / max(len(chunks), 1)
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     traffic = load_traffic(cfg, bytes_per_launch)
 
     line = {
-        "metric": metric_name(cfg), "value": E / (ms_per_step * 1e-3), "unit": "edges/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "metric": metric_name(cfg), "value": replicas * E / (ms_per_step * 1e-3),
+        "unit": "edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if weak else "strong", "vs_baseline": None,
         "dtype": "int64/f64 (T-CSR), int32/fp32 (sequence tensors)",
         "data": "synthetic (device generator, bit-identical to tgf::make_random_stream)",
-        "config": config_obj(cfg, ws),
-        "build": {"ms": build_med, "edges_per_s": E / (build_med * 1e-3),
+        "config": config_obj(cfg, ws, weak),
+        "build": {"ms": build_med, "edges_per_s": replicas * E / (build_med * 1e-3),
                   "alg_bytes": build_bytes,
                   "achieved_gbs": build_bytes / (build_med * 1e-3) / 1e9,
                   "frac": build_bytes / (build_med * 1e-3) / 1e9 / peak},
-        "sample": {"ms": samp_med, "queries_per_s": q_local * ws / (samp_med * 1e-3),
-                   "launches_per_step": len(chunks), "mean_taken": total_taken / Q},
+        "sample": {"ms": samp_med, "queries_per_s": q_all / (samp_med * 1e-3),
+                   "launches_per_step": len(chunks), "mean_taken": taken_all / max(q_all, 1)},
         "roofline": {"kernel": "k_recent_line (fused recent-k line-probe sampler + sequence packing)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -330,8 +348,10 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = run_e2e(args, cfg, ev, nodes, times, chunks, ws)
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, ev, nodes, times, chunks, ws, rank, weak, red)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         ev_host = ev[: args.cpu_events * 32].cpu().numpy().view(_event_dtype())
@@ -366,14 +386,33 @@ def load_traffic(cfg, bytes_per_launch):
         return None
 
 
-def run_e2e(args, cfg, ev, nodes, times, chunks, ws):
+def run_e2e(args, cfg, ev, nodes, times, chunks, ws, rank, weak, red="cuda"):
     """Same step through the C ABI with HOST buffers (pinned): tgfx_build_parallel from host
-    events, then tgfx_sample_assemble per chunk with host queries and host outputs."""
+    events, then tgfx_sample_assemble per chunk with host queries and host outputs.  At N > 1
+    every rank runs it at once (PCIe and host memory are shared, as in a real job) when the
+    host has the memory for N pinned copies; wall time is the max over ranks."""
     import numpy as np
     import torch
     from paper_2409_05477_b200 import _lib
+    from paper_2409_05477_b200 import shard as S
     L = _lib.lib()
     E, V, k, l = cfg["E"], cfg["V"], cfg["k"], cfg["l"]
+    need = 32 * E + 16 * (chunks[-1][1] - chunks[0][0]) + (12 * l + 4) * args.chunk
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = float("inf")
+    # all ranks pin their own copies at once if every rank sees room for N copies (decided
+    # collectively so every rank takes the same branch)
+    short = S.max_over_ranks([0.0 if avail > 1.25 * ws * need else 1.0], device=red)[0]
+    everyone = ws == 1 or short == 0.0
+    active = everyone or rank == 0
+    if not active:  # rank 0 alone measures; the others only join the collectives
+        torch.distributed.barrier()
+        S.max_over_ranks([0.0], device=red)
+        S.sum_over_ranks([0], device=red)
+        return None
     h_ev = torch.empty(ev.numel(), dtype=torch.uint8, pin_memory=True)
     h_ev.copy_(ev)
     lo, hi = chunks[0][0], chunks[-1][1]
@@ -401,16 +440,25 @@ def run_e2e(args, cfg, ev, nodes, times, chunks, ws):
 
     step()  # warm-up
     n_steps = max(1, min(args.steps, args.e2e_steps))
+    if ws > 1:
+        torch.distributed.barrier()  # inactive ranks wait here too
     t0 = time.perf_counter()
     for _ in range(n_steps):
         step()
     dt = (time.perf_counter() - t0) / n_steps
-    q = hi - lo
-    return {"value": E / dt, "unit": "edges/s", "ms_per_step": dt * 1e3, "steps": n_steps,
-            "h2d_bytes_per_step": 32 * E + 16 * q,
-            "d2h_bytes_per_step": (12 * l + 4) * q,
+    from paper_2409_05477_b200 import shard as S
+    dt = S.max_over_ranks([dt], device=red)[0]
+    q_all = int(S.sum_over_ranks([hi - lo], device=red)[0])  # queries over all ranks
+    nr = ws if everyone else 1
+    passes = nr if weak else 1
+    if not everyone:
+        q_all = hi - lo
+    return {"value": passes * E / dt, "unit": "edges/s", "ms_per_step": dt * 1e3,
+            "steps": n_steps, "ranks": nr,
+            "h2d_bytes_per_step": nr * 32 * E + 16 * q_all,  # every rank uploads the stream
+            "d2h_bytes_per_step": (12 * l + 4) * q_all,
             "path": "C ABI host-buffer calls tgfx_build_parallel + tgfx_sample_assemble "
-                    "(pinned host memory), wall clock"}
+                    "(pinned host memory), wall clock, max over ranks"}
 
 
 def main():
@@ -425,6 +473,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plan", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = each rank a full data-parallel pass (default); "
+                         "strong = one pass, queries sharded across ranks")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: W >= 3 required by the timing rules; using 3", file=sys.stderr)

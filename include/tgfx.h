@@ -103,6 +103,36 @@ int tgfx_graph_free(tgfx_graph* g);
 /* path the last build took: 0 presorted fast path, 1 general (re-sort), 2 large-V path */
 int tgfx_graph_build_path(const tgfx_graph* g);
 
+/* ---------------------------------------------------------------- partitioned build */
+/* Node-range-partitioned multi-GPU build (the reference has no distributed
+ * construction).  Host driver: paper_2409_05477_b200/partition.py.
+ * Per-rank node degrees of a stream chunk (src, + dst if reverse); d_deg[num_nodes] is zeroed. */
+int tgfx_degree_hist_device(const tgfx_event* d_events, int64_t n, int64_t num_nodes, int reverse,
+                            uint64_t* d_deg, void* stream);
+/* warps the partition kernels use for n events (size of the count/offset tables / nparts) */
+int64_t tgfx_partition_warps(int64_t n);
+/* d_bounds[nparts+1]: rank d owns nodes [d_bounds[d], d_bounds[d+1]).  Count pass:
+ * d_counts[w*nparts + d] = entries of warp w's event range destined to rank d. */
+int tgfx_partition_count_device(const tgfx_event* d_events, int64_t n, int reverse,
+                                const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                int64_t* d_counts, void* stream);
+/* Stable scatter of the entries into per-destination records (32-byte tgfx_event: edge_id,
+ * src = node - d_bounds[d] (owner-local id), dst = other endpoint (global id), timestamp) at
+ * d_records[d_offsets[w*nparts + d] + rank in warp w], emission order preserved. */
+int tgfx_partition_scatter_device(const tgfx_event* d_events, int64_t n, int reverse,
+                                  const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                  const int64_t* d_offsets, tgfx_event* d_records, void* stream);
+/* Build one node range from received records (in global stream order): a reverse = 0 build
+ * over num_local_nodes nodes whose neighbour ids stay global (< num_nodes_total). */
+int tgfx_build_range_device(const tgfx_event* d_records, int64_t n, int64_t num_local_nodes,
+                            int64_t num_nodes_total, int64_t num_edges_total, void* stream,
+                            unsigned flags, tgfx_graph** out);
+/* New graph from device columns (copied), e.g. the all-gathered partitions.  Without
+ * TGFX_TRUSTED the slices are checked on the device (sorted, NaN-free) to pick the search. */
+int tgfx_graph_from_device(int64_t num_nodes, int64_t num_edges, int reverse, int64_t m,
+                           const int64_t* d_indptr, const int64_t* d_nbr, const int64_t* d_eid,
+                           const double* d_ts, void* stream, unsigned flags, tgfx_graph** out);
+
 /* ---------------------------------------------------------------- sampling */
 /* replaces tgf::sample_batch (sampler.hpp:42-45, sampler.cpp:84-104) [and sample_recent /
  * sample_random for q = 1, sampler.hpp:32-38].  Query i uses RNG stream stream_base + i

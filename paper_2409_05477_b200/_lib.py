@@ -68,6 +68,12 @@ SIGNATURES = {
     "tgfx_build_device": [_P, _I64, _I64, _I, _P, _U, C.POINTER(_P)],
     "tgfx_rebuild_device": [_P, _P, _P, _U],
     "tgfx_graph_from_host": [_I64, _I64, _I, _I64, _P, _P, _P, _P, C.POINTER(_P)],
+    "tgfx_graph_from_device": [_I64, _I64, _I, _I64, _P, _P, _P, _P, _P, _U, C.POINTER(_P)],
+    "tgfx_build_range_device": [_P, _I64, _I64, _I64, _I64, _P, _U, C.POINTER(_P)],
+    "tgfx_degree_hist_device": [_P, _I64, _I64, _I, _P, _P],
+    "tgfx_partition_warps": [_I64],
+    "tgfx_partition_count_device": [_P, _I64, _I, _P, _I, _I64, _P, _P],
+    "tgfx_partition_scatter_device": [_P, _I64, _I, _P, _I, _I64, _P, _P, _P],
     "tgfx_graph_info": [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I)],
     "tgfx_graph_export": [_P, _P, _P, _P, _P],
     "tgfx_graph_device_arrays": [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
@@ -92,7 +98,7 @@ SIGNATURES = {
     "tgfx_make_queries_device": [_P, _I64, _I64, _I64, _I64, _U64, _P, _P, _P],
 }
 _RESTYPE = {"tgfx_last_error": C.c_char_p, "tgfx_launch_count": C.c_uint64,
-            "tgfx_device_bytes": C.c_int64}
+            "tgfx_device_bytes": C.c_int64, "tgfx_partition_warps": C.c_int64}
 
 _lib = None
 

@@ -141,7 +141,7 @@ void check_queries(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64
 
 void check_int32_outputs(const tgfx_graph* g, int64_t self_edge_index) {
   const int64_t lim = INT32_MAX;
-  if (g->V >= lim || g->max_eid + 1 > lim || g->min_eid + 1 < INT32_MIN ||
+  if (std::max(g->V, g->other_limit) >= lim || g->max_eid + 1 > lim || g->min_eid + 1 < INT32_MIN ||
       self_edge_index > lim || self_edge_index < INT32_MIN)
     throw Error(TGFX_EUNSUPPORTED,
                 "ids do not fit int32 outputs (use tgfx_sample_assemble_device with TGFX_INDEX64)");
@@ -156,6 +156,8 @@ tgfx_graph* new_graph(int64_t n, int64_t V, int reverse, cudaStream_t s) {
   g->V = V;
   g->n = n;
   g->reverse = reverse ? 1 : 0;
+  g->other_limit = V;
+  g->eid_limit = n;
   try {
     graph_alloc(g, s);
   } catch (...) {
@@ -237,6 +239,106 @@ int tgfx_build_device(const tgfx_event* d_events, int64_t n, int64_t num_nodes, 
       throw;
     }
     *out = g;
+  });
+}
+
+int tgfx_build_range_device(const tgfx_event* d_records, int64_t n, int64_t num_local_nodes,
+                            int64_t num_nodes_total, int64_t num_edges_total, void* stream,
+                            unsigned flags, tgfx_graph** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    if (num_nodes_total < num_local_nodes)
+      throw Error(TGFX_EVALIDATION, "num_nodes_total < num_local_nodes");
+    cudaStream_t s = as_stream(stream);
+    tgfx_graph* g = new_graph(n, num_local_nodes, 0, s);
+    g->other_limit = num_nodes_total;
+    g->eid_limit = num_edges_total;
+    try {
+      build_graph(g, d_records, s, (flags & TGFX_TRUSTED) != 0);
+      if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tgfx_graph_from_device(int64_t num_nodes, int64_t num_edges, int reverse, int64_t m,
+                           const int64_t* d_indptr, const int64_t* d_nbr, const int64_t* d_eid,
+                           const double* d_ts, void* stream, unsigned flags, tgfx_graph** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    if (m != num_edges * (reverse ? 2 : 1))
+      throw Error(TGFX_EVALIDATION, "column arrays disagree in length");
+    cudaStream_t s = as_stream(stream);
+    tgfx_graph* g = new_graph(num_edges, num_nodes, reverse, s);
+    try {
+      const auto d2d = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) TGFX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+      };
+      d2d(g->indptr, d_indptr, sizeof(int64_t) * (num_nodes + 1));
+      d2d(g->nbr, d_nbr, sizeof(int64_t) * m);
+      d2d(g->eid, d_eid, sizeof(int64_t) * m);
+      d2d(g->ts, d_ts, sizeof(double) * m);
+      g->min_eid = 0;
+      g->max_eid = num_edges - 1;
+      if (flags & TGFX_TRUSTED) {
+        g->search_exact = 0;  // caller vouches: slices sorted, NaN-free (e.g. built by tgfx)
+      } else {
+        // interpolation search needs sorted, NaN-free slices; otherwise replay lower_bound
+        g->search_exact = (!validate_graph(g, s).empty() || any_nan(g->ts, m, s)) ? 1 : 0;
+      }
+      build_node_dir(g, s);
+      TGFX_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tgfx_degree_hist_device(const tgfx_event* d_events, int64_t n, int64_t num_nodes, int reverse,
+                            uint64_t* d_deg, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    if (num_nodes > 0)
+      TGFX_CUDA(cudaMemsetAsync(d_deg, 0, sizeof(uint64_t) * num_nodes, s));
+    launch_degree_hist(d_events, n, num_nodes, reverse,
+                       reinterpret_cast<unsigned long long*>(d_deg), s);
+  });
+}
+
+int64_t tgfx_partition_warps(int64_t n) {
+  try {
+    return partition_warps(n);
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+
+int tgfx_partition_count_device(const tgfx_event* d_events, int64_t n, int reverse,
+                                const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                int64_t* d_counts, void* stream) {
+  return guarded([&] {
+    if (nparts < 1 || nparts > 8) throw Error(TGFX_EUNSUPPORTED, "1..8 partitions supported");
+    launch_partition_count(d_events, n, reverse, d_bounds, nparts, nwarps, d_counts,
+                           as_stream(stream));
+  });
+}
+
+int tgfx_partition_scatter_device(const tgfx_event* d_events, int64_t n, int reverse,
+                                  const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                  const int64_t* d_offsets, tgfx_event* d_records, void* stream) {
+  return guarded([&] {
+    if (nparts < 1 || nparts > 8) throw Error(TGFX_EUNSUPPORTED, "1..8 partitions supported");
+    if (n > 0)
+      launch_partition_scatter(d_events, n, reverse, d_bounds, nparts, nwarps, d_offsets,
+                               d_records, as_stream(stream));
   });
 }
 

@@ -53,7 +53,8 @@ __global__ void k_init_flags(BuildFlags* f) {
 // K1: validation + order check + per-chunk node histogram (HIST) -------------------------
 template <int R, bool HIST>
 __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restrict__ ev,
-                                                       int64_t n, int64_t V, int64_t chunk_ev,
+                                                       int64_t n, int64_t V, int64_t Vd,
+                                                       int64_t chunk_ev,
                                                        uint32_t* __restrict__ cnt,
                                                        BuildFlags* flags) {
   extern __shared__ uint32_t hist[];
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
         unsorted |= !ok;
       }
       const bool ok_s = valid && x.src >= 0 && x.src < V;
-      const bool ok_d = valid && x.dst >= 0 && x.dst < V;
+      const bool ok_d = valid && x.dst >= 0 && x.dst < Vd;  // Vd = V unless a range build
       if (valid && !(ok_s && ok_d)) bad = min(bad, (unsigned long long)e);
       if (valid) {
         nan |= x.t != x.t;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kTkWarps * 32) k_scatter(
     for (int r = 0; r < kTkRounds; ++r) {
       const int64_t j = T0 + r * 32 + lane;
       const bool side = R == 2 && (j & 1);
-      const bool ok = j < E1 && x[r].src >= 0 && x[r].src < V && x[r].dst >= 0 && x[r].dst < V;
+      const bool ok = j < E1;  // endpoints validated by k_hist
       node[r] = ok ? static_cast<uint32_t>(side ? x[r].dst : x[r].src) : 0xffffffffu;
       if (side) {  // keep the other endpoint in .dst, so .dst is always the neighbour
         const int64_t a = x[r].src;
@@ -938,14 +939,14 @@ __global__ void k_gather_events(const tgfx_event* __restrict__ ev,
 
 // ------------------------------------------------------------------ large-V path helpers
 template <int R>
-__global__ void k_global_deg(const tgfx_event* __restrict__ ev, int64_t n, int64_t V,
+__global__ void k_global_deg(const tgfx_event* __restrict__ ev, int64_t n, int64_t V, int64_t Vd,
                              uint32_t* deg) {
   const int lane = threadIdx.x & 31;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = b + threadIdx.x;
     Ev x{0, -1, -1, 0.0};
     if (e < n) x = load_event(ev, e);
-    const bool ok = x.src >= 0 && x.src < V && x.dst >= 0 && x.dst < V;
+    const bool ok = x.src >= 0 && x.src < V && x.dst >= 0 && x.dst < Vd;
 #pragma unroll
     for (int side = 0; side < R; ++side) {
       const unsigned long long key = ok ? (unsigned long long)(side ? x.dst : x.src) : ~0ull;
@@ -1001,7 +1002,7 @@ __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __r
 // ------------------------------------------------------------------ validate (tcsr.cpp:54-81)
 __global__ void k_validate(const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
                            const int64_t* __restrict__ eid, const double* __restrict__ ts,
-                           int64_t V, int64_t E, int64_t m, int* err) {
+                           int64_t V, int64_t Vn, int64_t E, int64_t m, int* err) {
   // err codes: 1 indptr endpoints, 2 not monotone, 3 slice not sorted, 4 nbr range, 5 eid range
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1009,7 +1010,7 @@ __global__ void k_validate(const int64_t* __restrict__ indptr, const int64_t* __
   for (int64_t u = t0; u < V; u += stride)
     if (indptr[u] > indptr[u + 1]) atomicMin(err, 2);
   for (int64_t i = t0; i < m; i += stride) {
-    if (nbr[i] < 0 || nbr[i] >= V) atomicMin(err, 4);
+    if (nbr[i] < 0 || nbr[i] >= Vn) atomicMin(err, 4);
     if (eid[i] < 0 || eid[i] >= E) atomicMin(err, 5);
   }
   // sortedness within slices: i and i+1 in the same slice <=> no indptr boundary between
@@ -1217,14 +1218,16 @@ void run_flags_pass(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_
     if (g->reverse) {
       TGFX_CUDA(cudaFuncSetAttribute(k_hist<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      k_hist<2, true><<<C, kHistThreads, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, g->dflags);
+      k_hist<2, true><<<C, kHistThreads, smem, s>>>(d_ev, g->n, V, V, chunk_ev, cnt, g->dflags);
     } else {
       TGFX_CUDA(cudaFuncSetAttribute(k_hist<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      k_hist<1, true><<<C, kHistThreads, smem, s>>>(d_ev, g->n, V, chunk_ev, cnt, g->dflags);
+      k_hist<1, true><<<C, kHistThreads, smem, s>>>(d_ev, g->n, V, g->other_limit, chunk_ev, cnt,
+                                                    g->dflags);
     }
   } else {
-    k_hist<1, false><<<C, kHistThreads, 0, s>>>(d_ev, g->n, V, chunk_ev, nullptr, g->dflags);
+    k_hist<1, false><<<C, kHistThreads, 0, s>>>(d_ev, g->n, V, g->reverse ? V : g->other_limit,
+                                                 chunk_ev, nullptr, g->dflags);
   }
   after_launch("k_hist");
 }
@@ -1385,9 +1388,9 @@ void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
   const int grid = grid_for(std::max(n, m), 256);
   if (n > 0) {
     if (g->reverse)
-      k_global_deg<2><<<grid, 256, 0, s>>>(d_ev, n, V, deg);
+      k_global_deg<2><<<grid, 256, 0, s>>>(d_ev, n, V, V, deg);
     else
-      k_global_deg<1><<<grid, 256, 0, s>>>(d_ev, n, V, deg);
+      k_global_deg<1><<<grid, 256, 0, s>>>(d_ev, n, V, g->other_limit, deg);
     after_launch("k_global_deg");
   }
   scan_u32_to_i64(deg, V, g->indptr, s);
@@ -1516,7 +1519,8 @@ std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {
   const int big = 1 << 30;
   TGFX_CUDA(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, s));
   k_validate<<<grid_for(std::max(g->V, g->m), 256), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
-                                                                 g->V, g->n, g->m, err);
+                                                                 g->V, g->other_limit, g->eid_limit,
+                                                                 g->m, err);
   after_launch("k_validate");
   std::vector<int64_t> ip(static_cast<size_t>(g->V + 1));
   TGFX_CUDA(cudaMemcpyAsync(ip.data(), g->indptr, sizeof(int64_t) * (g->V + 1),

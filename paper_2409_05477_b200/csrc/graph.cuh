@@ -35,6 +35,10 @@ struct tgfx_graph {
   // node directory, 32 B per node: {slice start, slice end, ts[start], ts[end-1]} -- one
   // record gives the sampler both the slice bounds and the interpolation bracket
   NodeDir* dir = nullptr;
+  // bound on the other endpoint (nbr ids): V for an ordinary build; the global node count for
+  // one node range of a partitioned build (reverse = 0, nbr ids stay global)
+  int64_t other_limit = 0;
+  int64_t eid_limit = 0;  // edge ids are < eid_limit (n, or the global event count of a range build)
   int64_t max_eid = -1, min_eid = 0;
   // build workspace, kept for rebuilds
   void* ws = nullptr;  // per-chunk node count / cursor table
@@ -118,6 +122,18 @@ void launch_random_stream(int64_t E, int64_t V, uint64_t seed, double zipf, tgfx
                           cudaStream_t s);
 void launch_make_queries(const tgfx_event* ev, int64_t e0, int64_t e1, int64_t batch, int64_t V,
                          uint64_t neg_seed, int64_t* nodes, double* times, cudaStream_t s);
+
+// ------------------------------------------------------------------ partitioned build
+void launch_degree_hist(const tgfx_event* ev, int64_t n, int64_t V, int reverse,
+                        unsigned long long* deg, cudaStream_t s);
+int64_t partition_warps(int64_t n);
+void launch_partition_count(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
+                            int N, int64_t nw, int64_t* counts, cudaStream_t s);
+void launch_partition_scatter(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
+                              int N, int64_t nw, const int64_t* offs, tgfx_event* out,
+                              cudaStream_t s);
+// 1 if any ts is NaN
+bool any_nan(const double* ts, int64_t m, cudaStream_t s);
 
 // ------------------------------------------------------------------ primitives
 // exclusive scan of n uint32 counts into int64 offsets (out has n+1 entries: out[n] = total)

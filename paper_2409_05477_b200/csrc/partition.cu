@@ -1,0 +1,190 @@
+// partition.cu -- kernels of the node-range-partitioned multi-GPU T-CSR build (sm_100a).
+//
+// The reference has no distributed construction; this is the MAG-scale build
+// of BASELINE.json's north star.  Each rank holds a contiguous chunk of the
+// stream; the host (paper_2409_05477_b200/partition.py) drives:
+//   1. k_degree_hist   per-rank node degrees (src, and dst if reverse) -> all-reduce
+//   2. node ranges     split so every rank owns ~m/N entries (host, from the global degrees)
+//   3. k_part_count    per-warp entry counts per destination rank
+//   4. k_part_scatter  stable partition of the rank's entries into per-destination buckets of
+//                      32-byte records (eid, node - owner's first node, other endpoint, t): the
+//                      record is a TemporalEvent whose src is the owner-local node id, so the
+//                      owner builds its range with the ordinary builder (reverse = 0, other
+//                      endpoint checked against the global node count)
+//   5. one all-to-all-v of the records (NCCL); receivers concatenate in rank order, which is
+//      global stream order, so the local build reproduces the single-GPU slices exactly.
+#include <algorithm>
+
+#include "graph.cuh"
+
+namespace tgfx {
+namespace {
+
+constexpr int kPT = 256;
+
+template <int R>
+__global__ void __launch_bounds__(kPT) k_degree_hist(const tgfx_event* __restrict__ ev, int64_t n,
+                                                     int64_t V,
+                                                     unsigned long long* __restrict__ deg) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = blockIdx.x * (int64_t)kPT; b < n; b += (int64_t)gridDim.x * kPT) {
+    const int64_t e = b + threadIdx.x;
+    Ev x{0, -1, -1, 0.0};
+    if (e < n) x = load_event(ev, e);
+#pragma unroll
+    for (int side = 0; side < R; ++side) {
+      const int64_t u = side ? x.dst : x.src;
+      const bool ok = u >= 0 && u < V;
+      const unsigned long long key = ok ? static_cast<unsigned long long>(u) : ~0ull;
+      const unsigned peers = __match_any_sync(kFull, key);  // warp-aggregated (Zipf hub)
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&deg[u], static_cast<unsigned long long>(__popc(peers)));
+    }
+  }
+}
+
+__device__ __forceinline__ int owner_of(int64_t u, const int64_t* __restrict__ bounds, int N) {
+  int d = 0;
+  while (d + 1 < N && u >= bounds[d + 1]) ++d;
+  return d;
+}
+
+// entries of warp w's contiguous event range [w*per, (w+1)*per): counts[w * N + d]
+template <int R>
+__global__ void __launch_bounds__(kPT) k_part_count(const tgfx_event* __restrict__ ev, int64_t n,
+                                                    int64_t per, const int64_t* __restrict__ bounds,
+                                                    int N, int64_t nw, int64_t* __restrict__ counts) {
+  __shared__ int64_t sb[9];
+  if (threadIdx.x <= N) sb[threadIdx.x] = bounds[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kPT + threadIdx.x) >> 5;
+  if (w >= nw) return;
+  const int64_t e0 = w * per, e1 = min(n, e0 + per);
+  int64_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const Ev x = load_event(ev, e);
+#pragma unroll
+    for (int side = 0; side < R; ++side) {
+      const int d = owner_of(side ? x.dst : x.src, sb, N);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] += (k == d);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t v = c[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0 && k < N) counts[w * N + k] = v;
+  }
+}
+
+// stable scatter: offs[w * N + d] = first output slot of warp w's records for rank d
+template <int R>
+__global__ void __launch_bounds__(kPT) k_part_scatter(const tgfx_event* __restrict__ ev, int64_t n,
+                                                      int64_t per, const int64_t* __restrict__ bounds,
+                                                      int N, int64_t nw,
+                                                      const int64_t* __restrict__ offs,
+                                                      tgfx_event* __restrict__ out) {
+  __shared__ int64_t sb[9];
+  if (threadIdx.x <= N) sb[threadIdx.x] = bounds[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kPT + threadIdx.x) >> 5;
+  if (w >= nw) return;
+  const int64_t e0 = w * per, e1 = min(n, e0 + per);
+  int64_t cur[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cur[k] = k < N ? offs[w * N + k] : 0;
+  for (int64_t b = e0; b < e1; b += 32) {
+    const int64_t e = b + lane;
+    const bool ok = e < e1;
+    Ev x{0, 0, 0, 0.0};
+    if (ok) x = load_event(ev, e);
+    // emission order: src entry of event e, then its dst entry (tcsr.cpp:99-102)
+#pragma unroll
+    for (int side = 0; side < R; ++side) {
+      const int64_t u = side ? x.dst : x.src;
+      const int64_t other = side ? x.src : x.dst;
+      const int d = ok ? owner_of(u, sb, N) : -1;
+      int64_t pos = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k >= N) break;
+        const unsigned m = __ballot_sync(kFull, d == k);
+        if (d == k) pos = cur[k] + __popc(m & lanemask_lt());
+        cur[k] += __popc(m);
+      }
+      if (ok) {
+        longlong2* o = reinterpret_cast<longlong2*>(out + pos);
+        o[0] = make_longlong2(x.eid, u - sb[d]);
+        o[1] = make_longlong2(other, __double_as_longlong(x.t));
+      }
+    }
+  }
+}
+
+__global__ void k_any_nan(const double* __restrict__ ts, int64_t m, int* flag) {
+  bool nan = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    nan |= ts[i] != ts[i];
+  if (__any_sync(kFull, nan) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+}  // namespace
+
+bool any_nan(const double* ts, int64_t m, cudaStream_t s) {
+  if (m <= 0) return false;
+  int* d = static_cast<int*>(dmalloc(sizeof(int), s));
+  TGFX_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), device_info().sms * 8));
+  k_any_nan<<<grid, 256, 0, s>>>(ts, m, d);
+  after_launch("k_any_nan");
+  int h = 0;
+  TGFX_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaStreamSynchronize(s));
+  dfree(d, s);
+  return h != 0;
+}
+
+void launch_degree_hist(const tgfx_event* ev, int64_t n, int64_t V, int reverse,
+                        unsigned long long* deg, cudaStream_t s) {
+  if (n <= 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, kPT), device_info().sms * 8));
+  if (reverse)
+    k_degree_hist<2><<<grid, kPT, 0, s>>>(ev, n, V, deg);
+  else
+    k_degree_hist<1><<<grid, kPT, 0, s>>>(ev, n, V, deg);
+  after_launch("k_degree_hist");
+}
+
+int64_t partition_warps(int64_t n) {
+  // one warp per >= 4096 events, at most 16 warps per SM
+  return std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 4096), device_info().sms * 16LL));
+}
+
+void launch_partition_count(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
+                            int N, int64_t nw, int64_t* counts, cudaStream_t s) {
+  const int64_t per = ceil_div(std::max<int64_t>(n, 1), nw);
+  const int grid = static_cast<int>(ceil_div(nw * 32, kPT));
+  if (reverse)
+    k_part_count<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, counts);
+  else
+    k_part_count<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, counts);
+  after_launch("k_part_count");
+}
+
+void launch_partition_scatter(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
+                              int N, int64_t nw, const int64_t* offs, tgfx_event* out,
+                              cudaStream_t s) {
+  const int64_t per = ceil_div(std::max<int64_t>(n, 1), nw);
+  const int grid = static_cast<int>(ceil_div(nw * 32, kPT));
+  if (reverse)
+    k_part_scatter<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, offs, out);
+  else
+    k_part_scatter<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, offs, out);
+  after_launch("k_part_scatter");
+}
+
+}  // namespace tgfx

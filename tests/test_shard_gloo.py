@@ -81,3 +81,19 @@ def test_sharded_sampling_equals_single_process(tmp_path):
         assert np.array_equal(got[strat], want), strat
     assert got["t"].tolist() == [2.0, 5.0]          # max over ranks, element-wise
     assert got["s"].tolist() == [float(len(nodes))]  # shards cover every query once
+
+
+def test_partition_plan_balances_entries():
+    """plan_bounds / plan_offsets (partition.py), pure host arithmetic."""
+    from paper_2409_05477_b200 import partition as P
+    deg = torch.tensor([50, 1, 1, 1, 30, 2, 2, 2, 2, 9], dtype=torch.int64)
+    for world in (1, 2, 3, 4, 8):
+        b = P.plan_bounds(deg, world)
+        assert b[0] == 0 and b[-1] == len(deg) and bool((b[1:] >= b[:-1]).all())
+        assert len(b) == world + 1
+    b = P.plan_bounds(deg, 2)
+    assert b.tolist() == [0, 1, 10]  # the hub (50 of 100 entries) fills rank 0
+    counts = torch.tensor([[3, 1], [0, 2], [4, 0]], dtype=torch.int64)
+    offs, send = P.plan_offsets(counts, 2)
+    assert send.tolist() == [7, 3]
+    assert offs.tolist() == [[0, 7], [3, 8], [3, 10]]
