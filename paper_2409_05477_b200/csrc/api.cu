@@ -542,6 +542,11 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
   });
 }
 
+// Host-buffer sample_assemble, pipelined: the output rows (136 B/query at l = 11) dwarf the
+// inputs (16 B/query), so the call is bound by device->host copies.  Node ids go up first
+// (every query is validated before any output is written, sampler.cpp:88-93); then the
+// queries are processed in sub-chunks on two streams, so the times upload of one sub-chunk,
+// the kernel of the next and the row download of the previous overlap on the copy engines.
 int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double* times,
                          int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
                          int64_t l, int64_t self_edge_index, int32_t* node_index,
@@ -550,39 +555,77 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     check_graph(g);
     cudaStream_t s = 0;
     const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
-    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
+    DBuf dn(sizeof(int64_t) * qb, s);
     h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
-    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
-    check_queries(g, dn.as<int64_t>(), q, k, s);
+    check_queries(g, dn.as<int64_t>(), q, k, s);  // synchronises
     check_l(l);
     check_int32_outputs(g, self_edge_index);
     if (q == 0) return;
-    const size_t ql = qb * static_cast<size_t>(l);
-    DBuf on(sizeof(int32_t) * ql, s), oe(sizeof(int32_t) * ql, s), ov(sizeof(int32_t) * qb, s);
-    DBuf o32(dt32 ? sizeof(float) * ql : 16, s), o64(dt64 ? sizeof(double) * ql : 16, s);
-    SampleArgs a{};
-    a.g = g;
-    a.nodes = dn.as<int64_t>();
-    a.times = dt.as<double>();
-    a.q = q;
-    a.k = k;
-    a.strategy = strategy;
-    a.seed = seed;
-    a.stream_base = stream_base;
-    a.l = l;
-    a.self_edge_index = self_edge_index;
-    a.node_index = on.p;
-    a.edge_index = oe.p;
-    a.dt32 = dt32 ? o32.as<float>() : nullptr;
-    a.dt64 = dt64 ? o64.as<double>() : nullptr;
-    a.valid_len = ov.p;
-    launch_sample(a, s);
-    d2h(node_index, on.p, sizeof(int32_t) * q * l, s);
-    d2h(edge_index, oe.p, sizeof(int32_t) * q * l, s);
-    d2h(dt32, o32.p, dt32 ? sizeof(float) * q * l : 0, s);
-    d2h(dt64, o64.p, dt64 ? sizeof(double) * q * l : 0, s);
-    d2h(valid_len, ov.p, sizeof(int32_t) * q, s);
-    TGFX_CUDA(cudaStreamSynchronize(s));
+    constexpr int kStreams = 2;
+    const int64_t sub = std::min<int64_t>(q, int64_t(1) << 22);  // 4 M queries per sub-chunk
+    const size_t sl = static_cast<size_t>(sub) * static_cast<size_t>(l);
+    struct Lane {
+      cudaStream_t st = nullptr;
+      void *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr, *o64 = nullptr,
+           *ov = nullptr;
+    } lanes[kStreams];
+    auto release = [&] {
+      for (Lane& ln : lanes) {
+        if (!ln.st) continue;
+        cudaStreamSynchronize(ln.st);
+        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
+          if (p) cudaFreeAsync(p, ln.st);
+        cudaStreamSynchronize(ln.st);
+        cudaStreamDestroy(ln.st);
+        ln.st = nullptr;
+      }
+    };
+    try {
+      for (Lane& ln : lanes) {
+        TGFX_CUDA(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+        ln.t = dmalloc(sizeof(double) * sub, ln.st);
+        ln.on = dmalloc(sizeof(int32_t) * sl, ln.st);
+        ln.oe = dmalloc(sizeof(int32_t) * sl, ln.st);
+        if (dt32) ln.o32 = dmalloc(sizeof(float) * sl, ln.st);
+        if (dt64) ln.o64 = dmalloc(sizeof(double) * sl, ln.st);
+        ln.ov = dmalloc(sizeof(int32_t) * sub, ln.st);
+      }
+      int i = 0;
+      for (int64_t c0 = 0; c0 < q; c0 += sub, ++i) {
+        Lane& ln = lanes[i % kStreams];
+        const int64_t c = std::min(sub, q - c0);
+        const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
+        h2d(ln.t, times + c0, sizeof(double) * c, ln.st);
+        SampleArgs a{};
+        a.g = g;
+        a.nodes = dn.as<int64_t>() + c0;
+        a.times = static_cast<const double*>(ln.t);
+        a.q = c;
+        a.k = k;
+        a.strategy = strategy;
+        a.seed = seed;
+        a.stream_base = stream_base + static_cast<uint64_t>(c0);
+        a.l = l;
+        a.self_edge_index = self_edge_index;
+        a.node_index = ln.on;
+        a.edge_index = ln.oe;
+        a.dt32 = static_cast<float*>(ln.o32);
+        a.dt64 = static_cast<double*>(ln.o64);
+        a.valid_len = ln.ov;
+        launch_sample(a, ln.st);
+        const size_t r0 = static_cast<size_t>(c0) * static_cast<size_t>(l);
+        d2h(node_index + r0, ln.on, sizeof(int32_t) * cl, ln.st);
+        d2h(edge_index + r0, ln.oe, sizeof(int32_t) * cl, ln.st);
+        if (dt32) d2h(dt32 + r0, ln.o32, sizeof(float) * cl, ln.st);
+        if (dt64) d2h(dt64 + r0, ln.o64, sizeof(double) * cl, ln.st);
+        d2h(valid_len + c0, ln.ov, sizeof(int32_t) * c, ln.st);
+      }
+      for (Lane& ln : lanes) TGFX_CUDA(cudaStreamSynchronize(ln.st));
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
   });
 }
 
