@@ -410,13 +410,15 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
       a[j] = max(A[j] - d[j].start, lo[j]);
       b[j] = min(A[j] - d[j].start + W, hi[j]);
       if (len > 0) {
-        const double2* src = reinterpret_cast<const double2*>(ts + A[j]);
+        // 256-bit loads (LDG.E.ENL2.256, sm_100): one L1 wavefront per 32-byte sector
+        // instead of two 128-bit loads per sector -- the probe loop is L1-throughput-bound
+        const double* src = ts + A[j];
 #pragma unroll
-        for (int w = 0; w < W / 2; ++w) {
-          const double2 x = __ldg(src + w);
-          v[j][2 * w] = x.x;
-          v[j][2 * w + 1] = x.y;
-        }
+        for (int w = 0; w < W / 4; ++w)
+          asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                       : "=d"(v[j][4 * w]), "=d"(v[j][4 * w + 1]), "=d"(v[j][4 * w + 2]),
+                         "=d"(v[j][4 * w + 3])
+                       : "l"(src + 4 * w));
       }
     }
 #pragma unroll
@@ -451,7 +453,7 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
   for (int j = 0; j < QL; ++j) m[j] = lo[j];
 }
 
-template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB>
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, int EXPERIMENT = 0, bool PF = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
@@ -464,34 +466,74 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = ASSEMBLE ? l : static_cast<int>(k);
   const int64_t ngroups = ceil_div(Q, GQ);
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
-       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  // software pipeline across the warp's groups (grids smaller than one group per warp): the
+  // next group's queries are fetched before this group's search, and their directory
+  // records before this group's gather, so two of the dependent round trips overlap work
+  int64_t nu[QL];
+  double nt[QL];
+  bool npres[QL];
+  NodeDir nd[QL];
+  auto fetch_group = [&](int64_t gg) {
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      const int64_t q = gg * GQ + j * 32 + lane;
+      nu[j] = 0;
+      nt[j] = 0.0;
+      npres[j] = gg < ngroups && q < Q && fetch_query(in, q, nu[j], nt[j]);
+    }
+  };
+  auto fetch_dir = [&]() {
+#pragma unroll
+    for (int j = 0; j < QL; ++j) {
+      if (npres[j]) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(dir + nu[j]);
+        const longlong2 x = __ldg(p), y = __ldg(p + 1);
+        nd[j].start = x.x;
+        nd[j].end = x.y;
+        nd[j].t_first = __longlong_as_double(y.x);
+        nd[j].t_last = __longlong_as_double(y.y);
+      } else {
+        nd[j].start = nd[j].end = 0;
+        nd[j].t_first = nd[j].t_last = 0.0;
+      }
+    }
+  };
+  int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  fetch_group(g);
+  fetch_dir();
+  for (; g < ngroups; g += gstride) {
     int64_t u[QL], m[QL];
     double t[QL];
     bool pres[QL];
     NodeDir d[QL];
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
-      const int64_t q = g * GQ + j * 32 + lane;
-      u[j] = 0;
-      t[j] = 0.0;
-      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
+      u[j] = nu[j];
+      t[j] = nt[j];
+      pres[j] = npres[j];
+      d[j] = nd[j];
     }
+    if (PF) fetch_group(g + gstride);
+    if (EXPERIMENT == 2) {  // timing experiment: no search (window = the slice's tail)
 #pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      if (pres[j]) {
-        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[j]);
-        const longlong2 x = __ldg(p), y = __ldg(p + 1);
-        d[j].start = x.x;
-        d[j].end = x.y;
-        d[j].t_first = __longlong_as_double(y.x);
-        d[j].t_last = __longlong_as_double(y.y);
-      } else {
-        d[j].start = d[j].end = 0;
-        d[j].t_first = d[j].t_last = 0.0;
-      }
+      for (int j = 0; j < QL; ++j) m[j] = d[j].end - d[j].start;
+    } else {
+      search_lines<W, QL>(ts, d, pres, t, m);
     }
-    search_lines<W, QL>(ts, d, pres, t, m);
+    if (PF) fetch_dir();
+    if (EXPERIMENT == 1) {  // timing experiment: search only
+#pragma unroll
+      for (int j = 0; j < QL; ++j) {
+        const int64_t q = g * GQ + j * 32 + lane;
+        if (q < Q) write_vlen<IDX64>(o, q, m[j]);
+      }
+      if (!PF) {
+        fetch_group(g + gstride);
+        fetch_dir();
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
       const int64_t q = g * GQ + j * 32 + lane;
@@ -550,6 +592,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       }
     }
     __syncwarp();
+    if (!PF) {
+      fetch_group(g + gstride);
+      fetch_dir();
+    }
   }
 }
 
@@ -998,6 +1044,193 @@ int grid_groups(int64_t Q) {
   return static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(device_info().sms) * 8));
 }
 
+// ------------------------------------------------------------------ uniform-k, k <= 32
+// Default uniform-k kernel for k <= 32 (LastFM-shaped uniform-20).  Phase 1: one query per
+// lane, line-probe search through the node directory (as k_recent_line).  Phase 2: Floyd's
+// algorithm with the reference's counter RNG (rng.hpp:23-38, sampler.cpp:66-80) run by
+// 8-lane groups, four queries per warp at a time: lane r of a group draws d = r, r+8, ...
+// (O(1) skip-ahead), the draws are resolved in order d = 0..k-1 with one group-masked ballot
+// each, and every chosen offset is ranked against the group's others with width-8 shuffles.
+// Resolution is inherently sequential in d; running four queries per warp through it (instead
+// of one) is what keeps small batches (12,000 queries) from being latency-bound.
+template <int P, bool ASSEMBLE, bool IDX64>
+__global__ void __launch_bounds__(kThreads) k_random_g(
+    const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
+    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, Outs o) {
+  constexpr int G = 8;                      // lanes per query
+  constexpr int NG = 32 / G;                // queries per warp round
+  __shared__ int64_t s_lo[kWarps][32], s_m[kWarps][32], s_u[kWarps][32];
+  __shared__ double s_t[kWarps][32];
+  __shared__ int s_pres[kWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / G, r = lane % G;
+  const unsigned gmask = ((1u << G) - 1u) << (grp * G);
+  const int kk = static_cast<int>(k);
+  const uint64_t seed_mix = mix64(seed);
+  const int64_t ngroups = ceil_div(Q, 32);
+  for (int64_t gq = static_cast<int64_t>(blockIdx.x) * kWarps + warp; gq < ngroups;
+       gq += static_cast<int64_t>(gridDim.x) * kWarps) {
+    {  // phase 1: one query per lane
+      const int64_t q = gq * 32 + lane;
+      int64_t u[1] = {0}, m[1];
+      double t[1] = {0.0};
+      bool pres[1];
+      pres[0] = q < Q && fetch_query(in, q, u[0], t[0]);
+      NodeDir d[1];
+      if (pres[0]) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[0]);
+        const longlong2 x = __ldg(p), y = __ldg(p + 1);
+        d[0].start = x.x;
+        d[0].end = x.y;
+        d[0].t_first = __longlong_as_double(y.x);
+        d[0].t_last = __longlong_as_double(y.y);
+      } else {
+        d[0].start = d[0].end = 0;
+        d[0].t_first = d[0].t_last = 0.0;
+      }
+      search_lines<8, 1>(ts, d, pres, t, m);
+      s_lo[warp][lane] = d[0].start;
+      s_m[warp][lane] = m[0];
+      s_u[warp][lane] = u[0];
+      s_t[warp][lane] = t[0];
+      s_pres[warp][lane] = pres[0] ? 1 : 0;
+    }
+    __syncwarp();
+    const int nq = static_cast<int>(min((int64_t)32, Q - gq * 32));
+    for (int q0 = 0; q0 < nq; q0 += NG) {
+      const int qi = q0 + grp;
+      const bool live = qi < nq;
+      const int64_t qq = gq * 32 + qi;
+      const bool pr = live && s_pres[warp][qi];
+      const int64_t qlo = live ? s_lo[warp][qi] : 0;
+      const int64_t qm = live ? s_m[warp][qi] : 0;
+      const int64_t qu = live ? s_u[warp][qi] : 0;
+      const double qt = live ? s_t[warp][qi] : 0.0;
+      const bool floyd = pr && qm > k;
+      // Floyd (all groups run the loop so the shuffles/ballots see every lane)
+      const uint64_t s0 = mix64(seed_mix ^ ((stream_base + static_cast<uint64_t>(qq)) * kStreamMul));
+      int64_t jd[P], c[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int dd = p * G + r;
+        const uint64_t bound = static_cast<uint64_t>(qm - kk + dd) + 1;
+        jd[p] = (floyd && dd < kk) ? static_cast<int64_t>(mulhi64(rng_draw(s0, dd), bound)) : -1;
+        c[p] = -1;
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        for (int o2 = 0; o2 < G; ++o2) {
+          const int dd = p * G + o2;
+          if (dd >= kk) break;
+          const int64_t jv = __shfl_sync(kFull, jd[p], o2, G);
+          bool hit = false;
+#pragma unroll
+          for (int p2 = 0; p2 <= p; ++p2) hit |= (p2 < p || r < o2) && c[p2] == jv;
+          hit = (__ballot_sync(kFull, hit) & gmask) != 0;
+          if (r == o2) c[p] = hit ? (qm - kk + dd) : jv;
+        }
+      }
+      int rank[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) rank[p] = 0;
+#pragma unroll
+      for (int p2 = 0; p2 < P; ++p2) {
+        for (int o2 = 0; o2 < G; ++o2) {
+          if (p2 * G + o2 >= kk) break;
+          const int64_t v = __shfl_sync(kFull, c[p2], o2, G);
+#pragma unroll
+          for (int p = 0; p < P; ++p) rank[p] += v < c[p];
+        }
+      }
+      if (!live) continue;
+      if (ASSEMBLE) {
+        if (!pr) {  // absent hop-2 slot
+          for (int j = r; j < l; j += G) write_slot<IDX64>(o, qq * l + j, 0, 0, 0.0);
+          if (r == 0) write_vlen<IDX64>(o, qq, 0);
+          continue;
+        }
+        if (!floyd) {  // whole prefix (sampler.cpp:59-63), most recent l-1 kept
+          const int kb = static_cast<int>(min(qm, (int64_t)(l - 1)));
+          const int64_t start = qlo + qm - kb;
+          for (int j = r; j < l; j += G) {
+            int64_t ni = 0, ei = 0;
+            double dt = 0.0;
+            if (j < kb) {
+              ni = ldg_i64(nbr + start + j) + 1;
+              ei = ldg_i64(eid + start + j) + 1;
+              dt = qt - ldg_f64(ts + start + j);
+            } else if (j == kb) {
+              ni = qu + 1;
+              ei = self_idx;
+            }
+            write_slot<IDX64>(o, qq * l + j, ni, ei, dt);
+          }
+          if (r == 0) write_vlen<IDX64>(o, qq, kb + 1);
+          continue;
+        }
+        const int kb = min(kk, l - 1);
+        const int drop = kk - kb;  // keep the most recent l-1 (sequence.cpp:70-71)
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int dd = p * G + r;
+          if (dd < kk && rank[p] >= drop) {
+            const int64_t pos = qlo + c[p];
+            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ldg_i64(nbr + pos) + 1,
+                              ldg_i64(eid + pos) + 1, qt - ldg_f64(ts + pos));
+          }
+        }
+        for (int j = kb + r; j < l; j += G)
+          write_slot<IDX64>(o, qq * l + j, j == kb ? qu + 1 : 0, j == kb ? self_idx : 0, 0.0);
+        if (r == 0) write_vlen<IDX64>(o, qq, kb + 1);
+      } else {
+        if (!floyd) {
+          const int64_t take = pr ? qm : 0;
+          for (int j = r; j < kk; j += G) {
+            const bool h = j < take;
+            o.e_nbr[qq * k + j] = h ? ldg_i64(nbr + qlo + j) : 0;
+            o.e_eid[qq * k + j] = h ? ldg_i64(eid + qlo + j) : 0;
+            o.e_ts[qq * k + j] = h ? ldg_f64(ts + qlo + j) : 0.0;
+          }
+          if (r == 0) o.counts[qq] = take;
+          continue;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int dd = p * G + r;
+          if (dd < kk) {
+            const int64_t pos = qlo + c[p];
+            o.e_nbr[qq * k + rank[p]] = ldg_i64(nbr + pos);
+            o.e_eid[qq * k + rank[p]] = ldg_i64(eid + pos);
+            o.e_ts[qq * k + rank[p]] = ldg_f64(ts + pos);
+          }
+        }
+        if (r == 0) o.counts[qq] = kk;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <bool ASM, bool I64>
+void launch_random_g(const SampleArgs& a, const QueryIn& in, const Outs& o, int grid,
+                     cudaStream_t s) {
+  const tgfx_graph* g = a.g;
+  const int l = static_cast<int>(a.l);
+#define TGFX_RANDOM_G(PP)                                                                      \
+  k_random_g<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, \
+                                                     l, a.self_edge_index, a.seed,             \
+                                                     a.stream_base, o);
+  if (a.k <= 8)
+    TGFX_RANDOM_G(1)
+  else if (a.k <= 16)
+    TGFX_RANDOM_G(2)
+  else
+    TGFX_RANDOM_G(4)
+#undef TGFX_RANDOM_G
+  after_launch("k_random_g");
+}
+
 template <bool ASM, bool I64>
 void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& o, int grid,
                      cudaStream_t s) {
@@ -1067,6 +1300,19 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
           g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, g->search_exact, o);    \
   }
     if (variant >= 30 && !g->search_exact) {  // line-probe kernel (default)
+#define TGFX_LINE_EXP(X)                                                                        \
+  {                                                                                             \
+    const int gl = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX)); \
+    k_recent_line<true, false, 8, 1, 4, X><<<gl, kThreads, 0, s>>>(                             \
+        g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);           \
+  }
+#define TGFX_LINE_PF(WAVES)                                                                     \
+  {                                                                                             \
+    const int gl = static_cast<int>(std::min<int64_t>(                                          \
+        ceil_div(ceil_div(a.q, 32), kWarps), static_cast<int64_t>(device_info().sms) * 4 * WAVES)); \
+    k_recent_line<true, false, 8, 1, 4, 0, true><<<gl, kThreads, 0, s>>>(                       \
+        g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);           \
+  }
 #define TGFX_LINE_LAUNCH(W, QL, MINB)                                                           \
   {                                                                                             \
     const int gl = static_cast<int>(                                                            \
@@ -1088,6 +1334,11 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
         case 36: TGFX_LINE_LAUNCH(8, 1, 6) break;
         case 37: TGFX_LINE_LAUNCH(4, 1, 6) break;
         case 38: TGFX_LINE_LAUNCH(8, 1, 1) break;
+        case 41: TGFX_LINE_EXP(1) break;
+        case 42: TGFX_LINE_EXP(2) break;
+        case 43: TGFX_LINE_PF(4) break;
+        case 44: TGFX_LINE_PF(8) break;
+        case 45: TGFX_LINE_PF(16) break;
         default: TGFX_LINE_LAUNCH(8, 1, 4) break;
       }
 #undef TGFX_LINE_LAUNCH
@@ -1147,6 +1398,17 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     }
 #undef TGFX_RECENT_LAUNCH
     after_launch("k_recent");
+    return;
+  }
+  if (!g->search_exact && a.k <= 32 && recent_variant() != 29) {  // grouped Floyd (default)
+    if (assemble) {
+      if (a.index64)
+        launch_random_g<true, true>(a, in, o, grid, s);
+      else
+        launch_random_g<true, false>(a, in, o, grid, s);
+    } else {
+      launch_random_g<false, false>(a, in, o, grid, s);
+    }
     return;
   }
   const int P = a.k <= 32 ? 1 : a.k <= 64 ? 2 : a.k <= 128 ? 4 : a.k <= 256 ? 8 : 0;

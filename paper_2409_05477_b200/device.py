@@ -136,3 +136,4 @@ def two_hop(g, roots, times, k1, k2, strategy, seed, l, self_edge_index, seed2=N
         _p(h2["edge_index"]), _p(h2["time_delta"]), _p(h2["valid_len"]), _stream(stream),
         TGFX_TRUSTED if trusted else 0))
     return out
+

@@ -43,7 +43,8 @@ def main(rep, lib, fun_sub, top=30):
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
-    wi = h.index("Warp Stall Sampling (All Samples)")
+    col = os.environ.get("NCU_COLUMN", "Warp Stall Sampling (All Samples)")
+    wi = h.index(col)
     addrs = []
     for r in rows[2:]:
         try:
