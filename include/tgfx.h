@@ -168,6 +168,18 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
                                 float* d_dt32, double* d_dt64, void* d_valid_len, void* stream,
                                 unsigned flags);
 
+/* Many forward_concat batches in one launch (an epoch of training.cpp:211-214 calls): the q
+ * queries are consecutive batches of batch_q; batch b is sampled exactly as
+ * sample_batch(..., seed = d_seeds[b]) would (uniform RNG stream = index within the batch,
+ * sampler.cpp:100-101) and packed as build_sequence_batch.  d_seeds: device array of
+ * ceil(q / batch_q) seeds (may be NULL for TGFX_RECENT).  Flags as tgfx_sample_assemble_device. */
+int tgfx_sample_assemble_batched_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                        const double* d_times, int64_t q, int64_t batch_q,
+                                        int64_t k, int strategy, const uint64_t* d_seeds,
+                                        int64_t l, int64_t self_edge_index, void* d_node_index,
+                                        void* d_edge_index, float* d_dt32, double* d_dt64,
+                                        void* d_valid_len, void* stream, unsigned flags);
+
 /* 2-hop composition (not in the reference): hop-1 = sample_batch(roots,
  * k1) rows [q, l]; hop-2 rows [q, k1, l]: slot j of root r holds the row of the query
  * (nbr_j, ts_j) of hop-1 entry j (recent-k2, or sample_random(seed2, stream = r*k1 + j));

@@ -542,6 +542,47 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
   });
 }
 
+int tgfx_sample_assemble_batched_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                        const double* d_times, int64_t q, int64_t batch_q,
+                                        int64_t k, int strategy, const uint64_t* d_seeds,
+                                        int64_t l, int64_t self_edge_index, void* d_node_index,
+                                        void* d_edge_index, float* d_dt32, double* d_dt64,
+                                        void* d_valid_len, void* stream, unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    if (batch_q < 1) throw Error(TGFX_EVALIDATION, "batch size must be at least 1");
+    if (strategy == TGFX_RANDOM && !d_seeds && q > 0)
+      throw Error(TGFX_EVALIDATION, "per-batch seeds required for uniform sampling");
+    cudaStream_t s = as_stream(stream);
+    if (!(flags & TGFX_TRUSTED)) check_queries(g, d_nodes, q, k, s);
+    check_k(k);
+    check_l(l);
+    const bool i64 = (flags & TGFX_INDEX64) != 0;
+    if (!i64) check_int32_outputs(g, self_edge_index);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = d_nodes;
+    a.times = d_times;
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = 0;
+    a.stream_base = 0;
+    a.l = l;
+    a.self_edge_index = self_edge_index;
+    a.node_index = d_node_index;
+    a.edge_index = d_edge_index;
+    a.dt32 = d_dt32;
+    a.dt64 = d_dt64;
+    a.valid_len = d_valid_len;
+    a.index64 = i64;
+    a.seeds = d_seeds;
+    a.batch_q = batch_q;
+    launch_sample(a, s);
+    if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 // Host-buffer sample_assemble, pipelined: the output rows (136 B/query at l = 11) dwarf the
 // inputs (16 B/query), so the call is bound by device->host copies.  Node ids go up first
 // (every query is validated before any output is written, sampler.cpp:88-93); then the

@@ -97,6 +97,9 @@ struct SampleArgs {
   // hop-2 mode: query (nodes, times) given padded [q_roots, k1] with per-root counts
   const int64_t* hop_counts = nullptr;
   int64_t hop_k1 = 0;
+  // batched uniform sampling: batch b = query / batch_q uses seeds[b] (device array)
+  const uint64_t* seeds = nullptr;
+  int64_t batch_q = 0;
 };
 
 // first invalid query index (or -1); validates node range on device (sampler.cpp:22-27)

@@ -39,7 +39,22 @@ struct QueryIn {
   const double* times;
   const int64_t* hop_counts;  // hop-2 mode: presence of virtual query qq = r*k1 + j
   int64_t hop_k1;
+  // batched mode (uniform-k): query qq belongs to batch b = qq / batch_q, sampled as one
+  // sample_batch(seed = seeds[b]) call: RNG stream = qq - b * batch_q (sampler.cpp:100-101)
+  const uint64_t* seeds = nullptr;
+  int64_t batch_q = 0;
 };
+
+// CounterRng(seed, stream) initial state of query qq (rng.hpp:23-24)
+__device__ __forceinline__ uint64_t query_rng(const QueryIn& in, uint64_t seed_mix,
+                                              uint64_t stream_base, int64_t qq) {
+  if (in.seeds) {
+    const int64_t b = qq / in.batch_q;
+    return mix64(mix64(__ldg(reinterpret_cast<const unsigned long long*>(in.seeds) + b)) ^
+                 (static_cast<uint64_t>(qq - b * in.batch_q) * kStreamMul));
+  }
+  return mix64(seed_mix ^ ((stream_base + static_cast<uint64_t>(qq)) * kStreamMul));
+}
 
 __device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_t& u, double& t) {
   if (in.hop_counts) {
@@ -459,9 +474,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
   constexpr int GQ = 32 * QL;
-  __shared__ int64_t s_start[kWarps][GQ];
+  __shared__ longlong2 s_st[kWarps][GQ];  // {window start, query time bits}: one LDS.128
   __shared__ int64_t s_u[kWarps][GQ];
-  __shared__ double s_t[kWarps][GQ];
   __shared__ int s_kb[kWarps][GQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = ASSEMBLE ? l : static_cast<int>(k);
@@ -549,9 +563,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
           o.counts[q] = max(kb, 0);
       }
       const int qi = j * 32 + lane;
-      s_start[warp][qi] = d[j].start + m[j] - kb;
+      s_st[warp][qi] = make_longlong2(d[j].start + m[j] - kb, __double_as_longlong(t[j]));
       s_u[warp][qi] = u[j];
-      s_t[warp][qi] = t[j];
       s_kb[warp][qi] = kb;
     }
     __syncwarp();
@@ -559,19 +572,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const int nq = static_cast<int>(min(static_cast<int64_t>(GQ), Q - qbase));
     const int total = nq * width;
     const int64_t obase = qbase * width;
+    // slot s = lane + 32 i of the warp's [nq x width] block: (query, column) advanced
+    // incrementally instead of divided per slot
+    int qi = div_slot(lane, width, magic);
+    int j = lane - qi * width;
+    const int dq = div_slot(32, width, magic), dj = 32 - dq * width;
 #pragma unroll 4
     for (int s = lane; s < total; s += 32) {
-      const int qi = div_slot(s, width, magic);
-      const int j = s - qi * width;
       const int kbq = s_kb[warp][qi];
       if (ASSEMBLE) {
         int64_t ni = 0, ei = 0;
         double dt = 0.0;
         if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
+          const longlong2 st = s_st[warp][qi];
+          const int64_t p = st.x + j;
           ni = ldg_i64(nbr + p) + 1;
           ei = ldg_i64(eid + p) + 1;
-          dt = s_t[warp][qi] - ldg_f64(ts + p);
+          dt = __longlong_as_double(st.y) - ldg_f64(ts + p);
         } else if (j == kbq) {
           ni = s_u[warp][qi] + 1;
           ei = self_idx;
@@ -581,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
         int64_t a = 0, b = 0;
         double c = 0.0;
         if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
+          const int64_t p = s_st[warp][qi].x + j;
           a = ldg_i64(nbr + p);
           b = ldg_i64(eid + p);
           c = ldg_f64(ts + p);
@@ -589,6 +606,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
         o.e_nbr[obase + s] = a;
         o.e_eid[obase + s] = b;
         o.e_ts[obase + s] = c;
+      }
+      j += dj;
+      qi += dq;
+      if (j >= width) {
+        j -= width;
+        ++qi;
       }
     }
     __syncwarp();
@@ -885,7 +908,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
       }
       // Floyd: for d = 0..k-1, i_d = m-k+d, j_d = next_below(i_d+1); c_d = j_d unless already
       // chosen, then i_d.  Draws are independent of the resolution (one draw per iteration).
-      const uint64_t s0 = mix64(seed_mix ^ ((stream_base + static_cast<uint64_t>(qq)) * kStreamMul));
+      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq);
       int64_t jd[P], c[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -1109,7 +1132,7 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
       const double qt = live ? s_t[warp][qi] : 0.0;
       const bool floyd = pr && qm > k;
       // Floyd (all groups run the loop so the shuffles/ballots see every lane)
-      const uint64_t s0 = mix64(seed_mix ^ ((stream_base + static_cast<uint64_t>(qq)) * kStreamMul));
+      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq);
       int64_t jd[P], c[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -1273,7 +1296,7 @@ int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, c
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (a.q <= 0) return;
   const tgfx_graph* g = a.g;
-  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1};
+  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q};
   Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
          a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
   const int grid = grid_groups(a.q);

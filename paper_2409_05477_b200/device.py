@@ -108,6 +108,21 @@ def sample_assemble(g, nodes, times, k, strategy, seed, l, self_edge_index, out=
     return out
 
 
+def sample_assemble_batched(g, nodes, times, batch_q, k, strategy, seeds, l, self_edge_index,
+                            out=None, trusted=False, index64=False, dt64=False, stream=None):
+    """One launch for many forward_concat batches of batch_q queries; batch b uses seeds[b]
+    (int64/uint64 device tensor) -- equal to one sample_assemble call per batch."""
+    q = nodes.numel()
+    if out is None:
+        out = alloc_rows(q, l, index64=index64, dt64=dt64)
+    flags = (TGFX_TRUSTED if trusted else 0) | (TGFX_INDEX64 if index64 else 0)
+    check(lib().tgfx_sample_assemble_batched_device(
+        g.handle, _p(nodes), _p(times), q, batch_q, k, _strategy_code(strategy), _p(seeds), l,
+        self_edge_index, _p(out["node_index"]), _p(out["edge_index"]), _p(out.get("time_delta")),
+        _p(out.get("time_delta64")), _p(out["valid_len"]), _stream(stream), flags))
+    return out
+
+
 def sample_batch(g, nodes, times, k, strategy, seed, stream_base=0, trusted=False, stream=None):
     """sample_batch into padded device arrays: counts [Q], nbr/eid/ts [Q, k]."""
     q = nodes.numel()

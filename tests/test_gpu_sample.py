@@ -265,3 +265,30 @@ def test_exact_search_on_unsorted_or_nan_slices(T, oracle_mod):
         assert np.array_equal(got["valid_len"].astype(np.int64), want["valid_len"]), strat
         # NaN entries: compare as values (the payload bits of a NaN result are not specified)
         assert np.array_equal(got["time_delta64"], want["time_delta"], equal_nan=True), strat
+
+
+def test_batched_launch_equals_one_call_per_batch(T, oracle_mod):
+    """tgfx_sample_assemble_batched_device: many forward_concat batches in one launch, batch b
+    sampled with seeds[b] and stream = index within the batch -- must equal one
+    sample_batch + build_sequence_batch per batch (the oracle, and the per-batch device call)."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V, B = 200_000, 1980, 4000
+    ev = D.random_stream(E, V, 42)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 0, 60_000, B, V)
+    qb = 3 * B
+    nb = -(-nodes.numel() // qb)
+    seeds = torch.tensor([(0x9E3779B97F4A7C15 * (b + 1)) & (2**63 - 1) for b in range(nb)],
+                         dtype=torch.int64, device="cuda")
+    h_ev = ev.cpu().numpy().view(oracle_mod.EVENT_DTYPE)
+    og = oracle_mod.build(h_ev, V, True)
+    hn, ht = nodes.cpu().numpy(), times.cpu().numpy()
+    for strat, k, l in (("random", 20, 21), ("recent", 10, 11), ("random", 64, 40)):
+        out = D.sample_assemble_batched(g, nodes, times, qb, k, strat, seeds, l, E + 1, dt64=True)
+        for b in range(nb):
+            s, e = b * qb, min(nodes.numel(), (b + 1) * qb)
+            want = oracle_mod.sample_assemble(og, hn[s:e], ht[s:e], k, strat,
+                                              int(seeds[b].item()), l, E + 1)
+            got = {kk: v[s:e].cpu().numpy() for kk, v in out.items()}
+            check_rows(got, want, (strat, b))
