@@ -489,22 +489,30 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
       __syncwarp();
       int rank[KPT];
       uint32_t dig[KPT];
+      unsigned peers[KPT];
+      // lanes with the same 8-bit digit: intersect the 8 bit-plane ballots (fixed cost,
+      // unlike MATCH whose latency grows with the number of distinct values); all keys'
+      // ballots first, so the chains interleave, then the counter updates in key order
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         dig[k] = (key[k] >> shift) & 0xffu;
-        // lanes with the same 8-bit digit: intersect the 8 bit-plane ballots (fixed cost,
-        // unlike MATCH whose latency grows with the number of distinct values)
-        unsigned peers = kFull;
+        peers[k] = kFull;
+      }
 #pragma unroll
-        for (int bit = 0; bit < 8; ++bit) {
+      for (int bit = 0; bit < 8; ++bit) {
+#pragma unroll
+        for (int k = 0; k < KPT; ++k) {
           const unsigned m = __ballot_sync(kFull, (dig[k] >> bit) & 1u);
-          peers &= ((dig[k] >> bit) & 1u) ? m : ~m;
+          peers[k] &= ((dig[k] >> bit) & 1u) ? m : ~m;
         }
+      }
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
         const uint32_t b = wc[dig[k]];
         __syncwarp();
-        if (lane == __ffs(peers) - 1) wc[dig[k]] = b + __popc(peers);
+        if (lane == __ffs(peers[k]) - 1) wc[dig[k]] = b + __popc(peers[k]);
         __syncwarp();
-        rank[k] = static_cast<int>(b) + __popc(peers & lanemask_lt());
+        rank[k] = static_cast<int>(b) + __popc(peers[k] & lanemask_lt());
       }
       __syncthreads();
       // exclusive scan of the kTW x 256 counters in (digit, warp) order; thread t owns the 8

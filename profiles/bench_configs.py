@@ -6,7 +6,7 @@ the parity-test configs, measured for DESIGN.md; the headline line is bench.py's
 Each config: device-generated make_random_stream(E, V, 42), rev = 1 build (median of 5), then
 every forward_concat batch [src | dst | neg] of B events sampled + packed, one launch per
 batch as forward_concat calls it (seed 9 + batch), CUDA events around the whole sweep; and
-the same queries as one launch.  W and R are launch-latency-bound (a batch is ~1,800
+the same batches (same per-batch seeds) as one tgfx_sample_assemble_batched_device launch.  W and R are launch-latency-bound (a batch is ~1,800
 queries), so µs/batch is the figure of merit there."""
 import os
 import statistics
@@ -57,8 +57,10 @@ def run(name, c):
                 D.sample_assemble(g, nodes[s:e], times[s:e], k, c["strat"], 9 + i, l, E + 1,
                                   out=sub, trusted=True)
         big = D.alloc_rows(Q, l)
-        one = lambda: D.sample_assemble(g, nodes, times, k, c["strat"], 9, l, E + 1, out=big,  # noqa: E731
-                                        trusted=True)
+        seeds = torch.arange(9, 9 + len(batches), dtype=torch.int64, device="cuda")
+        # the same per-batch seeds (9 + b) as the per-batch loop, in one launch
+        one = lambda: D.sample_assemble_batched(g, nodes, times, qb, k, c["strat"], seeds, l,  # noqa: E731
+                                                E + 1, out=big, trusted=True)
     else:
         out = dict(h1=D.alloc_rows(qb, l), h2=D.alloc_rows(qb * k, l))
 
