@@ -46,6 +46,11 @@ extern "C" {
 #define TGFX_MASK_TGAT 1
 #define TGFX_MASK_SELF_LOOP 2
 
+/* element types of assemble_inputs operands */
+#define TGFX_F32 0
+#define TGFX_F64 1
+#define TGFX_BF16 2
+
 /* flags for *_device calls */
 #define TGFX_TRUSTED 1u   /* inputs known valid: no validation pass, no synchronisation */
 #define TGFX_INDEX64 2u   /* sample_assemble: node/edge index and valid_len are int64 */
@@ -209,6 +214,25 @@ int tgfx_assemble(int64_t q, int64_t kpad, const int64_t* counts, const int64_t*
 /* replaces tgf::build_mask (sequence.hpp:50, sequence.cpp:93-111): (q*l) x l doubles */
 int tgfx_build_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
                     int kind, double* mask);
+
+/* replaces tgf::assemble_inputs (proj/src/attention.cpp:414-451), the sequence tensors' first
+ * consumer: z [q*l, d] with, for j < valid_len[b], row b*l+j =
+ *   combine sum (concat = 0; d = d_v = d_e = d_t):
+ *     node_table[ni] + edge_table[ei] + cos(omega * dt + phi)
+ *   combine concat (concat = 1; d = d_v + d_e + d_t):
+ *     [node_table[ni] | edge_table[ei] | cos(omega * dt + phi)]
+ * and zero rows for padding.  Indices int32 (index64 = 0: the sampler's compact outputs) or
+ * int64; time_delta f32/f64 (dt_type); tables f32/f64 (table_type); omega, phi: f64 [d_t];
+ * z f32/f64/bf16 (z_type); the encoding is computed in f64 and rounded once.  An index outside
+ * its table: TGFX_EVALIDATION "sequence index outside embedding tables". */
+int tgfx_assemble_inputs_device(int64_t q, int64_t l, const void* d_node_index,
+                                const void* d_edge_index, const void* d_time_delta,
+                                const void* d_valid_len, int index64, int dt_type,
+                                const void* d_node_table, int64_t node_rows,
+                                const void* d_edge_table, int64_t edge_rows, int table_type,
+                                const double* d_omega, const double* d_phi, int64_t d_v,
+                                int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
+                                void* stream, unsigned flags);
 
 /* ---------------------------------------------------------------- synthetic inputs */
 /* bit-identical to tgf::make_random_stream (synthetic.hpp:17-18, synthetic.cpp:12-43);

@@ -10,6 +10,7 @@ float64, events as the 32-byte TemporalEvent record (event_stream.hpp:13-18).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -99,6 +100,8 @@ def ref():
         L.ref_build_sequence_batch.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P,
                                                _P, _P, _P, _P]
         L.ref_build_mask.argtypes = [_I64, _I64, _P, _P, C.c_int, _P]
+        L.ref_assemble_inputs.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P,
+                                          _I64, _I64, _I64, C.c_int, _P]
         _ref = L
     return _ref
 
@@ -423,3 +426,60 @@ def ref_build_mask(valid_len, target_row, l, kind):
     if rc:
         _ref_err(rc)
     return mask.reshape(q * l, l)
+
+
+# ---------------------------------------------------------------------- assemble_inputs
+def assemble_inputs(node_index, edge_index, time_delta, valid_len, node_table, edge_table,
+                    omega, phi, concat):
+    """Restatement of tgf::assemble_inputs (proj/src/attention.cpp:414-451) in numpy fp64:
+    z[b*l+j] for j < valid_len[b] = node_table[ni] + edge_table[ei] + cos(omega*dt + phi)
+    (sum) or [node_table[ni] | edge_table[ei] | cos(omega*dt + phi)] (concat); other rows 0.
+    Raises OracleError on an index outside its table (attention.cpp:427-431)."""
+    ni = np.asarray(node_index, np.int64)
+    ei = np.asarray(edge_index, np.int64)
+    dt = np.asarray(time_delta, np.float64)
+    q, l = ni.shape
+    vl = np.asarray(valid_len, np.int64)
+    live = np.arange(l)[None, :] < vl[:, None]
+    nt = np.asarray(node_table, np.float64)
+    et = np.asarray(edge_table, np.float64)
+    if np.any(live & ((ni < 0) | (ni >= len(nt)) | (ei < 0) | (ei >= len(et)))):
+        raise OracleError(1, "sequence index outside embedding tables")
+    om = np.asarray(omega, np.float64).reshape(-1)
+    ph = np.asarray(phi, np.float64).reshape(-1)
+    nrow = nt[np.where(live, ni, 0)]
+    erow = et[np.where(live, ei, 0)]
+    # omega * dt + phi is contracted to one fma by the reference's compiler (-march with FMA,
+    # GCC's default -ffp-contract=fast) and by nvcc: emulate the single rounding in extended
+    # precision.  Then glibc cos (math.cos, = std::cos); numpy's vectorised cos is less
+    # accurate for the large arguments omega * dt reaches.
+    ld = np.longdouble
+    arg = (om.astype(ld)[None, None, :] * dt.astype(ld)[:, :, None]
+           + ph.astype(ld)[None, None, :]).astype(np.float64)
+    enc = np.frompyfunc(math.cos, 1, 1)(arg).astype(np.float64)
+    z = (np.concatenate([nrow, erow, enc], axis=2) if concat else (nrow + erow) + enc)
+    z[~live] = 0.0
+    return z.reshape(q * l, -1)
+
+
+def ref_assemble_inputs(node_index, edge_index, time_delta, valid_len, node_table, edge_table,
+                        omega, phi, concat):
+    """The reference's own assemble_inputs (oracle/_ref, attention.cpp compiled in place)."""
+    ni = np.ascontiguousarray(node_index, np.int64)
+    ei = np.ascontiguousarray(edge_index, np.int64)
+    dt = np.ascontiguousarray(time_delta, np.float64)
+    vl = np.ascontiguousarray(valid_len, np.int64)
+    nt = np.ascontiguousarray(node_table, np.float64)
+    et = np.ascontiguousarray(edge_table, np.float64)
+    om = np.ascontiguousarray(omega, np.float64).reshape(-1)
+    ph = np.ascontiguousarray(phi, np.float64).reshape(-1)
+    q, l = ni.shape
+    d_v, d_e, d_t = nt.shape[1], et.shape[1], len(om)
+    d = d_v + d_e + d_t if concat else d_t
+    z = np.zeros((q * l, d), np.float64)
+    rc = ref().ref_assemble_inputs(q, l, _ptr(ni), _ptr(ei), _ptr(dt), _ptr(vl), _ptr(nt),
+                                   len(nt), _ptr(et), len(et), _ptr(om), _ptr(ph), d_v, d_e, d_t,
+                                   1 if concat else 0, _ptr(z))
+    if rc:
+        _ref_err(rc)
+    return z

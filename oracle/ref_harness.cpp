@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "tgformer/attention.hpp"
 #include "tgformer/event_stream.hpp"
 #include "tgformer/sampler.hpp"
 #include "tgformer/sequence.hpp"
@@ -231,6 +232,46 @@ int ref_build_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t
                       : (kind == 1 ? tgf::MaskKind::tgat : tgf::MaskKind::self_loop));
     for (int64_t r = 0; r < q * l; ++r)
       for (int64_t c = 0; c < l; ++c) mask[r * l + c] = m.at(r, c);
+    return 0;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
+// tgf::assemble_inputs (attention.cpp:414-451) on a SequenceBatch given as int64/f64 arrays
+// and tables given as row-major f64 arrays; concat = 0 sum, 1 concat.  z: [q*l, d].
+int ref_assemble_inputs(int64_t q, int64_t l, const int64_t* node_index, const int64_t* edge_index,
+                        const double* time_delta, const int64_t* valid_len,
+                        const double* node_table, int64_t node_rows, const double* edge_table,
+                        int64_t edge_rows, const double* omega, const double* phi, int64_t d_v,
+                        int64_t d_e, int64_t d_t, int concat, double* z) {
+  try {
+    tgf::ModelParams p;
+    p.config.d_v = d_v;
+    p.config.d_e = d_e;
+    p.config.d_t = d_t;
+    p.config.d_model = concat ? d_v + d_e + d_t : d_t;
+    p.config.combine = concat ? tgf::CombineMode::concat : tgf::CombineMode::sum;
+    p.node_table = tgf::Matrix(static_cast<size_t>(node_rows), static_cast<size_t>(d_v));
+    p.edge_table = tgf::Matrix(static_cast<size_t>(edge_rows), static_cast<size_t>(d_e));
+    p.omega = tgf::Matrix(1, static_cast<size_t>(d_t));
+    p.phi = tgf::Matrix(1, static_cast<size_t>(d_t));
+    std::memcpy(p.node_table.data(), node_table, sizeof(double) * node_rows * d_v);
+    std::memcpy(p.edge_table.data(), edge_table, sizeof(double) * edge_rows * d_e);
+    std::memcpy(p.omega.data(), omega, sizeof(double) * d_t);
+    std::memcpy(p.phi.data(), phi, sizeof(double) * d_t);
+    tgf::SequenceBatch b;
+    b.batch = q;
+    b.l = l;
+    b.node_index.assign(node_index, node_index + q * l);
+    b.edge_index.assign(edge_index, edge_index + q * l);
+    b.time_delta = tgf::Matrix(static_cast<size_t>(q), static_cast<size_t>(l));
+    std::memcpy(b.time_delta.data(), time_delta, sizeof(double) * q * l);
+    b.valid_len.assign(valid_len, valid_len + q);
+    b.target_row.resize(static_cast<size_t>(q));
+    for (int64_t i = 0; i < q; ++i) b.target_row[static_cast<size_t>(i)] = valid_len[i] - 1;
+    const tgf::Matrix out = tgf::assemble_inputs(p, b);
+    std::memcpy(z, out.data(), sizeof(double) * out.size());
     return 0;
   } catch (const std::exception& ex) {
     return fail(ex);

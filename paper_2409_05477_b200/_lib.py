@@ -89,6 +89,8 @@ SIGNATURES = {
                                     _P, _P, _P, _P, _U],
     "tgfx_sample_assemble_batched_device": [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I64, _I64,
                                             _P, _P, _P, _P, _P, _P, _U],
+    "tgfx_assemble_inputs_device": [_I64, _I64, _P, _P, _P, _P, _I, _I, _P, _I64, _P, _I64, _I,
+                                    _P, _P, _I64, _I64, _I64, _I, _P, _I, _P, _U],
     "tgfx_sample_two_hop_device": [_P, _P, _P, _I64, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P,
                                    _P, _P, _P, _P, _P, _P, _P, _P, _U],
     "tgfx_sample_two_hop": [_P, _P, _P, _I64, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P, _P,

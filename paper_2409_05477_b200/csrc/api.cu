@@ -542,6 +542,56 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
   });
 }
 
+int tgfx_assemble_inputs_device(int64_t q, int64_t l, const void* d_node_index,
+                                const void* d_edge_index, const void* d_time_delta,
+                                const void* d_valid_len, int index64, int dt_type,
+                                const void* d_node_table, int64_t node_rows,
+                                const void* d_edge_table, int64_t edge_rows, int table_type,
+                                const double* d_omega, const double* d_phi, int64_t d_v,
+                                int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
+                                void* stream, unsigned flags) {
+  return guarded([&] {
+    if (q < 0 || l < 0) throw Error(TGFX_EVALIDATION, "bad batch shape");
+    if (d_v < 0 || d_e < 0 || d_t < 0) throw Error(TGFX_EVALIDATION, "bad model dimensions");
+    if (!concat && !(d_v == d_t && d_e == d_t))  // ModelConfig::validate, attention.hpp:21-23
+      throw Error(TGFX_EVALIDATION, "combine sum requires d_v = d_e = d_t = d_model");
+    cudaStream_t s = as_stream(stream);
+    AssembleInputsArgs a;
+    a.q = q;
+    a.l = l;
+    a.node_index = d_node_index;
+    a.edge_index = d_edge_index;
+    a.time_delta = d_time_delta;
+    a.valid_len = d_valid_len;
+    a.index64 = index64;
+    a.dt_type = dt_type;
+    a.node_table = d_node_table;
+    a.edge_table = d_edge_table;
+    a.node_rows = node_rows;
+    a.edge_rows = edge_rows;
+    a.table_type = table_type;
+    a.omega = d_omega;
+    a.phi = d_phi;
+    a.d_v = d_v;
+    a.d_e = d_e;
+    a.d_t = d_t;
+    a.concat = concat;
+    a.z = d_z;
+    a.z_type = z_type;
+    if (flags & TGFX_TRUSTED) {
+      launch_assemble_inputs(a, nullptr, s);
+      return;
+    }
+    DBuf bad(sizeof(int), s);
+    TGFX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    launch_assemble_inputs(a, bad.as<int>(), s);
+    int h = 0;
+    TGFX_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    if (h) throw Error(TGFX_EVALIDATION, "sequence index outside embedding tables");
+  });
+}
+
 int tgfx_sample_assemble_batched_device(const tgfx_graph* g, const int64_t* d_nodes,
                                         const double* d_times, int64_t q, int64_t batch_q,
                                         int64_t k, int strategy, const uint64_t* d_seeds,

@@ -120,6 +120,27 @@ void launch_assemble_entries(int64_t q, int64_t kpad, const int64_t* counts, con
 void launch_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
                  int kind, double* mask, cudaStream_t s);
 
+// ------------------------------------------------------------------ assemble_inputs
+struct AssembleInputsArgs {
+  int64_t q = 0, l = 0;
+  const void* node_index = nullptr;  // int32 or int64 [q*l] (index64)
+  const void* edge_index = nullptr;
+  const void* time_delta = nullptr;  // f32 or f64 [q*l] (dt_type)
+  const void* valid_len = nullptr;   // int32 or int64 [q]
+  int index64 = 0, dt_type = 0;
+  const void* node_table = nullptr;  // [node_rows, d_v]
+  const void* edge_table = nullptr;  // [edge_rows, d_e]
+  int64_t node_rows = 0, edge_rows = 0;
+  int table_type = 0;
+  const double* omega = nullptr;  // [d_t]
+  const double* phi = nullptr;
+  int64_t d_v = 0, d_e = 0, d_t = 0;
+  int concat = 0;
+  void* z = nullptr;  // [q*l, d]
+  int z_type = 0;
+};
+void launch_assemble_inputs(const AssembleInputsArgs& a, int* bad, cudaStream_t s);
+
 // ------------------------------------------------------------------ synthetic
 void launch_random_stream(int64_t E, int64_t V, uint64_t seed, double zipf, tgfx_event* d_out,
                           cudaStream_t s);

@@ -152,3 +152,27 @@ def two_hop(g, roots, times, k1, k2, strategy, seed, l, self_edge_index, seed2=N
         TGFX_TRUSTED if trusted else 0))
     return out
 
+
+
+_DT = {torch.float32: 0, torch.float64: 1, torch.bfloat16: 2}
+
+
+def assemble_inputs(rows, node_table, edge_table, omega, phi, concat=False, z_dtype=torch.float32,
+                    trusted=False, stream=None):
+    """tgf::assemble_inputs (proj/src/attention.cpp:414-451) on the device: the sampler's rows
+    (dict with node_index, edge_index, valid_len and time_delta or time_delta64) ->
+    z [q*l, d] with d = d_t (sum) or d_v + d_e + d_t (concat)."""
+    ni, ei, vl = rows["node_index"], rows["edge_index"], rows["valid_len"]
+    dt = rows.get("time_delta64", rows.get("time_delta"))
+    q, l = ni.shape
+    d_v, d_e, d_t = node_table.shape[1], edge_table.shape[1], omega.numel()
+    d = d_v + d_e + d_t if concat else d_t
+    z = torch.empty((q * l, d), dtype=z_dtype, device="cuda")
+    om = omega.to(torch.float64).contiguous()
+    ph = phi.to(torch.float64).contiguous()
+    check(lib().tgfx_assemble_inputs_device(
+        q, l, _p(ni), _p(ei), _p(dt), _p(vl), 1 if ni.dtype == torch.int64 else 0, _DT[dt.dtype],
+        _p(node_table), node_table.shape[0], _p(edge_table), edge_table.shape[0],
+        _DT[node_table.dtype], _p(om), _p(ph), d_v, d_e, d_t, 1 if concat else 0, _p(z),
+        _DT[z_dtype], _stream(stream), TGFX_TRUSTED if trusted else 0))
+    return z

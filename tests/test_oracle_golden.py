@@ -112,3 +112,29 @@ def test_reference_unit_known_answers(oracle_mod):
     assert sb["node_index"][0].tolist() == [2, 3, 6, 8, 0, 0, 0, 0]
     assert sb["edge_index"][0].tolist() == [1, 2, 3, 100, 0, 0, 0, 0]
     assert sb["time_delta"][0, :4].tolist() == [8.0, 6.0, 3.0, 0.0]
+
+
+def test_assemble_inputs_restatement_vs_reference(oracle_mod):
+    """oracle.assemble_inputs (numpy restatement of attention.cpp:414-451) against the
+    reference's own assemble_inputs compiled from its sources (oracle/_ref)."""
+    import os
+    if not os.path.exists(oracle_mod.REF_SO):
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(11)
+    q, l = 64, 11
+    vl = rng.integers(1, l + 1, q)
+    ni = rng.integers(0, 40, (q, l))
+    ei = rng.integers(0, 90, (q, l))
+    dt = rng.uniform(0, 1e6, (q, l))
+    for concat, (dv, de, dtt) in ((False, (16, 16, 16)), (True, (8, 12, 20))):
+        nt = rng.normal(size=(40, dv))
+        et = rng.normal(size=(90, de))
+        om, ph = rng.normal(size=dtt), rng.normal(size=dtt)
+        a = oracle_mod.assemble_inputs(ni, ei, dt, vl, nt, et, om, ph, concat)
+        b = oracle_mod.ref_assemble_inputs(ni, ei, dt, vl, nt, et, om, ph, concat)
+        # one fma-rounded argument of size <= 1e6 away: 4 ulp(1e6)
+        assert np.abs(a - b).max() <= 4 * np.spacing(1e6 * 5)
+    bad = ni.copy()
+    bad[0, 0] = 40
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.assemble_inputs(bad, ei, dt, vl, nt, et, om, ph, True)
