@@ -147,3 +147,16 @@ def test_full_gdelt_size_properties():
         return ((a * 0x9E3779B1 + b * 0x85EBCA77) & 0xFFFFFFFF).sum()
     want = h(raw[:, 2], raw[:, 0]) + h(raw[:, 1], raw[:, 0])
     assert int(h(nb, ed)) == int(want)
+
+
+def test_permuted_ids_and_reverse_settings(T, oracle_mod):
+    """Hub nodes at arbitrary ids (a random relabelling of a Zipf stream), both reverse
+    settings, several sizes: the builder's hot-node selection must not depend on ids."""
+    rng = np.random.default_rng(8)
+    for E, V, seed in ((300_000, 5000, 3), (2_000_000, 16682, 4), (50_000, 65535, 5)):
+        ev = oracle_mod.make_random_stream(E, V, seed)
+        perm = rng.permutation(V)
+        ev["src"] = perm[ev["src"]]
+        ev["dst"] = perm[ev["dst"]]
+        for rev in (True, False):
+            assert_same(T.build_parallel(T.EventStream(ev, V), rev, 4), oracle_mod.build(ev, V, rev))
