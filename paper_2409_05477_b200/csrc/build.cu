@@ -11,18 +11,22 @@
 //   and the build is a stable counting sort by node:
 //
 //   K1 k_hist      one pass over the events (32 B each, 16-byte vector loads): endpoint
-//                  validation (first bad stream index), (t, eid)-order check, eid range,
-//                  and a per-chunk node histogram in shared memory (warp-aggregated with
-//                  __match_any_sync; the Zipf hub would serialise plain atomics).
-//   K2 k_colsum / k_indptr_scan / k_coloff
-//                  degrees, indptr (int64, V+1), and every chunk's starting cursor per node
-//                  (a C x V table, C = resident CTAs; 20 MB for GDELT-shaped V).
-//   K3 k_scatter   one more pass over the events: each CTA loads its V cursors into shared
-//                  memory and walks its chunk in 1024-entry tiles; a shared-memory hash of
-//                  the tile's nodes with per-warp byte counters gives every entry its stable
-//                  rank without sorting, then (nbr, eid, ts) are written to the SoA columns.
+//                  validation (first bad stream index), (t, eid)-order and NaN check, eid
+//                  range, and a per-chunk node histogram in shared memory.
+//   K2 k_colsum / k_coldflags / k_indptr_scan / k_coloff
+//                  degrees, indptr (int64, V+1), cold-node bitmask (nodes with few entries
+//                  per chunk) and dense cold-index bases, and every chunk's starting cursor
+//                  per node (a C x V table, C = resident CTAs; ~20 MB for GDELT-shaped V).
+//   K3 k_scatter_tile  one more pass: each CTA streams its chunk through shared memory in
+//                  bulk-copied tiles and ranks every tile by node with a block-wide stable
+//                  radix sort, so each node's tile entries are one run written at
+//                  cursor[u] + offset (details at the kernel).  Cold nodes' entries go out as
+//                  full 32-byte records, placed by K4 k_cold_u.
+//                  (k_scatter, the earlier ticketed-warp kernel, remains for node counts
+//                  whose cursors do not fit the tile kernel's shared memory.)
 //
-//   Algorithmic bytes: 32 B/event read twice (K1, K3) + 24 B/entry written + 8(V+1).
+//   Algorithmic bytes: 32 B/event read (K3; K1 reads them once more) + 24 B/entry written
+//   + 8(V+1).
 //
 // Unsorted streams take the general path: a stable LSD radix sort of the events by
 // (t, eid) (-0.0 keyed as +0.0, payload bits kept), then the fast path.  Streams whose
@@ -253,8 +257,6 @@ __global__ void k_coldflags(const int64_t* __restrict__ deg, int32_t V, int64_t 
 // leader of every node group reads and bumps that node's cursor (distinct nodes per round, so
 // one LDS/STS per group, rounds in order).  Emission order is preserved by construction.
 // Positions are written after the ticket is passed on.
-constexpr int kTkRoundsDefault = 8;  // rounds (32 entries each) per warp tile
-constexpr int kTkWarpsDefault = 8;
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -621,264 +623,6 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
   }
 }
 
-// K3 (default, variant 30): hashed tile ranking.  Like k_scatter_tile, each CTA streams its
-// chunk through shared memory in bulk-copied tiles of 256 entries (one 32-entry round per
-// warp, emission order = (warp, lane)), but the stable rank of an entry within the tile comes
-// without sorting:
-//   1. per warp, __match_any_sync groups the lanes by node: in-warp rank and count;
-//   2. each group leader inserts its node into a small shared-memory hash (the tile has at
-//      most 256 distinct nodes) and adds its count into the warp's 8-bit field of the slot's
-//      64-bit counter word (8 warps x 8 bits; no carries since a field holds at most 32);
-//   3. after one barrier, a leader reads the word: the fields of the earlier warps sum to
-//      the node's count in front of its warp, all fields to the node's tile total; its
-//      position base is cursor[u] + that prefix;
-//   4. after a second barrier, the first warp holding u advances cursor[u] by the total and
-//      clears the slot, while every lane stores its entry.
-// Three barriers per tile and no serial handover between warps.
-constexpr int kHW = 8;                 // warps per CTA (one 8-bit counter field each)
-constexpr int kHNE = kHW * 32;         // entries per tile
-constexpr int kHSlots = 512;           // hash slots (>= 2x the distinct nodes of a tile)
-constexpr int kHStages = 4;
-
-template <int R>
-size_t hash_scatter_smem_t(int64_t V) {
-  const int64_t vpad = (V + 31) & ~31LL;
-  return static_cast<size_t>(kHStages) * (kHNE / R) * 32  // event stages
-         + kHSlots * 8 + kHSlots * 4                       // hash counters + keys
-         + 64 * 8                                          // barriers
-         + vpad * 4 + (vpad / 32) * 4;                     // cursors + cold bits
-}
-
-__device__ __forceinline__ uint32_t byte_sum(unsigned long long x) {
-  x = (x & 0x00FF00FF00FF00FFull) + ((x >> 8) & 0x00FF00FF00FF00FFull);  // 4 x 16-bit sums
-  return static_cast<uint32_t>((x * 0x0001000100010001ull) >> 48);
-}
-
-template <int R>
-__global__ void __launch_bounds__(kHW * 32) k_scatter_hash(
-    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
-    ulonglong2* __restrict__ cold_img, int64_t* __restrict__ nbr_out,
-    int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
-  constexpr int TE = kHNE / R;  // events per tile
-  constexpr uint32_t kEmpty = 0xffffffffu;
-  extern __shared__ __align__(128) unsigned char sm[];
-  tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
-  unsigned long long* hcnt =
-      reinterpret_cast<unsigned long long*>(sm + static_cast<size_t>(kHStages) * TE * 32);
-  uint32_t* hkey = reinterpret_cast<uint32_t*>(hcnt + kHSlots);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(hkey + kHSlots);
-  const int vpad = (V + 31) & ~31;
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(bars + 64);
-  uint32_t* coldbits = cursor + vpad;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
-  const int64_t e1 = min(n, e0 + chunk_ev);
-  if (e0 >= e1) return;
-  const int64_t ntiles = ceil_div(e1 - e0, TE);
-  if (tid == 0) {
-    for (int s = 0; s < kHStages; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < kHStages && s < ntiles; ++s) {
-      const int64_t b = e0 + static_cast<int64_t>(s) * TE;
-      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
-      mbar_arrive_tx(&bars[s], bytes);
-      bulk_g2s(stage + s * TE, ev + b, bytes, &bars[s]);
-    }
-  }
-  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
-  for (int i = tid; i < V; i += kHW * 32) cursor[i] = orow[i];
-  for (int i = tid; i < vpad / 32; i += kHW * 32) coldbits[i] = coldbits_g[i];
-  for (int i = tid; i < kHSlots; i += kHW * 32) {
-    hkey[i] = kEmpty;
-    hcnt[i] = 0ull;
-  }
-  __syncthreads();
-
-  for (int64_t it = 0; it < ntiles; ++it) {
-    const int sidx = static_cast<int>(it % kHStages);
-    const uint32_t phase = static_cast<uint32_t>((it / kHStages) & 1);
-    const int64_t tb = e0 + it * TE;
-    const int ent = static_cast<int>(min(static_cast<int64_t>(TE), e1 - tb)) * R;
-    const tgfx_event* sev = stage + sidx * TE;
-    mbar_wait(&bars[sidx], phase);
-
-    const int j = warp * 32 + lane;  // entry of this lane, emission order
-    const bool ok = j < ent;
-    longlong2 a = make_longlong2(0, 0), b = make_longlong2(0, 0);
-    if (ok) {
-      const longlong2* e = reinterpret_cast<const longlong2*>(sev + (R == 2 ? (j >> 1) : j));
-      a = e[0];  // (eid, src)
-      b = e[1];  // (dst, t bits)
-    }
-    const bool side = R == 2 && (j & 1);
-    const uint32_t u = ok ? static_cast<uint32_t>(side ? b.x : a.y) : kEmpty;
-    const long long other = side ? a.y : b.x;
-    const unsigned peers = __match_any_sync(kFull, u);
-    const int leader = __ffs(peers) - 1;
-    const bool lead = ok && lane == leader;
-    int slot = 0;
-    if (lead) {
-      uint32_t h = (u * 2654435761u) >> 23;  // 9-bit multiplicative hash
-      while (true) {
-        const uint32_t old = atomicCAS(&hkey[h], kEmpty, u);
-        if (old == kEmpty || old == u) break;
-        h = (h + 1) & (kHSlots - 1);
-      }
-      slot = static_cast<int>(h);
-      atomicAdd(&hcnt[h], static_cast<unsigned long long>(__popc(peers)) << (8 * warp));
-    }
-    __syncthreads();
-    uint32_t base = 0, total = 0;
-    bool first = false;
-    if (lead) {
-      const unsigned long long w = hcnt[slot];
-      const unsigned long long below = warp ? (w & ((1ull << (8 * warp)) - 1)) : 0ull;
-      const uint32_t pre = byte_sum(below);
-      total = byte_sum(w);
-      first = pre == 0;
-      base = cursor[u] + pre;
-    }
-    const uint32_t pos = __shfl_sync(kFull, base, leader) + __popc(peers & lanemask_lt());
-    __syncthreads();  // every leader has read its cursor and counter word
-    if (lead && first) {
-      cursor[u] = base + total;
-      hkey[slot] = kEmpty;
-      hcnt[slot] = 0ull;
-    }
-    if (ok) {
-      if ((coldbits[u >> 5] >> (u & 31)) & 1u) {
-        // cold node: cursors run in dense cold-index space (k_coloff), record carries u
-        ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
-        rec[0] = make_ulonglong2(static_cast<unsigned long long>(other),
-                                 static_cast<unsigned long long>(a.x));
-        rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u));
-      } else {
-        nbr_out[pos] = other;
-        eid_out[pos] = a.x;
-        ts_out[pos] = __longlong_as_double(b.y);
-      }
-    }
-    __syncthreads();  // stage consumed, cursors advanced, hash cleared
-    if (tid == 0 && it + kHStages < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int64_t nb = e0 + (it + kHStages) * TE;
-      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - nb) * 32);
-      mbar_arrive_tx(&bars[sidx], bytes);
-      bulk_g2s(stage + sidx * TE, ev + nb, bytes, &bars[sidx]);
-    }
-  }
-}
-
-// K3'' (variant 20+): ticketed warps with register prefetch.  Tiles of 64 entries (two
-// 32-entry rounds) are taken by the CTA's warps round-robin; a warp groups its rounds with
-// __match_any_sync, waits for the previous tile's warp to hand over (named barrier, no
-// spinning), bumps the shared-memory cursors of its groups (two dependent LDS/STS per group,
-// the whole critical section), hands over, then stores.  Each warp keeps the events of its
-// next D tiles in registers, loaded D tiles ahead, so the handover chain never waits on HBM;
-// only the cursors live in shared memory, so several CTAs fit per SM.
-template <int R, int W, int D>
-__global__ void __launch_bounds__(W * 32) k_scatter_pf(
-    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
-    const int64_t* __restrict__ cdelta, ulonglong2* __restrict__ cold_img,
-    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  const int vpad = (V + 31) & ~31;
-  uint32_t* cursor = smem;
-  uint32_t* coldbits = cursor + vpad;
-  const int lane = threadIdx.x & 31;
-  const int warp = __shfl_sync(kFull, static_cast<int>(threadIdx.x >> 5), 0);
-  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
-  const int64_t e1 = min(n, e0 + chunk_ev);
-  if (e0 >= e1) return;
-  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
-  for (int i = threadIdx.x; i < V; i += W * 32) cursor[i] = orow[i];
-  for (int i = threadIdx.x; i < vpad / 32; i += W * 32) coldbits[i] = coldbits_g[i];
-  __syncthreads();
-
-  const int64_t E0 = e0 * R, E1 = e1 * R;
-  const int64_t ntiles = ceil_div(E1 - E0, 64);
-  auto load_tile = [&](int64_t t, Ev (&x)[2]) {
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int64_t j = E0 + t * 64 + r * 32 + lane;
-      x[r] = (t < ntiles && j < E1) ? load_event(ev, R == 2 ? (j >> 1) : j) : Ev{0, -1, -1, 0.0};
-    }
-  };
-  Ev buf[D][2];
-#pragma unroll
-  for (int d = 0; d < D; ++d) load_tile(warp + static_cast<int64_t>(d) * W, buf[d]);
-
-  for (int64_t i0 = 0;; i0 += D) {
-    bool stop = false;
-#pragma unroll
-    for (int s = 0; s < D; ++s) {
-      const int64_t t = warp + (i0 + s) * W;
-      if (t >= ntiles) {
-        stop = true;
-        break;
-      }
-      Ev x[2] = {buf[s][0], buf[s][1]};
-      load_tile(t + static_cast<int64_t>(D) * W, buf[s]);  // refill this slot D tiles ahead
-      uint32_t node[2], peers[2];
-      int64_t cd[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int64_t j = E0 + t * 64 + r * 32 + lane;
-        const bool side = R == 2 && (j & 1);
-        const bool ok = j < E1;
-        node[r] = ok ? static_cast<uint32_t>(side ? x[r].dst : x[r].src) : 0xffffffffu;
-        if (side) {  // keep the other endpoint in .dst
-          const int64_t a = x[r].src;
-          x[r].src = x[r].dst;
-          x[r].dst = a;
-        }
-        peers[r] = __match_any_sync(kFull, node[r]);
-        const bool cold = ok && ((coldbits[node[r] >> 5] >> (node[r] & 31)) & 1u);
-        cd[r] = cold ? __ldg(reinterpret_cast<const long long*>(cdelta) + node[r]) : INT64_MIN;
-      }
-      if (t > 0) named_bar_sync(1 + warp, 64);
-      uint32_t base[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const bool lead = node[r] != 0xffffffffu && lane == __ffs(peers[r]) - 1;
-        uint32_t b = 0;
-        if (lead) {
-          b = cursor[node[r]];
-          cursor[node[r]] = b + __popc(peers[r]);
-        }
-        base[r] = b;
-        __syncwarp();
-      }
-      if (t + 1 < ntiles) named_bar_arrive(1 + (warp + 1) % W, 64);
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t pos =
-            __shfl_sync(kFull, base[r], __ffs(peers[r]) - 1) + __popc(peers[r] & lanemask_lt());
-        if (node[r] == 0xffffffffu) continue;
-        if (cd[r] != INT64_MIN) {
-          const int64_t ci = static_cast<int64_t>(pos) + cd[r];
-          ulonglong2* rec = cold_img + 2 * ci;
-          rec[0] = make_ulonglong2(static_cast<unsigned long long>(x[r].dst),
-                                   static_cast<unsigned long long>(x[r].eid));
-          rec[1] = make_ulonglong2(static_cast<unsigned long long>(__double_as_longlong(x[r].t)),
-                                   static_cast<unsigned long long>(pos));
-        } else {
-          nbr_out[pos] = x[r].dst;
-          eid_out[pos] = x[r].eid;
-          ts_out[pos] = x[r].t;
-        }
-      }
-    }
-    if (stop) break;
-  }
-}
-
 // K4: place the cold entries.  Consecutive cold indices are consecutive positions of a cold
 // node's slice, so both the 32-byte record reads and the column writes are coalesced.
 __global__ void __launch_bounds__(256) k_cold(const ulonglong2* __restrict__ img, int64_t ncold,
@@ -1076,29 +820,10 @@ int scatter_variant() {
   return v;
 }
 
-template <int R>
-int hash_bps_t(int64_t V) {
-  const size_t smem = hash_scatter_smem_t<R>(V);
-  int bps = 0;
-  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_hash<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_hash<R>, kHW * 32, smem));
-  return std::max(bps, 1);
-}
-
-// hashed tile ranking (variant 30, default) when its shared memory fits
-bool use_hash_scatter(int64_t V) {
-  return scatter_variant() == 30 && V < 0xffffffffLL &&
-         hash_scatter_smem_t<1>(V) <= static_cast<size_t>(device_info().smem_optin);
-}
-
-// tile-sorted scatter shapes (threads, events per tile): variant 10 (default) 256 x 256,
-// 11: 512 x 512, 12: 128 x 128, 13: 256 x 512
-#define TGFX_TILE_SHAPES(X) \
-  X(10, 256, 256)           \
-  X(11, 512, 512)           \
-  X(12, 128, 128)           \
-  X(13, 256, 512)
+// tile-sorted scatter shape (threads, events per tile), TGFX_SCATTER_VARIANT=10 (default).
+// Measured on the GDELT shape: 256 x 256 (2 CTAs/SM) 12.3 ms build, 512 x 512 (1 CTA/SM)
+// 12.9 ms, 256 x 512 12.0 ms but 1 CTA/SM on larger V, 128 x 128 16.7 ms.
+#define TGFX_TILE_SHAPES(X) X(10, 256, 256)
 
 size_t tile_smem_for(int64_t V) {
   const int v = scatter_variant();
@@ -1123,37 +848,6 @@ int tile_bps_t(int64_t V) {
                                  static_cast<int>(smem)));
   TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_tile<R, TT, TE>, TT, smem));
   return std::max(bps, 1);
-}
-
-// prefetching ticketed scatter shapes (warps per CTA, prefetch depth in tiles)
-#define TGFX_PF_SHAPES(X) \
-  X(20, 8, 4)             \
-  X(21, 12, 3)            \
-  X(22, 8, 2)             \
-  X(23, 16, 2)
-
-bool use_pf_scatter(int64_t V) {
-  const int v = scatter_variant();
-  return v >= 20 && v <= 23 && V <= 65535;
-}
-
-template <int R, int W, int D>
-int pf_bps_t(int64_t V) {
-  const size_t smem = scatter_smem(V);
-  int bps = 0;
-  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_pf<R, W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_pf<R, W, D>, W * 32, smem));
-  return std::max(bps, 1);
-}
-
-int pf_bps(int R, int64_t V) {
-  const int v = scatter_variant();
-#define X(ID, W, D) \
-  if (v == ID) return R == 2 ? pf_bps_t<2, W, D>(V) : pf_bps_t<1, W, D>(V);
-  TGFX_PF_SHAPES(X)
-#undef X
-  return 1;
 }
 
 int tile_bps(int R, int64_t V) {
@@ -1191,9 +885,7 @@ int ticket_variant() {
 }
 
 int scatter_blocks_per_sm(int R, int64_t V) {
-  if (use_hash_scatter(V)) return R == 2 ? hash_bps_t<2>(V) : hash_bps_t<1>(V);
   if (use_tile_scatter(V)) return tile_bps(R, V);
-  if (use_pf_scatter(V)) return pf_bps(R, V);
   const int v = ticket_variant();
 #define X(ID, RO, W) \
   if (v == ID) return R == 2 ? scatter_bps<2, RO, W>(V) : scatter_bps<1, RO, W>(V);
@@ -1296,7 +988,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   after_launch("k_indptr_scan");
   if (V > 0) {
     k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr, coldbits, cdelta,
-                               use_tile_scatter(V) || use_hash_scatter(V) ? 1 : 0);
+                               use_tile_scatter(V) ? 1 : 0);
     after_launch("k_coloff");
   }
   int64_t ncold = 0;
@@ -1305,21 +997,6 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   ulonglong2* img = static_cast<ulonglong2*>(
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
-  if (use_hash_scatter(V)) {
-    if (g->reverse)
-      k_scatter_hash<2><<<C, kHW * 32, hash_scatter_smem_t<2>(V), s>>>(
-          d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->nbr, g->eid, g->ts);
-    else
-      k_scatter_hash<1><<<C, kHW * 32, hash_scatter_smem_t<1>(V), s>>>(
-          d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->nbr, g->eid, g->ts);
-    after_launch("k_scatter_hash");
-    if (ncold > 0) {
-      k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
-                                                                      g->eid, g->ts);
-      after_launch("k_cold_u");
-    }
-    return;
-  }
   if (use_tile_scatter(V)) {
     const size_t tsm = tile_smem_for(V);
     int bits = 1;
@@ -1344,27 +1021,6 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
       k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
                                                                       g->eid, g->ts);
       after_launch("k_cold_u");
-    }
-    return;
-  }
-  if (use_pf_scatter(V)) {
-    const size_t psm = scatter_smem(V);
-    const int v = scatter_variant();
-#define X(ID, W, D)                                                                              \
-  if (v == ID) {                                                                                 \
-    if (g->reverse)                                                                              \
-      k_scatter_pf<2, W, D><<<C, W * 32, psm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
-                                                   img, g->nbr, g->eid, g->ts);                  \
-    else                                                                                         \
-      k_scatter_pf<1, W, D><<<C, W * 32, psm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, cdelta, \
-                                                   img, g->nbr, g->eid, g->ts);                  \
-  }
-    TGFX_PF_SHAPES(X)
-#undef X
-    after_launch("k_scatter_pf");
-    if (ncold > 0) {
-      k_cold<<<resident_grid(k_cold, 256, 0, ncold), 256, 0, s>>>(img, ncold, g->nbr, g->eid, g->ts);
-      after_launch("k_cold");
     }
     return;
   }

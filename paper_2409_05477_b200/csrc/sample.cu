@@ -1,22 +1,21 @@
 // sample.cu -- temporal neighbor sampler fused with the sequence assembler (sm_100a).
 //
 // Replaces sample_batch / sample_recent / sample_random (proj/src/sampler.cpp:16-104) and
-// build_sequence_batch (proj/src/sequence.cpp:55-86) with one kernel per strategy:
+// build_sequence_batch (proj/src/sequence.cpp:55-86):
 //
-//   * 32 queries per warp.  Each lane runs the strict-before-t search of its own query
-//     (lower_bound over the node's ts slice, sampler.cpp:16-20: #entries with ts < t;
-//     NaN t -> 0).  Thread-per-query searches keep one sector per probe and 32
-//     independent searches in flight per warp (a warp-cooperative k-ary probe would touch
-//     32 sectors per step).
-//   * recent-k: the kept window of the row is contiguous ([lo+m-kb, lo+m), kb =
-//     min(k, m, l-1)), so the warp assembles its 32 rows "slot-parallel": lane s handles
-//     output slot s of the warp's [32 x l] block, so gathers are near-contiguous and every
-//     output store is a fully coalesced run of 32*l elements.
+//   * the strict-before-t prefix m(u, t) = #{ts < t} of a slice (lower_bound,
+//     sampler.cpp:16-20; NaN t -> 0) is found by search_lines: interpolated probes that each
+//     read and resolve a whole 8-entry ts line, bracketed by the node directory record
+//     (slice bounds + first/last ts).  Any search that keeps ts[lo-1] < t <= ts[hi] returns
+//     the unique lower_bound on a sorted, NaN-free slice; graphs not known to be sorted and
+//     NaN-free replay std::lower_bound's own bisection (search_interleaved) instead.
+//   * recent-k (k_recent_line): one query per lane for the search, then the warp assembles its
+//     32 rows "slot-parallel": lane s handles output slot s of the warp's [32 x l] block, so
+//     window gathers are near-contiguous and every store is a coalesced run.
 //   * uniform-k: Floyd's algorithm with the reference's counter RNG (rng.hpp:23-38,
-//     sampler.cpp:66-80), warp-cooperative per query: lane d computes draw d by O(1)
-//     skip-ahead (x_d = mix64(s0 + d*gamma)), collisions are resolved sequentially in d with
-//     one __any_sync per draw, offsets are ranked (distinct) by shuffles, and each lane
-//     writes its entry straight to its sorted column.
+//     sampler.cpp:66-80): draw d by O(1) skip-ahead (x_d = mix64(s0 + d*gamma)), collisions
+//     resolved in order d with one ballot each, offsets ranked by shuffles -- by 8-lane groups
+//     (k_random_g, k <= 32, four queries per warp at a time) or by the whole warp (k_random).
 //   * suffix infilling epilogue: ids + 1, self-edge token at column kb, zero padding,
 //     dt = t_q - ts in fp64 then rounded to fp32 (and/or kept as fp64).
 #include <algorithm>
@@ -134,95 +133,6 @@ __device__ __forceinline__ void search_interleaved(const double* __restrict__ ts
   for (int j = 0; j < QL; ++j) m[j] = base[j] - lo[j];
 }
 
-// Safeguarded interpolation search, QL queries per lane interleaved.  Same result as
-// std::lower_bound on a sorted, NaN-free slice (any search that keeps the bracket
-// ts[lo-1] < t <= ts[hi] converges to the unique answer); the probe position is interpolated
-// from the bracket's values, and a step that fails to halve the bracket is followed by a
-// bisection step, so the probe count is at most ~2 log2(n) and ~log2 log2(n) on slices whose
-// timestamps grow roughly linearly (event streams).  Every probe is a dependent round trip to
-// L2/HBM, so fewer probes is the whole point: GDELT-shaped hub slices (78 M entries) take
-// ~27 bisection probes.
-template <int QL>
-__device__ __forceinline__ void search_interp(const double* __restrict__ ts,
-                                              const int64_t (&base)[QL], const int64_t (&n)[QL],
-                                              const double (&t)[QL], int64_t (&m)[QL]) {
-  int64_t lo[QL], hi[QL];
-  double vlo[QL], vhi[QL];
-  bool bis[QL];
-  // bracket values: first and last entry of every slice (independent loads)
-  double v0[QL], v1[QL];
-#pragma unroll
-  for (int j = 0; j < QL; ++j) {
-    v0[j] = n[j] > 0 ? __ldg(ts + base[j]) : 0.0;
-    v1[j] = n[j] > 1 ? __ldg(ts + base[j] + n[j] - 1) : v0[j];
-  }
-#pragma unroll
-  for (int j = 0; j < QL; ++j) {
-    bis[j] = false;
-    vlo[j] = v0[j];
-    vhi[j] = v1[j];
-    if (n[j] <= 0 || !(v0[j] < t[j])) {  // empty slice, t <= first, or NaN t -> 0
-      lo[j] = hi[j] = 0;
-    } else if (v1[j] < t[j]) {  // whole slice before t
-      lo[j] = hi[j] = n[j];
-    } else {  // ts[0] < t <= ts[n-1]: answer in [1, n-1]
-      lo[j] = 1;
-      hi[j] = n[j] - 1;
-    }
-  }
-  while (true) {
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < QL; ++j) any |= lo[j] < hi[j];
-    if (!any) break;
-    int64_t p[QL];
-    double v[QL];
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      const int64_t len = hi[j] - lo[j];
-      int64_t q = lo[j] + (len >> 1);
-      if (!bis[j]) {
-        // predicted answer under linear growth between ts[lo-1] = vlo and ts[hi] = vhi
-        // (fp32 fast divide: the probe position only steers the search, never its result)
-        const float f = __fdividef(static_cast<float>(t[j] - vlo[j]),
-                                   static_cast<float>(vhi[j] - vlo[j]));  // (0, 1] if finite
-        if (f >= 0.0f && f <= 1.0f)
-          q = lo[j] - 1 + static_cast<int64_t>(static_cast<double>(f) *
-                                               static_cast<double>(len + 1));
-        q = max(lo[j], min(q, hi[j] - 1));
-      }
-      p[j] = q;
-      v[j] = len > 0 ? __ldg(ts + base[j] + q) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      const int64_t len = hi[j] - lo[j];
-      if (len > 0) {
-        if (v[j] < t[j]) {
-          lo[j] = p[j] + 1;
-          vlo[j] = v[j];
-        } else {
-          hi[j] = p[j];
-          vhi[j] = v[j];
-        }
-        bis[j] = !bis[j] && 2 * (hi[j] - lo[j]) > len;
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < QL; ++j) m[j] = lo[j];
-}
-
-template <int QL>
-__device__ __forceinline__ void search(bool exact, const double* __restrict__ ts,
-                                       const int64_t (&lo)[QL], int64_t (&n)[QL],
-                                       const double (&t)[QL], int64_t (&m)[QL]) {
-  if (exact)
-    search_interleaved<QL>(ts, lo, n, t, m);
-  else
-    search_interp<QL>(ts, lo, n, t, m);
-}
-
 // floor(s / w) for s < 2^16 via a 32-bit multiply-high (magic = ceil(2^32 / w)), else divide
 __device__ __forceinline__ int div_slot(int s, int w, uint32_t magic) {
   return magic ? static_cast<int>(__umulhi(static_cast<uint32_t>(s), magic)) : s / w;
@@ -233,7 +143,7 @@ template <bool ASSEMBLE, bool IDX64, int QL, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent(
     const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint32_t magic, int exact, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
   constexpr int GQ = 32 * QL;  // queries per warp group
   __shared__ int64_t s_start[kWarps][GQ];
   __shared__ int64_t s_u[kWarps][GQ];
@@ -259,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
       lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
       n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
     }
-    search<QL>(exact != 0, ts, lo, n, t, m);
+    search_interleaved<QL>(ts, lo, n, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
       const int64_t q = g * GQ + j * 32 + lane;
@@ -318,52 +228,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
       }
     }
     __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ recent-k, split form
-// Phase A (k_recent_search): QL interleaved searches per lane, writes the kept window of each
-// query packed as (start << 8 | kb) -- kb = -1 (0xff) marks an absent hop-2 slot.
-// Phase B (k_recent_gather): streaming gather + suffix-infill packing over the packed windows;
-// no search latency on its path, so every warp keeps its loads in flight.
-template <bool ASSEMBLE, int QL>
-__global__ void __launch_bounds__(kThreads) k_recent_search(
-    const int64_t* __restrict__ indptr, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int exact, uint64_t* __restrict__ win) {
-  constexpr int GQ = 32 * QL;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t ngroups = ceil_div(Q, GQ);
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
-       g += static_cast<int64_t>(gridDim.x) * kWarps) {
-    int64_t u[QL], lo[QL], n[QL], m[QL];
-    double t[QL];
-    bool pres[QL];
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      const int64_t q = g * GQ + j * 32 + lane;
-      u[j] = 0;
-      t[j] = 0.0;
-      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      lo[j] = pres[j] ? ldg_i64(indptr + u[j]) : 0;
-      n[j] = pres[j] ? ldg_i64(indptr + u[j] + 1) - lo[j] : 0;
-    }
-    search<QL>(exact != 0, ts, lo, n, t, m);
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      const int64_t q = g * GQ + j * 32 + lane;
-      if (q < Q) {
-        uint64_t w = 0xffull;  // absent
-        if (pres[j]) {
-          const int64_t take = min(k, m[j]);
-          const int kb = static_cast<int>(ASSEMBLE ? min(take, static_cast<int64_t>(l - 1)) : take);
-          w = (static_cast<uint64_t>(lo[j] + m[j] - kb) << 8) | static_cast<uint64_t>(kb);
-        }
-        win[q] = w;
-      }
-    }
   }
 }
 
@@ -468,7 +332,7 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
   for (int j = 0; j < QL; ++j) m[j] = lo[j];
 }
 
-template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, int EXPERIMENT = 0, bool PF = false>
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
@@ -480,74 +344,34 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = ASSEMBLE ? l : static_cast<int>(k);
   const int64_t ngroups = ceil_div(Q, GQ);
-  const int64_t gstride = static_cast<int64_t>(gridDim.x) * kWarps;
-  // software pipeline across the warp's groups (grids smaller than one group per warp): the
-  // next group's queries are fetched before this group's search, and their directory
-  // records before this group's gather, so two of the dependent round trips overlap work
-  int64_t nu[QL];
-  double nt[QL];
-  bool npres[QL];
-  NodeDir nd[QL];
-  auto fetch_group = [&](int64_t gg) {
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      const int64_t q = gg * GQ + j * 32 + lane;
-      nu[j] = 0;
-      nt[j] = 0.0;
-      npres[j] = gg < ngroups && q < Q && fetch_query(in, q, nu[j], nt[j]);
-    }
-  };
-  auto fetch_dir = [&]() {
-#pragma unroll
-    for (int j = 0; j < QL; ++j) {
-      if (npres[j]) {
-        const longlong2* p = reinterpret_cast<const longlong2*>(dir + nu[j]);
-        const longlong2 x = __ldg(p), y = __ldg(p + 1);
-        nd[j].start = x.x;
-        nd[j].end = x.y;
-        nd[j].t_first = __longlong_as_double(y.x);
-        nd[j].t_last = __longlong_as_double(y.y);
-      } else {
-        nd[j].start = nd[j].end = 0;
-        nd[j].t_first = nd[j].t_last = 0.0;
-      }
-    }
-  };
-  int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
-  fetch_group(g);
-  fetch_dir();
-  for (; g < ngroups; g += gstride) {
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
+       g += static_cast<int64_t>(gridDim.x) * kWarps) {
     int64_t u[QL], m[QL];
     double t[QL];
     bool pres[QL];
     NodeDir d[QL];
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
-      u[j] = nu[j];
-      t[j] = nt[j];
-      pres[j] = npres[j];
-      d[j] = nd[j];
+      const int64_t q = g * GQ + j * 32 + lane;
+      u[j] = 0;
+      t[j] = 0.0;
+      pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
     }
-    if (PF) fetch_group(g + gstride);
-    if (EXPERIMENT == 2) {  // timing experiment: no search (window = the slice's tail)
 #pragma unroll
-      for (int j = 0; j < QL; ++j) m[j] = d[j].end - d[j].start;
-    } else {
-      search_lines<W, QL>(ts, d, pres, t, m);
-    }
-    if (PF) fetch_dir();
-    if (EXPERIMENT == 1) {  // timing experiment: search only
-#pragma unroll
-      for (int j = 0; j < QL; ++j) {
-        const int64_t q = g * GQ + j * 32 + lane;
-        if (q < Q) write_vlen<IDX64>(o, q, m[j]);
+    for (int j = 0; j < QL; ++j) {  // one 32-byte directory record: bounds + bracket
+      if (pres[j]) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[j]);
+        const longlong2 x = __ldg(p), y = __ldg(p + 1);
+        d[j].start = x.x;
+        d[j].end = x.y;
+        d[j].t_first = __longlong_as_double(y.x);
+        d[j].t_last = __longlong_as_double(y.y);
+      } else {
+        d[j].start = d[j].end = 0;
+        d[j].t_first = d[j].t_last = 0.0;
       }
-      if (!PF) {
-        fetch_group(g + gstride);
-        fetch_dir();
-      }
-      continue;
     }
+    search_lines<W, QL>(ts, d, pres, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
       const int64_t q = g * GQ + j * 32 + lane;
@@ -615,229 +439,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       }
     }
     __syncwarp();
-    if (!PF) {
-      fetch_group(g + gstride);
-      fetch_dir();
-    }
-  }
-}
-
-// Phase A, work-queue form (experimental variant 20).  The search's probe count varies a lot between
-// queries (empty slice: 0; GDELT hub: ~8 interpolation probes, up to ~25), and a warp that
-// runs 32 searches in lockstep waits for its slowest lane.  Here every lane is a small state
-// machine that takes the next query of its warp's block as soon as its current one finishes,
-// so a warp's time is the SUM of its lanes' probe chains / 32, not their max.  Each loop
-// iteration every lane issues the (at most two, independent) loads of its current state, then
-// consumes them:
-//   FETCH   node, time of query q            (hop-2 mode: HOPCHK first: is slot j present?)
-//   IPTR    indptr[u], indptr[u+1]
-//   BRACKET ts[first], ts[last] of the slice  (skipped in exact mode)
-//   SEARCH  one probe (interpolated, or bisection after a step that did not halve the range;
-//           exact mode: std::lower_bound's own midpoints)
-// and on convergence writes the packed window (start << 8 | kb) of query q.
-enum : int { kNeed = 0, kHopChk, kFetch, kIptr, kBracket, kSearch };
-
-template <bool ASSEMBLE>
-__global__ void __launch_bounds__(kThreads) k_recent_search_q(
-    const int64_t* __restrict__ indptr, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int exact, uint64_t* __restrict__ win) {
-  constexpr int64_t kBlk = 256;  // queries per warp block
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
-  const int64_t nblk = ceil_div(Q, kBlk);
-  int64_t blk = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
-  int64_t cur = blk * kBlk, end = min(Q, cur + kBlk);
-  const int64_t cap = ASSEMBLE ? min(k, static_cast<int64_t>(l - 1)) : k;
-  int st = kNeed;
-  int64_t q = 0, base = 0, lo = 0, hi = 0;
-  double t = 0.0, vlo = 0.0, vhi = 0.0;
-  bool bis = exact != 0;
-  while (true) {
-    // hand out queries of the warp's block to idle lanes (warp-uniform bookkeeping)
-    unsigned need = __ballot_sync(kFull, st == kNeed);
-    while (need && blk < nblk) {
-      const int64_t take = min(static_cast<int64_t>(__popc(need)), end - cur);
-      const int r = __popc(need & lanemask_lt());
-      if (st == kNeed && r < take) {
-        q = cur + r;
-        st = in.hop_counts ? kHopChk : kFetch;
-      }
-      cur += take;
-      if (cur >= end) {
-        blk += nwarps;
-        cur = blk * kBlk;
-        end = min(Q, cur + kBlk);
-      }
-      need = __ballot_sync(kFull, st == kNeed);
-    }
-    if (need == kFull) break;  // every lane idle and no blocks left
-    // load phase: one or two independent 8-byte loads per lane
-    const unsigned long long* pa = nullptr;
-    const unsigned long long* pb = nullptr;
-    int64_t p = 0;
-    if (st == kHopChk) {
-      pa = reinterpret_cast<const unsigned long long*>(in.hop_counts + q / in.hop_k1);
-    } else if (st == kFetch) {
-      pa = reinterpret_cast<const unsigned long long*>(in.nodes + q);
-      pb = reinterpret_cast<const unsigned long long*>(in.times + q);
-    } else if (st == kIptr) {
-      pa = reinterpret_cast<const unsigned long long*>(indptr + base);  // base holds u here
-      pb = pa + 1;
-    } else if (st == kBracket) {
-      pa = reinterpret_cast<const unsigned long long*>(ts + base);
-      pb = reinterpret_cast<const unsigned long long*>(ts + base + hi);  // hi holds n-1
-    } else if (st == kSearch) {
-      const int64_t len = hi - lo;
-      p = lo + (len >> 1);
-      if (!bis) {
-        // predicted answer under linear growth between ts[lo-1] = vlo and ts[hi] = vhi
-        const float f = __fdividef(static_cast<float>(t - vlo), static_cast<float>(vhi - vlo));
-        if (f >= 0.0f && f <= 1.0f)
-          p = lo - 1 + static_cast<int64_t>(static_cast<double>(f) * static_cast<double>(len + 1));
-        p = max(lo, min(p, hi - 1));
-      }
-      pa = reinterpret_cast<const unsigned long long*>(ts + base + p);
-    }
-    const unsigned long long va = pa ? __ldg(pa) : 0ull;
-    const unsigned long long vb = pb ? __ldg(pb) : 0ull;
-    // consume phase
-    bool done = false;
-    if (st == kHopChk) {
-      const int64_t j = q - (q / in.hop_k1) * in.hop_k1;
-      if (j >= static_cast<int64_t>(va)) {  // absent hop-2 slot
-        win[q] = 0xffull;
-        st = kNeed;
-      } else {
-        st = kFetch;
-      }
-    } else if (st == kFetch) {
-      base = static_cast<int64_t>(va);
-      t = __longlong_as_double(static_cast<long long>(vb));
-      st = kIptr;
-    } else if (st == kIptr) {
-      base = static_cast<int64_t>(va);
-      const int64_t n = static_cast<int64_t>(vb) - base;
-      lo = 0;
-      if (n <= 0) {
-        hi = 0;
-        done = true;
-      } else if (exact) {
-        hi = n;
-        st = kSearch;
-      } else {
-        hi = n - 1;
-        st = kBracket;
-      }
-    } else if (st == kBracket) {
-      const double v0 = __longlong_as_double(static_cast<long long>(va));
-      const double v1 = __longlong_as_double(static_cast<long long>(vb));
-      const int64_t n = hi + 1;
-      vlo = v0;
-      vhi = v1;
-      bis = false;
-      if (!(v0 < t)) {  // t <= first entry, or NaN t
-        lo = hi = 0;
-      } else if (v1 < t) {  // whole slice before t
-        lo = hi = n;
-      } else {  // ts[0] < t <= ts[n-1]
-        lo = 1;
-        hi = n - 1;
-      }
-      done = lo >= hi;
-      st = kSearch;
-    } else if (st == kSearch) {
-      const int64_t len = hi - lo;
-      const double v = __longlong_as_double(static_cast<long long>(va));
-      if (v < t) {
-        lo = p + 1;
-        vlo = v;
-      } else {
-        hi = p;
-        vhi = v;
-      }
-      if (!exact) bis = !bis && 2 * (hi - lo) > len;
-      done = lo >= hi;
-    }
-    if (done) {
-      const int kb = static_cast<int>(min(cap, lo));
-      win[q] = (static_cast<uint64_t>(base + lo - kb) << 8) | static_cast<uint64_t>(kb);
-      st = kNeed;
-    }
-  }
-}
-
-template <bool ASSEMBLE, bool IDX64>
-__global__ void __launch_bounds__(kThreads) k_recent_gather(
-    const int64_t* __restrict__ nbr, const int64_t* __restrict__ eid,
-    const double* __restrict__ ts, QueryIn in, int64_t Q, int64_t k, int l, int64_t self_idx,
-    uint32_t magic, const uint64_t* __restrict__ win, Outs o) {
-  constexpr int GQ = 32;  // queries per warp group
-  __shared__ int64_t s_start[kWarps][GQ];
-  __shared__ int64_t s_u[kWarps][GQ];
-  __shared__ double s_t[kWarps][GQ];
-  __shared__ int s_kb[kWarps][GQ];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int width = ASSEMBLE ? l : static_cast<int>(k);
-  const int64_t ngroups = ceil_div(Q, GQ);
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
-       g += static_cast<int64_t>(gridDim.x) * kWarps) {
-    const int64_t q = g * GQ + lane;
-    if (q < Q) {
-      const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(win) + q);
-      const int kb = (w & 0xff) == 0xff ? -1 : static_cast<int>(w & 0xff);
-      s_kb[warp][lane] = kb;
-      s_start[warp][lane] = static_cast<int64_t>(w >> 8);
-      s_u[warp][lane] = kb >= 0 || ASSEMBLE ? (kb >= 0 ? ldg_i64(in.nodes + q) : 0) : 0;
-      s_t[warp][lane] = kb >= 0 ? ldg_f64(in.times + q) : 0.0;
-      if (ASSEMBLE)
-        write_vlen<IDX64>(o, q, kb + 1);
-      else
-        o.counts[q] = max(kb, 0);
-    }
-    __syncwarp();
-    const int nq = static_cast<int>(min(static_cast<int64_t>(GQ), Q - g * GQ));
-    const int total = nq * width;
-    const int64_t obase = g * GQ * width;
-#pragma unroll 4
-    for (int sl = lane; sl < total; sl += 32) {
-      const int qi = div_slot(sl, width, magic);
-      const int j = sl - qi * width;
-      const int kbq = s_kb[warp][qi];
-      if (ASSEMBLE) {
-        int64_t ni = 0, ei = 0;
-        double dt = 0.0;
-        if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
-          ni = ldg_i64(nbr + p) + 1;
-          ei = ldg_i64(eid + p) + 1;
-          dt = s_t[warp][qi] - ldg_f64(ts + p);
-        } else if (j == kbq) {
-          ni = s_u[warp][qi] + 1;
-          ei = self_idx;
-        }
-        write_slot<IDX64>(o, obase + sl, ni, ei, dt);
-      } else {
-        int64_t a = 0, b = 0;
-        double c = 0.0;
-        if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
-          a = ldg_i64(nbr + p);
-          b = ldg_i64(eid + p);
-          c = ldg_f64(ts + p);
-        }
-        o.e_nbr[obase + sl] = a;
-        o.e_eid[obase + sl] = b;
-        o.e_ts[obase + sl] = c;
-      }
-    }
-    __syncwarp();
   }
 }
 
 // ------------------------------------------------------------------ uniform-k (Floyd)
 template <int P, bool ASSEMBLE, bool IDX64>
 __global__ void __launch_bounds__(kThreads) k_random(
-    const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ indptr, const NodeDir* __restrict__ dir,
+    const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, int exact,
     Outs o) {
@@ -855,10 +464,28 @@ __global__ void __launch_bounds__(kThreads) k_random(
       present = true;
       lo = ldg_i64(indptr + u);
     }
-    {
+    if (exact) {  // slices not known sorted / NaN-free: std::lower_bound's own bisection
       int64_t lo1[1] = {lo}, n1[1] = {present ? ldg_i64(indptr + u + 1) - lo : 0}, m1[1];
       const double t1[1] = {t};
-      search<1>(exact != 0, ts, lo1, n1, t1, m1);
+      search_interleaved<1>(ts, lo1, n1, t1, m1);
+      m = m1[0];
+    } else {
+      NodeDir d[1];
+      const bool pres[1] = {present};
+      const double t1[1] = {t};
+      int64_t m1[1];
+      if (present) {
+        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u);
+        const longlong2 x = __ldg(p), y = __ldg(p + 1);
+        d[0].start = x.x;
+        d[0].end = x.y;
+        d[0].t_first = __longlong_as_double(y.x);
+        d[0].t_last = __longlong_as_double(y.y);
+      } else {
+        d[0].start = d[0].end = 0;
+        d[0].t_first = d[0].t_last = 0.0;
+      }
+      search_lines<8, 1>(ts, d, pres, t1, m1);
       m = m1[0];
     }
     const int nq = static_cast<int>(min((int64_t)32, Q - g * 32));
@@ -1036,29 +663,6 @@ __global__ void k_mask(int64_t q, int64_t l, const int64_t* __restrict__ valid_l
       hi = kind == TGFX_MASK_SELF_LOOP ? kq + 1 : kq;
     mask[i] = col < hi ? 0.0 : __longlong_as_double(0xfff0000000000000LL);  // -inf
   }
-}
-
-int recent_variant() {
-  static int v = [] {
-    const char* e = getenv("TGFX_RECENT_VARIANT");
-    return e ? atoi(e) : 30;
-  }();
-  return v;
-}
-
-
-// Several waves of blocks measured faster than a persistent (resident-only) grid for the
-// sampler: per-block work varies with the queried slices (hub searches), and small blocks
-// balance better.  TGFX_RECENT_WAVES overrides the blocks-per-SM cap (default: none).
-template <int QL, int MINB>
-int recent_grid(int64_t q, bool, bool) {
-  static const int64_t per_sm = [] {
-    const char* e = getenv("TGFX_RECENT_WAVES");
-    return e ? atoll(e) : (1LL << 30);  // uncapped: one 256-query group per warp
-  }();
-  const int64_t groups = ceil_div(std::max<int64_t>(q, 1), 32 * QL);
-  const int64_t blocks = ceil_div(groups, kWarps);
-  return static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(device_info().sms) * per_sm));
 }
 
 int grid_groups(int64_t Q) {
@@ -1261,7 +865,7 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
   const int l = static_cast<int>(a.l);
 #define TGFX_RANDOM_CASE(PP)                                                                 \
   case PP:                                                                                   \
-    k_random<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in, a.q, \
+    k_random<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->indptr, g->dir, g->nbr, g->eid, g->ts, in, a.q, \
                                                      a.k, l, a.self_edge_index, a.seed,      \
                                                      a.stream_base, g->search_exact, o);    \
     break;
@@ -1306,124 +910,37 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     const int width = assemble ? l : static_cast<int>(a.k);
     const uint32_t magic =
         (width < 512) ? static_cast<uint32_t>(((1ull << 32) + width - 1) / width) : 0u;
-    const int variant = recent_variant();
-#define TGFX_RECENT_LAUNCH(QL, MINB)                                                           \
-  {                                                                                            \
-    const int rgrid = recent_grid<QL, MINB>(a.q, assemble, a.index64);                         \
-    if (assemble && a.index64)                                                                 \
-      k_recent<true, true, QL, MINB><<<rgrid, kThreads, 0, s>>>(                               \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic,          \
-          g->search_exact, o);                                                                 \
-    else if (assemble)                                                                         \
-      k_recent<true, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                              \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic,          \
-          g->search_exact, o);                                                                 \
-    else                                                                                       \
-      k_recent<false, false, QL, MINB><<<rgrid, kThreads, 0, s>>>(                             \
-          g->indptr, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, g->search_exact, o);    \
-  }
-    if (variant >= 30 && !g->search_exact) {  // line-probe kernel (default)
-#define TGFX_LINE_EXP(X)                                                                        \
-  {                                                                                             \
-    const int gl = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX)); \
-    k_recent_line<true, false, 8, 1, 4, X><<<gl, kThreads, 0, s>>>(                             \
-        g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);           \
-  }
-#define TGFX_LINE_PF(WAVES)                                                                     \
-  {                                                                                             \
-    const int gl = static_cast<int>(std::min<int64_t>(                                          \
-        ceil_div(ceil_div(a.q, 32), kWarps), static_cast<int64_t>(device_info().sms) * 4 * WAVES)); \
-    k_recent_line<true, false, 8, 1, 4, 0, true><<<gl, kThreads, 0, s>>>(                       \
-        g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);           \
-  }
-#define TGFX_LINE_LAUNCH(W, QL, MINB)                                                           \
-  {                                                                                             \
-    const int gl = static_cast<int>(                                                            \
-        std::min<int64_t>(ceil_div(ceil_div(a.q, 32 * QL), kWarps), INT32_MAX));                \
-    if (assemble && a.index64)                                                                  \
-      k_recent_line<true, true, W, QL, MINB><<<gl, kThreads, 0, s>>>(                                 \
-          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
-    else if (assemble)                                                                          \
-      k_recent_line<true, false, W, QL, MINB><<<gl, kThreads, 0, s>>>(                                \
-          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);         \
-    else                                                                                        \
-      k_recent_line<false, false, W, QL, MINB><<<gl, kThreads, 0, s>>>(                               \
-          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);                         \
-  }
-      switch (variant) {
-        case 31: TGFX_LINE_LAUNCH(16, 1, 1) break;
-        case 32: TGFX_LINE_LAUNCH(8, 2, 1) break;
-        case 35: TGFX_LINE_LAUNCH(8, 1, 5) break;
-        case 36: TGFX_LINE_LAUNCH(8, 1, 6) break;
-        case 37: TGFX_LINE_LAUNCH(4, 1, 6) break;
-        case 38: TGFX_LINE_LAUNCH(8, 1, 1) break;
-        case 41: TGFX_LINE_EXP(1) break;
-        case 42: TGFX_LINE_EXP(2) break;
-        case 43: TGFX_LINE_PF(4) break;
-        case 44: TGFX_LINE_PF(8) break;
-        case 45: TGFX_LINE_PF(16) break;
-        default: TGFX_LINE_LAUNCH(8, 1, 4) break;
-      }
-#undef TGFX_LINE_LAUNCH
+    const int gq = static_cast<int>(
+        std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));  // a group per warp
+    if (!g->search_exact) {  // line probes through the node directory (default)
+      if (assemble && a.index64)
+        k_recent_line<true, true, 8, 1, 4><<<gq, kThreads, 0, s>>>(
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+      else if (assemble)
+        k_recent_line<true, false, 8, 1, 4><<<gq, kThreads, 0, s>>>(
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+      else
+        k_recent_line<false, false, 8, 1, 4><<<gq, kThreads, 0, s>>>(
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);
       after_launch("k_recent_line");
       return;
     }
-    const int64_t max_kb = assemble ? std::min<int64_t>(a.k, a.l - 1) : a.k;
-    if (variant >= 10 && max_kb < 255) {  // split search + gather (default)
-      constexpr int QLS = 4;
-      uint64_t* win = static_cast<uint64_t*>(dmalloc(sizeof(uint64_t) * a.q, s));
-      const int64_t sg = ceil_div(ceil_div(a.q, 32 * QLS), kWarps);
-      const int gs = static_cast<int>(std::min<int64_t>(sg, INT32_MAX));
-      if (variant >= 20) {  // work-queue search (default)
-        static const int gq = [] {
-          int bps = 0;
-          TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_recent_search_q<true>,
-                                                                  kThreads, 0));
-          return std::max(bps, 1) * device_info().sms;
-        }();
-        const int gsq = static_cast<int>(std::min<int64_t>(gq, ceil_div(ceil_div(a.q, 256), kWarps)));
-        if (assemble)
-          k_recent_search_q<true><<<gsq, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l,
-                                                            g->search_exact, win);
-        else
-          k_recent_search_q<false><<<gsq, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0,
-                                                             g->search_exact, win);
-        after_launch("k_recent_search_q");
-      } else {
-        if (assemble)
-          k_recent_search<true, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, l,
-                                                              g->search_exact, win);
-        else
-          k_recent_search<false, QLS><<<gs, kThreads, 0, s>>>(g->indptr, g->ts, in, a.q, a.k, 0,
-                                                               g->search_exact, win);
-        after_launch("k_recent_search");
-      }
-      const int gg = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));
-      if (assemble && a.index64)
-        k_recent_gather<true, true><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k, l,
-                                                             a.self_edge_index, magic, win, o);
-      else if (assemble)
-        k_recent_gather<true, false><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k, l,
-                                                              a.self_edge_index, magic, win, o);
-      else
-        k_recent_gather<false, false><<<gg, kThreads, 0, s>>>(g->nbr, g->eid, g->ts, in, a.q, a.k,
-                                                               0, 0, magic, win, o);
-      after_launch("k_recent_gather");
-      dfree(win, s);
-      return;
-    }
-    switch (variant >= 10 ? 4 : variant) {
-      case 1: TGFX_RECENT_LAUNCH(1, 4) break;
-      case 2: TGFX_RECENT_LAUNCH(2, 4) break;
-      case 3: TGFX_RECENT_LAUNCH(2, 3) break;
-      case 5: TGFX_RECENT_LAUNCH(4, 4) break;
-      default: TGFX_RECENT_LAUNCH(4, 3) break;
-    }
-#undef TGFX_RECENT_LAUNCH
+    // slices not known sorted / NaN-free: std::lower_bound's exact bisection, 4 per lane
+    const int gb = static_cast<int>(
+        std::min<int64_t>(ceil_div(ceil_div(a.q, 32 * 4), kWarps), INT32_MAX));
+    if (assemble && a.index64)
+      k_recent<true, true, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
+                                                          a.q, a.k, l, a.self_edge_index, magic, o);
+    else if (assemble)
+      k_recent<true, false, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
+                                                           a.q, a.k, l, a.self_edge_index, magic, o);
+    else
+      k_recent<false, false, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
+                                                            a.q, a.k, 0, 0, magic, o);
     after_launch("k_recent");
     return;
   }
-  if (!g->search_exact && a.k <= 32 && recent_variant() != 29) {  // grouped Floyd (default)
+  if (!g->search_exact && a.k <= 32) {  // grouped Floyd (default for k <= 32)
     if (assemble) {
       if (a.index64)
         launch_random_g<true, true>(a, in, o, grid, s);
