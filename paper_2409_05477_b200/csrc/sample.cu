@@ -332,12 +332,19 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
   for (int j = 0; j < QL; ++j) m[j] = lo[j];
 }
 
-template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB>
+// BULK: a full group's [32 x l] output block is staged in shared memory and written by three
+// 1-D bulk copies (cp.async.bulk.global.shared::cta, the TMA engine) instead of 3 x l / 32
+// strided store instructions per lane; l <= kBulkMaxL, int32/fp32 outputs, 16-byte aligned.
+constexpr int kBulkMaxL = 16;
+
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
   constexpr int GQ = 32 * QL;
+  // BULK staging: per warp [3][32 * l] 32-bit words (node, edge, dt)
+  extern __shared__ __align__(16) uint32_t s_out[];
   __shared__ longlong2 s_st[kWarps][GQ];  // {window start, query time bits}: one LDS.128
   __shared__ int64_t s_u[kWarps][GQ];
   __shared__ int s_kb[kWarps][GQ];
@@ -401,6 +408,58 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     int qi = div_slot(lane, width, magic);
     int j = lane - qi * width;
     const int dq = div_slot(32, width, magic), dj = 32 - dq * width;
+    if (BULK && nq == GQ) {
+      uint32_t* sn = s_out + static_cast<size_t>(warp) * 3 * GQ * l;
+      uint32_t* se = sn + GQ * l;
+      float* sd = reinterpret_cast<float*>(se + GQ * l);
+#pragma unroll 4
+      for (int s = lane; s < total; s += 32) {
+        const int kbq = s_kb[warp][qi];
+        uint32_t ni = 0, ei = 0;
+        float df = 0.0f;
+        if (j < kbq) {
+          const longlong2 st = s_st[warp][qi];
+          const int64_t p = st.x + j;
+          ni = static_cast<uint32_t>(ldg_i64(nbr + p) + 1);
+          ei = static_cast<uint32_t>(ldg_i64(eid + p) + 1);
+          df = __double2float_rn(__longlong_as_double(st.y) - ldg_f64(ts + p));
+        } else if (j == kbq) {
+          ni = static_cast<uint32_t>(s_u[warp][qi] + 1);
+          ei = static_cast<uint32_t>(self_idx);
+        }
+        sn[s] = ni;
+        se[s] = ei;
+        sd[s] = df;
+        j += dj;
+        qi += dq;
+        if (j >= width) {
+          j -= width;
+          ++qi;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bytes = static_cast<uint32_t>(total) * 4u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         static_cast<int32_t*>(o.node) + obase),
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(sn))), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         static_cast<int32_t*>(o.edge) + obase),
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(se))), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         o.dt32 + obase),
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(sd))), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // the staging is reused by this warp's next group / freed at exit: wait for the reads
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
+      continue;
+    }
 #pragma unroll 4
     for (int s = lane; s < total; s += 32) {
       const int kbq = s_kb[warp][qi];
@@ -665,6 +724,14 @@ __global__ void k_mask(int64_t q, int64_t l, const int64_t* __restrict__ valid_l
   }
 }
 
+bool bulk_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_BULK_ROWS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int grid_groups(int64_t Q) {
   const int64_t groups = ceil_div(std::max<int64_t>(Q, 1), 32);
   const int64_t blocks = ceil_div(groups, kWarps);
@@ -912,7 +979,19 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
         (width < 512) ? static_cast<uint32_t>(((1ull << 32) + width - 1) / width) : 0u;
     const int gq = static_cast<int>(
         std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));  // a group per warp
-    if (!g->search_exact) {  // line probes through the node directory (default)
+    const bool bulk = assemble && !a.index64 && a.dt32 && !a.dt64 && l <= kBulkMaxL &&
+                      ((reinterpret_cast<uintptr_t>(a.node_index) |
+                        reinterpret_cast<uintptr_t>(a.edge_index) |
+                        reinterpret_cast<uintptr_t>(a.dt32)) & 15) == 0 &&
+                      bulk_enabled();
+    if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
+      const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
+      k_recent_line<true, false, 8, 1, 4, true><<<gq, kThreads, sm, s>>>(
+          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+      after_launch("k_recent_line");
+      return;
+    }
+    if (!g->search_exact) {  // line probes through the node directory
       if (assemble && a.index64)
         k_recent_line<true, true, 8, 1, 4><<<gq, kThreads, 0, s>>>(
             g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
