@@ -36,6 +36,7 @@ extern "C" {
 #define TGFX_ECUDA 3        /* CUDA runtime / no device (std::runtime_error) */
 #define TGFX_ENOMEM 4       /* device or host allocation failed (std::bad_alloc) */
 #define TGFX_EUNSUPPORTED 5 /* e.g. ids that do not fit the requested int32 outputs */
+#define TGFX_EPARSE 6       /* tgf::ParseError (CSV ingestion) */
 
 /* sampling strategy: proj/include/tgformer/sampler.hpp:26 (SampleStrategy) */
 #define TGFX_RECENT 0
@@ -66,6 +67,9 @@ typedef struct tgfx_event {
 
 /* Opaque device-resident T-CSR (proj/include/tgformer/tcsr.hpp:20-33 TCsr). */
 typedef struct tgfx_graph tgfx_graph;
+
+/* Opaque device-resident parsed event stream (proj/include/tgformer/event_stream.hpp:26-39). */
+typedef struct tgfx_csv tgfx_csv;
 
 /* ---------------------------------------------------------------- runtime */
 const char* tgfx_last_error(void);
@@ -233,6 +237,28 @@ int tgfx_assemble_inputs_device(int64_t q, int64_t l, const void* d_node_index,
                                 const double* d_omega, const double* d_phi, int64_t d_v,
                                 int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
                                 void* stream, unsigned flags);
+
+/* ---------------------------------------------------------------- CSV ingestion */
+/* replaces tgf::load_csv (event_stream.hpp:44, event_stream.cpp:85-154): reads the file,
+ * parses it on the device (header required; rows "src,dst,timestamp[,features]"), stable
+ * sorts by timestamp and numbers the events 0..n-1 in that order; num_nodes = max id + 1.
+ * Errors carry the reference's exception type and text (TGFX_EVALIDATION / TGFX_EPARSE).
+ * Reals are parsed correctly rounded (from_chars); a literal with > 19 significant digits
+ * whose rounding needs big-integer arithmetic, or a NaN timestamp, is TGFX_EUNSUPPORTED. */
+int tgfx_load_csv(const char* path, int has_features, tgfx_csv** out);
+/* same, from CSV bytes already on the device */
+int tgfx_csv_parse_device(const char* d_bytes, int64_t nbytes, int has_features, void* stream,
+                          tgfx_csv** out);
+int tgfx_csv_info(const tgfx_csv* c, int64_t* num_events, int64_t* num_nodes, int64_t* d_e);
+/* device views: events [n] (feed tgfx_build_device directly), features [n * d_e] or NULL */
+int tgfx_csv_device_arrays(const tgfx_csv* c, const tgfx_event** events, const double** features);
+/* host copies (features may be NULL) */
+int tgfx_csv_export(const tgfx_csv* c, tgfx_event* events, double* features);
+int tgfx_csv_free(tgfx_csv* c);
+/* parse n fields d_bytes[d_off[i] .. d_off[i+1]) as int64 (kind 0) or double (kind 1) with
+ * std::from_chars semantics; d_status[i] 0 ok, 1 bad, 2 unsupported (see tgfx_load_csv) */
+int tgfx_parse_numbers_device(const char* d_bytes, const int64_t* d_off, int64_t n, int kind,
+                              int64_t* d_int, double* d_real, int* d_status, void* stream);
 
 /* ---------------------------------------------------------------- synthetic inputs */
 /* bit-identical to tgf::make_random_stream (synthetic.hpp:17-18, synthetic.cpp:12-43);

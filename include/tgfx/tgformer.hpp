@@ -130,6 +130,9 @@ struct EventStream {
   void validate() const;  // event_stream.cpp:62-83 checks and messages
 };
 
+// event_stream.hpp:44: parsed on the device (tgfx_load_csv); same ordering, ids, errors.
+EventStream load_csv(const std::string& path, bool has_features = false);
+
 // ------------------------------------------------------------------ tcsr.hpp
 namespace detail {
 struct DeviceCopy;  // device-resident T-CSR handle + content fingerprint (tgformer.cpp)

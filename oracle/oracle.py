@@ -39,6 +39,11 @@ _orc = None
 _ref = None
 
 
+def _setup_fromchars(L):
+    L.orc_from_chars_f64.argtypes = [C.c_char_p, _I64, C.POINTER(C.c_double)]
+    L.orc_from_chars_i64.argtypes = [C.c_char_p, _I64, C.POINTER(C.c_int64)]
+
+
 def lib():
     """The C restatement (oracle.c)."""
     global _orc
@@ -46,6 +51,7 @@ def lib():
         if not os.path.exists(ORACLE_SO):
             build_oracle()
         L = C.CDLL(ORACLE_SO)
+        _setup_fromchars(L)
         L.orc_mix64.restype = _U64
         L.orc_mix64.argtypes = [_U64]
         L.orc_rng_state.restype = _U64
@@ -100,6 +106,7 @@ def ref():
         L.ref_build_sequence_batch.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P,
                                                _P, _P, _P, _P]
         L.ref_build_mask.argtypes = [_I64, _I64, _P, _P, C.c_int, _P]
+        L.ref_load_csv.argtypes = [C.c_char_p, C.c_int, _P, _P, _P, _P, _P]
         L.ref_assemble_inputs.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P,
                                           _I64, _I64, _I64, C.c_int, _P]
         _ref = L
@@ -483,3 +490,38 @@ def ref_assemble_inputs(node_index, edge_index, time_delta, valid_len, node_tabl
     if rc:
         _ref_err(rc)
     return z
+
+
+# ---------------------------------------------------------------------- CSV ingestion
+def ref_load_csv(path, has_features=False):
+    """The reference's own load_csv (event_stream.cpp:85-154, compiled in oracle/_ref) ->
+    (events, num_nodes, features [n, d_e]).  Raises OracleError(code, message) with code 1
+    ValidationError, 6 ParseError (the reference's message texts)."""
+    n, v, de = (np.zeros(1, np.int64) for _ in range(3))
+    rc = ref().ref_load_csv(path.encode(), 1 if has_features else 0, _ptr(n), _ptr(v), _ptr(de),
+                            None, None)
+    if rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    ev = np.zeros(int(n[0]), dtype=EVENT_DTYPE)
+    feats = np.zeros((int(n[0]), int(de[0])), np.float64)
+    rc = ref().ref_load_csv(path.encode(), 1 if has_features else 0, _ptr(n), _ptr(v), _ptr(de),
+                            _ptr(ev) if len(ev) else _ptr(np.zeros(1, EVENT_DTYPE)),
+                            _ptr(feats) if feats.size else None)
+    if rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    return ev, int(v[0]), feats
+
+
+def from_chars(strings, kind):
+    """std::from_chars over a list of byte strings (oracle/fromchars.cpp): (ok[n], values[n])
+    with ok False where load_csv's parse_int / parse_real would throw."""
+    n = len(strings)
+    ok = np.zeros(n, bool)
+    vals = np.zeros(n, np.float64 if kind == "real" else np.int64)
+    f = lib().orc_from_chars_f64 if kind == "real" else lib().orc_from_chars_i64
+    out = (C.c_double if kind == "real" else C.c_int64)()
+    for i, b in enumerate(strings):
+        if f(b, len(b), C.byref(out)) == 0:
+            ok[i] = True
+            vals[i] = out.value
+    return ok, vals

@@ -30,6 +30,7 @@ int fail(const std::exception& e) {
   g_err = e.what();
   if (dynamic_cast<const tgf::ValidationError*>(&e)) return 1;
   if (dynamic_cast<const tgf::FormatError*>(&e)) return 2;
+  if (dynamic_cast<const tgf::ParseError*>(&e)) return 6;
   return 3;
 }
 }  // namespace
@@ -274,6 +275,34 @@ int ref_assemble_inputs(int64_t q, int64_t l, const int64_t* node_index, const i
     std::memcpy(z, out.data(), sizeof(double) * out.size());
     return 0;
   } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
+// tgf::load_csv (event_stream.cpp:85-154): two calls -- with events == nullptr it parses
+// and reports the shape (cached); then the same path again copies events / features out.
+int ref_load_csv(const char* path, int has_features, int64_t* n, int64_t* num_nodes,
+                 int64_t* d_e, void* events, double* features) {
+  static std::string cached_path;
+  static tgf::EventStream cached;
+  try {
+    if (!events || cached_path != path) {
+      cached = tgf::load_csv(path, has_features != 0);
+      cached_path = path;
+    }
+    *n = cached.size();
+    *num_nodes = cached.num_nodes;
+    *d_e = cached.d_e;
+    if (events) {
+      std::memcpy(events, cached.events.data(), sizeof(tgf::TemporalEvent) * cached.events.size());
+      if (features && cached.d_e > 0)
+        std::memcpy(features, cached.edge_features.data(),
+                    sizeof(double) * cached.edge_features.size());
+      cached_path.clear();
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    cached_path.clear();
     return fail(ex);
   }
 }

@@ -37,6 +37,12 @@ class FormatError(TgfxError):
     code = TGFX_EFORMAT
 
 
+class ParseError(TgfxError):
+    """proj/include/tgformer/common.hpp:20-22"""
+
+    code = 6
+
+
 class CudaError(TgfxError):
     code = TGFX_ECUDA
 
@@ -49,7 +55,8 @@ class Unsupported(TgfxError):
     code = TGFX_EUNSUPPORTED
 
 
-_ERRORS = {1: ValidationError, 2: FormatError, 3: CudaError, 4: OutOfMemory, 5: Unsupported}
+_ERRORS = {1: ValidationError, 2: FormatError, 3: CudaError, 4: OutOfMemory, 5: Unsupported,
+           6: ParseError}
 
 _P = C.c_void_p
 _I64 = C.c_int64
@@ -91,6 +98,13 @@ SIGNATURES = {
                                             _P, _P, _P, _P, _P, _P, _U],
     "tgfx_assemble_inputs_device": [_I64, _I64, _P, _P, _P, _P, _I, _I, _P, _I64, _P, _I64, _I,
                                     _P, _P, _I64, _I64, _I64, _I, _P, _I, _P, _U],
+    "tgfx_load_csv": [C.c_char_p, _I, C.POINTER(_P)],
+    "tgfx_csv_parse_device": [_P, _I64, _I, _P, C.POINTER(_P)],
+    "tgfx_csv_info": [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)],
+    "tgfx_csv_device_arrays": [_P, C.POINTER(_P), C.POINTER(_P)],
+    "tgfx_csv_export": [_P, _P, _P],
+    "tgfx_csv_free": [_P],
+    "tgfx_parse_numbers_device": [_P, _P, _I64, _I, _P, _P, _P, _P],
     "tgfx_sample_two_hop_device": [_P, _P, _P, _I64, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P,
                                    _P, _P, _P, _P, _P, _P, _P, _P, _U],
     "tgfx_sample_two_hop": [_P, _P, _P, _I64, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P, _P,

@@ -2,7 +2,10 @@
 // error texts, host<->device staging for the synchronous host-buffer calls, and the
 // process-wide runtime bits (thread-local error, launch counter, stream-ordered pool).
 #include <atomic>
+#include <charconv>
 #include <cstring>
+#include <fstream>
+#include <vector>
 #include <mutex>
 #include <new>
 #include <string>
@@ -539,6 +542,174 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
     a.index64 = i64;
     launch_sample(a, s);
     if (!(flags & TGFX_TRUSTED)) TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+namespace {
+
+std::string trimmed(const std::string& x) {
+  size_t a = 0, b = x.size();
+  while (a < b && (x[a] == ' ' || x[a] == '\t' || x[a] == '\r')) ++a;
+  while (b > a && (x[b - 1] == ' ' || x[b - 1] == '\t' || x[b - 1] == '\r')) --b;
+  return x.substr(a, b - a);
+}
+
+std::vector<std::string> split_commas(const std::string& line) {
+  std::vector<std::string> out;
+  size_t start = 0;
+  while (true) {
+    const size_t c = line.find(',', start);
+    if (c == std::string::npos) {
+      out.push_back(line.substr(start));
+      return out;
+    }
+    out.push_back(line.substr(start, c - start));
+    start = c + 1;
+  }
+}
+
+// The message of the first failing line, rebuilt on the host from that one line's text with
+// the reference's own checks (event_stream.cpp:111-131); the device found the line.
+[[noreturn]] void throw_csv_line_error(const std::string& raw, int64_t line_no, int code, int d_e) {
+  const std::string line = trimmed(raw);
+  const std::vector<std::string> f = split_commas(line);
+  const std::string at = "line " + std::to_string(line_no) + ": ";
+  if (code == kCsvFields)
+    throw Error(TGFX_EPARSE, at + "expected " + std::to_string(3 + d_e) + " fields, got " +
+                                 std::to_string(f.size()));
+  if (code == kCsvNegNode) throw Error(TGFX_EVALIDATION, at + "negative node id");
+  if (code == kCsvNegTime) throw Error(TGFX_EVALIDATION, at + "negative timestamp");
+  auto bad = [&](int idx, const char* what) -> std::string {
+    return at + "bad " + what + " '" + trimmed(f[static_cast<size_t>(idx)]) + "'";
+  };
+  if (code == kCsvSrc) throw Error(TGFX_EPARSE, bad(0, "src"));
+  if (code == kCsvDst) throw Error(TGFX_EPARSE, bad(1, "dst"));
+  if (code == kCsvTime) throw Error(TGFX_EPARSE, bad(2, "timestamp"));
+  // features: the first field from_chars rejects (or the first the device flagged)
+  for (int k = 0; k < d_e; ++k) {
+    const std::string v = trimmed(f[static_cast<size_t>(3 + k)]);
+    double x = 0.0;
+    const auto r = std::from_chars(v.data(), v.data() + v.size(), x);
+    if (code == kCsvFeature && (r.ec != std::errc{} || r.ptr != v.data() + v.size()))
+      throw Error(TGFX_EPARSE, bad(3 + k, "feature"));
+  }
+  throw Error(TGFX_EUNSUPPORTED,
+              at + "a real with more than 19 significant digits whose rounding needs "
+                   "big-integer arithmetic, or a NaN timestamp (not parsed on the device)");
+}
+
+}  // namespace
+
+int tgfx_csv_parse_device(const char* d_bytes, int64_t nbytes, int has_features, void* stream,
+                          tgfx_csv** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    if (nbytes < 0) throw Error(TGFX_EVALIDATION, "negative size");
+    cudaStream_t s = as_stream(stream);
+    device_info();
+    // header (event_stream.cpp:90-95): first line, on the host
+    std::string header;
+    for (int64_t got = 0; got < nbytes;) {
+      const int64_t take = std::min<int64_t>(nbytes - got, 1 << 16);
+      std::string piece(static_cast<size_t>(take), '\0');
+      TGFX_CUDA(cudaMemcpyAsync(&piece[0], d_bytes + got, take, cudaMemcpyDeviceToHost, s));
+      TGFX_CUDA(cudaStreamSynchronize(s));
+      const size_t nl = piece.find('\n');
+      header += piece.substr(0, nl);
+      got += take;
+      if (nl != std::string::npos) break;
+    }
+    if (nbytes == 0) throw Error(TGFX_EPARSE, "empty input");
+    const size_t hf = split_commas(trimmed(header)).size();
+    if (hf < 3) throw Error(TGFX_EPARSE, "line 1: header needs at least src,dst,timestamp");
+    const int d_e = has_features ? static_cast<int>(hf - 3) : 0;
+    CsvResult r;
+    const uint64_t err = parse_csv_device(d_bytes, nbytes, d_e, &r, s);
+    if (err != ~0ull) {
+      std::string raw(static_cast<size_t>(r.err_line_end - r.err_line_start), '\0');
+      if (!raw.empty())
+        TGFX_CUDA(cudaMemcpyAsync(&raw[0], d_bytes + r.err_line_start, raw.size(),
+                                  cudaMemcpyDeviceToHost, s));
+      TGFX_CUDA(cudaStreamSynchronize(s));
+      throw_csv_line_error(raw, static_cast<int64_t>(err >> 8), static_cast<int>(err & 0xff), d_e);
+    }
+    tgfx_csv* c = new tgfx_csv();
+    c->n = r.n;
+    c->num_nodes = r.num_nodes;
+    c->d_e = d_e;
+    c->events = r.events;
+    c->features = r.features;
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    *out = c;
+  });
+}
+
+int tgfx_load_csv(const char* path, int has_features, tgfx_csv** out) {
+  return guarded([&] {
+    if (!out) throw Error(TGFX_EVALIDATION, "null output");
+    *out = nullptr;
+    const std::string p = path ? path : "";
+    std::ifstream in(p, std::ios::binary | std::ios::ate);
+    if (!in) throw Error(TGFX_EVALIDATION, "cannot open '" + p + "'");  // event_stream.cpp:87
+    const std::streamsize size = in.tellg();
+    in.seekg(0);
+    if (size <= 0) throw Error(TGFX_EPARSE, "empty file '" + p + "'");  // :90
+    std::vector<char> host(static_cast<size_t>(size));
+    in.read(host.data(), size);
+    if (!in) throw Error(TGFX_EVALIDATION, "cannot read '" + p + "'");
+    cudaStream_t s = 0;
+    device_info();
+    DBuf dev(static_cast<size_t>(size), s);
+    h2d(dev.p, host.data(), static_cast<size_t>(size), s);
+    const int rc = tgfx_csv_parse_device(dev.as<char>(), size, has_features, s, out);
+    if (rc) throw Error(rc, g_err);
+  });
+}
+
+int tgfx_csv_info(const tgfx_csv* c, int64_t* num_events, int64_t* num_nodes, int64_t* d_e) {
+  return guarded([&] {
+    if (!c) throw Error(TGFX_EVALIDATION, "null stream");
+    if (num_events) *num_events = c->n;
+    if (num_nodes) *num_nodes = c->num_nodes;
+    if (d_e) *d_e = c->d_e;
+  });
+}
+
+int tgfx_csv_device_arrays(const tgfx_csv* c, const tgfx_event** events, const double** features) {
+  return guarded([&] {
+    if (!c) throw Error(TGFX_EVALIDATION, "null stream");
+    if (events) *events = c->events;
+    if (features) *features = c->features;
+  });
+}
+
+int tgfx_csv_export(const tgfx_csv* c, tgfx_event* events, double* features) {
+  return guarded([&] {
+    if (!c) throw Error(TGFX_EVALIDATION, "null stream");
+    cudaStream_t s = 0;
+    d2h(events, c->events, sizeof(tgfx_event) * c->n, s);
+    if (features && c->d_e > 0) d2h(features, c->features, sizeof(double) * c->n * c->d_e, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tgfx_csv_free(tgfx_csv* c) {
+  return guarded([&] {
+    if (!c) return;
+    if (c->events) dfree(c->events, 0);
+    if (c->features) dfree(c->features, 0);
+    delete c;
+  });
+}
+
+int tgfx_parse_numbers_device(const char* d_bytes, const int64_t* d_off, int64_t n, int kind,
+                              int64_t* d_int, double* d_real, int* d_status, void* stream) {
+  return guarded([&] {
+    if (kind != 0 && kind != 1) throw Error(TGFX_EVALIDATION, "kind must be 0 (int) or 1 (real)");
+    cudaStream_t s = as_stream(stream);
+    launch_parse_numbers(d_bytes, d_off, n, kind, d_int, d_real, d_status, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
   });
 }
 

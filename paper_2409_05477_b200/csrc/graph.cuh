@@ -51,6 +51,13 @@ struct tgfx_graph {
   BuildFlags* hflags = nullptr;  // pinned host mirror
 };
 
+// Parsed event stream resident on the device (tgfx_load_csv / tgfx_csv_parse_device).
+struct tgfx_csv {
+  int64_t n = 0, num_nodes = 0, d_e = 0;
+  tgfx_event* events = nullptr;
+  double* features = nullptr;
+};
+
 namespace tgfx {
 
 // max num_nodes of the shared-memory (per-chunk cursor) fast path
@@ -140,6 +147,25 @@ struct AssembleInputsArgs {
   int z_type = 0;
 };
 void launch_assemble_inputs(const AssembleInputsArgs& a, int* bad, cudaStream_t s);
+
+// ------------------------------------------------------------------ CSV ingestion
+struct CsvResult {
+  int64_t n = 0, num_nodes = 0;
+  tgfx_event* events = nullptr;  // device, n
+  double* features = nullptr;    // device, n x d_e (or null)
+  int64_t err_line_start = 0, err_line_end = 0;  // byte span of the failing line
+};
+// error codes of parse_csv_device's error word (line_no << 8 | code)
+enum CsvError : int {
+  kCsvFields = 1, kCsvSrc, kCsvDst, kCsvTime, kCsvNegNode, kCsvNegTime, kCsvFeature,
+  kCsvUnsupported
+};
+// ~0 on success (res filled), else the first failing line's error word
+uint64_t parse_csv_device(const char* d_buf, int64_t nbytes, int d_e, CsvResult* res,
+                          cudaStream_t s);
+// fields [off[i], off[i+1]) as int64 (kind 0) / double (kind 1); status 0 ok, 1 bad, 2 unsupported
+void launch_parse_numbers(const char* buf, const int64_t* off, int64_t n, int kind, int64_t* iout,
+                          double* dout, int* status, cudaStream_t s);
 
 // ------------------------------------------------------------------ synthetic
 void launch_random_stream(int64_t E, int64_t V, uint64_t seed, double zipf, tgfx_event* d_out,

@@ -24,6 +24,7 @@ void check(int rc) {
   const std::string msg = tgfx_last_error();
   if (rc == TGFX_EVALIDATION) throw ValidationError(msg);
   if (rc == TGFX_EFORMAT) throw FormatError(msg);
+  if (rc == TGFX_EPARSE) throw ParseError(msg);
   if (rc == TGFX_ENOMEM) throw std::bad_alloc();
   throw std::runtime_error(msg);
 }
@@ -130,6 +131,25 @@ void EventStream::validate() const {
   if (!node_features.empty() && (node_features.rows() != static_cast<std::size_t>(num_nodes) ||
                                  node_features.cols() != static_cast<std::size_t>(d_v)))
     throw ValidationError("node feature matrix shape mismatch");
+}
+
+EventStream load_csv(const std::string& path, bool has_features) {
+  tgfx_csv* c = nullptr;
+  detail::check(tgfx_load_csv(path.c_str(), has_features ? 1 : 0, &c));
+  struct Free {
+    tgfx_csv* c;
+    ~Free() { tgfx_csv_free(c); }
+  } guard{c};
+  std::int64_t n = 0, v = 0, d_e = 0;
+  detail::check(tgfx_csv_info(c, &n, &v, &d_e));
+  EventStream s;
+  s.num_nodes = v;
+  s.d_e = d_e;
+  s.events.resize(static_cast<std::size_t>(n));
+  if (d_e > 0) s.edge_features = Matrix(static_cast<std::size_t>(n), static_cast<std::size_t>(d_e));
+  detail::check(tgfx_csv_export(c, reinterpret_cast<tgfx_event*>(s.events.data()),
+                                d_e > 0 ? s.edge_features.data() : nullptr));
+  return s;
 }
 
 // ------------------------------------------------------------------ T-CSR

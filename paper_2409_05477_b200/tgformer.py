@@ -24,7 +24,7 @@ from typing import List, NamedTuple
 import numpy as np
 
 from ._lib import (TGFX_INDEX64, TGFX_RANDOM, TGFX_RECENT, TGFX_TRUSTED, FormatError,
-                   TgfxError, ValidationError, check, lib)
+                   ParseError, TgfxError, ValidationError, check, lib)
 
 EVENT_DTYPE = np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
 
@@ -33,6 +33,7 @@ __all__ = ["EventStream", "TCsr", "NeighborEntry", "NeighborSample", "SequenceBa
            "sample_batch", "sample_batch_arrays", "sample_assemble", "sample_two_hop",
            "build_sequence", "build_sequence_batch", "build_mask", "make_random_stream",
            "parse_strategy", "parse_mask_kind", "ValidationError", "FormatError", "TgfxError",
+           "ParseError", "load_csv",
            "EVENT_DTYPE"]
 
 
@@ -373,3 +374,20 @@ def make_random_stream(num_edges, num_nodes, seed, zipf_exponent=1.2):
     ev = np.zeros(max(num_edges, 1), EVENT_DTYPE)
     check(lib().tgfx_make_random_stream(num_edges, num_nodes, seed, zipf_exponent, _ptr(ev)))
     return EventStream(ev[:num_edges], num_nodes)
+
+
+def load_csv(path, has_features=False):
+    """tgf::load_csv (proj/src/event_stream.cpp:85-154), parsed on the device ->
+    EventStream (events in the reference's layout) and the edge features [n, d_e]."""
+    h = C.c_void_p()
+    check(lib().tgfx_load_csv(str(path).encode(), 1 if has_features else 0, C.byref(h)))
+    try:
+        n, v, de = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().tgfx_csv_info(h, C.byref(n), C.byref(v), C.byref(de)))
+        ev = np.zeros(n.value, dtype=EVENT_DTYPE)
+        feats = np.zeros((n.value, de.value), dtype=np.float64)
+        check(lib().tgfx_csv_export(h, _ptr(ev) if n.value else None,
+                                    _ptr(feats) if feats.size else None))
+    finally:
+        lib().tgfx_csv_free(h)
+    return EventStream(ev, v.value), feats
