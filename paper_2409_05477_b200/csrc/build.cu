@@ -738,17 +738,116 @@ __global__ void k_gather_entries(const tgfx_event* __restrict__ ev,
 }
 
 // ------------------------------------------------------------------ node directory
+// Slice time buckets (sampler search acceleration).  A sorted, NaN-free slice of n >=
+// kBucketMinSlice entries with finite t_first < t_last gets nb = ceil(n / R) buckets of
+// equal time width; bkt[j] = #entries e with bucket_of(ts[e]) < j, j = 0..nb.  bucket_of is
+// monotone, so for t_first < t <= t_last and j = bucket_of(t) every entry before bkt[j] has
+// ts < t and every entry from bkt[j + 1] on has ts > t: lower_bound(t) is in [bkt[j],
+// bkt[j + 1]], typically a range of R entries -- one line probe instead of a chain of them.
+constexpr int64_t kBucketMinSlice = 32;
+
+__device__ __forceinline__ int64_t bucket_count(int64_t n, double t_first, double t_last,
+                                                int64_t R, double* scale) {
+  if (R <= 0 || n < kBucketMinSlice || n > 0xffffffffLL) return 0;
+  if (!(t_first < t_last) || isinf(t_first) || isinf(t_last)) return 0;
+  const int64_t nb = ceil_div(n, R);
+  const double sc = static_cast<double>(nb) / (t_last - t_first);
+  if (!(sc < 1e300)) return 0;  // near-zero time span: no useful bucket grid
+  *scale = sc;
+  return nb;
+}
+
+// pass 1: directory records (bkt pointer filled in pass 2) and bucket table sizes
+constexpr int kFillPer = 8;
+constexpr int64_t kFillTile = 256 * kFillPer;
+
 __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __restrict__ ts,
-                           int64_t V, NodeDir* __restrict__ dir) {
+                           int64_t V, int64_t R, NodeDir* __restrict__ dir,
+                           uint32_t* __restrict__ cnt, int32_t* __restrict__ tile_node) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= V) return;
   const int64_t a = indptr[u], b = indptr[u + 1];
+  if (tile_node)  // the node holding the first entry of each k_bucket_fill tile
+    for (int64_t t = ceil_div(a, kFillTile); t * kFillTile < b; ++t)
+      tile_node[t] = static_cast<int32_t>(u);
   NodeDir d;
   d.start = a;
   d.end = b;
   d.t_first = b > a ? ts[a] : 0.0;
   d.t_last = b > a ? ts[b - 1] : 0.0;
+  d.bkt = nullptr;
+  d.scale = 0.0;
+  d.nb = cnt ? bucket_count(b - a, d.t_first, d.t_last, R, &d.scale) : 0;
+  d.width = d.nb ? (d.t_last - d.t_first) / static_cast<double>(d.nb) : 0.0;
   dir[u] = d;
+  if (cnt) cnt[u] = d.nb ? static_cast<uint32_t>(d.nb + 1) : 0u;
+}
+
+// pass 2: bucket table offsets (exclusive scan of the sizes) -> pointers
+__global__ void k_node_dir_bkt(const int64_t* __restrict__ off, int64_t V, uint32_t* bkt,
+                               NodeDir* __restrict__ dir) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= V) return;
+  if (dir[u].nb) dir[u].bkt = bkt + off[u];
+}
+
+// pass 3: one thread per slice entry writes the table entries of the buckets that start at
+// it: bkt[j] = r for j in (bucket_of(ts[r - 1]), bucket_of(ts[r])], and bkt[nb] = n.  Tile
+// t's node range starts at tile_node[t] and ends at or before tile_node[t + 1]; within it
+// an entry's node is found by a bisection of indptr (tiles spanning several slices only).
+__global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__ indptr,
+                                                     const double* __restrict__ ts,
+                                                     const NodeDir* __restrict__ dir,
+                                                     const int32_t* __restrict__ tile_node,
+                                                     int64_t V, int64_t m) {
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kFillTile;
+  if (i0 >= m) return;
+  const int64_t i1 = min(i0 + kFillTile, m) - 1;
+  const int64_t v0 = tile_node[blockIdx.x];
+  const int64_t v1 = i1 + 1 < m ? tile_node[blockIdx.x + 1] : V - 1;
+  if (dir[v0].end > i1) {  // the whole tile lies in one slice (hub slices): no node search
+    const NodeDir d = dir[v0];
+    if (!d.nb) return;
+    uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) {
+      const int64_t i = i0 + k * 256 + threadIdx.x;
+      const double x = i <= i1 ? ts[i] : 0.0;
+      double xp = __shfl_up_sync(0xffffffffu, x, 1);  // every lane runs every iteration
+      if (lane == 0 && i > d.start && i <= i1) xp = ts[i - 1];
+      if (i > i1) continue;
+      const int64_t r = i - d.start;
+      const int64_t jr = bucket_of(x, d.t_first, d.scale, d.nb);
+      const int64_t jp = r ? bucket_of(xp, d.t_first, d.scale, d.nb) : -1;
+      for (int64_t j = jp + 1; j <= jr; ++j) bkt[j] = static_cast<uint32_t>(r);
+      if (i == d.end - 1) bkt[d.nb] = static_cast<uint32_t>(d.end - d.start);
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < kFillPer; ++k) {
+    const int64_t i = i0 + k * 256 + threadIdx.x;
+    if (i > i1) break;
+    int64_t lo = v0, n = v1 - v0 + 2;  // upper_bound over indptr[v0..v1+1]
+    while (n > 0) {
+      const int64_t h = n >> 1;
+      if (__ldg(reinterpret_cast<const long long*>(indptr) + lo + h) <= i) {
+        lo += h + 1;
+        n -= h + 1;
+      } else {
+        n = h;
+      }
+    }
+    const NodeDir& d = dir[lo - 1];
+    if (!d.nb) continue;
+    uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
+    const int64_t r = i - d.start;
+    const int64_t jr = bucket_of(ts[i], d.t_first, d.scale, d.nb);
+    const int64_t jp = r ? bucket_of(ts[i - 1], d.t_first, d.scale, d.nb) : -1;
+    for (int64_t j = jp + 1; j <= jr; ++j) bkt[j] = static_cast<uint32_t>(r);
+    if (i == d.end - 1) bkt[d.nb] = static_cast<uint32_t>(d.end - d.start);
+  }
 }
 
 // ------------------------------------------------------------------ validate (tcsr.cpp:54-81)
@@ -1110,6 +1209,7 @@ void graph_release(tgfx_graph* g) {
   if (g->ts) dfree(g->ts, s);
   if (g->dflags) dfree(g->dflags, s);
   if (g->dir) dfree(g->dir, s);
+  if (g->bkt) dfree(g->bkt, s);
   if (g->ws) dfree(g->ws, s);
   if (g->ws_small) dfree(g->ws_small, s);
   if (g->ws_rec) dfree(g->ws_rec, s);
@@ -1117,6 +1217,8 @@ void graph_release(tgfx_graph* g) {
   g->indptr = g->nbr = g->eid = nullptr;
   g->ts = nullptr;
   g->dir = nullptr;
+  g->bkt = nullptr;
+  g->bkt_cap = 0;
   g->dflags = nullptr;
   g->hflags = nullptr;
   g->ws = g->ws_small = g->ws_rec = nullptr;
@@ -1172,10 +1274,48 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   build_node_dir(g, s);
 }
 
+// entries per time bucket (TGFX_BUCKET_ENTRIES, default 8; 0 disables the tables)
+static int64_t bucket_entries() {
+  static const int64_t r = [] {
+    const char* e = getenv("TGFX_BUCKET_ENTRIES");
+    return e ? static_cast<int64_t>(atoll(e)) : static_cast<int64_t>(8);
+  }();
+  return r;
+}
+
 void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   if (g->V <= 0) return;
-  k_node_dir<<<static_cast<int>(ceil_div(g->V, 256)), 256, 0, s>>>(g->indptr, g->ts, g->V, g->dir);
+  const int64_t R = g->search_exact ? 0 : bucket_entries();
+  const int vb = static_cast<int>(ceil_div(g->V, 256));
+  if (R <= 0) {
+    k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr, nullptr);
+    after_launch("k_node_dir");
+    return;
+  }
+  // table size <= sum over slices of (n / R + 2) = m / R + 2V: allocated without a sync
+  const int64_t cap = g->m / R + 2 * g->V + 1;
+  if (g->bkt_cap < cap) {
+    if (g->bkt) dfree(g->bkt, s);
+    g->bkt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * cap, s));
+    g->bkt_cap = cap;
+  }
+  uint32_t* cnt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->V, s));
+  int64_t* off = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (g->V + 1), s));
+  const int64_t tiles = ceil_div(g->m, kFillTile);
+  int32_t* tile_node = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * std::max<int64_t>(tiles, 1), s));
+  k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, cnt, tile_node);
   after_launch("k_node_dir");
+  scan_u32_to_i64(cnt, g->V, off, s);
+  k_node_dir_bkt<<<vb, 256, 0, s>>>(off, g->V, g->bkt, g->dir);
+  after_launch("k_node_dir_bkt");
+  if (g->m > 0) {
+    k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->ts, g->dir, tile_node,
+                                                          g->V, g->m);
+    after_launch("k_bucket_fill");
+  }
+  dfree(tile_node, s);
+  dfree(cnt, s);
+  dfree(off, s);
 }
 
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {

@@ -12,10 +12,31 @@ struct BuildFlags {
   long long min_eid;
 };
 
-struct __align__(16) NodeDir {
+// 64 B per node (one 64-byte line, two 256-bit loads).  bkt != nullptr: the slice has a time
+// bucket table of nb + 1 entries, bkt[j] = #slice entries whose bucket_of(ts) < j (relative),
+// so lower_bound(t) lies in [bkt[j], bkt[j + 1]] for j = bucket_of(t) (see build_node_dir).
+struct __align__(32) NodeDir {
   int64_t start, end;
   double t_first, t_last;
+  const uint32_t* bkt;
+  double scale;  // nb / (t_last - t_first)
+  int64_t nb;
+  double width;  // (t_last - t_first) / nb: bucket edges for the interpolation hints
 };
+
+// bucket of time t in a slice with a bucket table: floor((t - t_first) * scale) clamped to
+// nb - 1.  Monotone non-decreasing in t; the builder and the sampler evaluate this same
+// expression (explicitly rounded, never contracted), which is all exactness needs.
+__host__ __device__ __forceinline__ int64_t bucket_of(double t, double t_first, double scale,
+                                                      int64_t nb) {
+#ifdef __CUDA_ARCH__
+  const double x = __dmul_rn(__dsub_rn(t, t_first), scale);
+#else
+  volatile double dx = t - t_first;
+  const double x = dx * scale;
+#endif
+  return x < static_cast<double>(nb - 1) ? static_cast<int64_t>(x) : nb - 1;
+}
 
 // proj/include/tgformer/tcsr.hpp:20-33 (TCsr), resident on one device.  SoA columns in HBM:
 //   indptr int64[V+1] | nbr int64[m] | eid int64[m] | ts f64[m]   (m = n * (1 + reverse))
@@ -35,6 +56,9 @@ struct tgfx_graph {
   // node directory, 32 B per node: {slice start, slice end, ts[start], ts[end-1]} -- one
   // record gives the sampler both the slice bounds and the interpolation bracket
   NodeDir* dir = nullptr;
+  // time bucket tables of the slices (uint32, ~m / bucket_entries + 2V), see NodeDir
+  uint32_t* bkt = nullptr;
+  int64_t bkt_cap = 0;
   // bound on the other endpoint (nbr ids): V for an ordinary build; the global node count for
   // one node range of a partitioned build (reverse = 0, nbr ids stay global)
   int64_t other_limit = 0;

@@ -245,6 +245,35 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
 //   (last) window gather    suffix-infill rows written slot-parallel (coalesced), as k_recent.
 // On the GDELT-shaped workload this is ~3 probe rounds per query on average (vs ~13 for
 // bisection and ~7 for point interpolation), and ~5.5 for the slowest lane of a warp.
+// one 64-byte directory record (two 256-bit loads); absent queries get an empty record
+__device__ __forceinline__ NodeDir load_dir(const NodeDir* __restrict__ dir, int64_t u, bool pres) {
+  NodeDir d;
+  if (pres) {
+    unsigned long long x0, x1, x2, x3, y0, y1, y2, y3;
+    const NodeDir* p = dir + u;
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(p));
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(y0), "=l"(y1), "=l"(y2), "=l"(y3) : "l"(reinterpret_cast<const char*>(p) + 32));
+    d.start = static_cast<int64_t>(x0);
+    d.end = static_cast<int64_t>(x1);
+    d.t_first = __longlong_as_double(static_cast<long long>(x2));
+    d.t_last = __longlong_as_double(static_cast<long long>(x3));
+    d.bkt = reinterpret_cast<const uint32_t*>(y0);
+    d.scale = __longlong_as_double(static_cast<long long>(y1));
+    d.nb = static_cast<int64_t>(y2);
+    d.width = __longlong_as_double(static_cast<long long>(y3));
+  } else {
+    d.start = d.end = 0;
+    d.t_first = d.t_last = 0.0;
+    d.bkt = nullptr;
+    d.scale = 0.0;
+    d.nb = 0;
+    d.width = 0.0;
+  }
+  return d;
+}
+
 template <int W, int QL>
 __device__ __forceinline__ void search_lines(const double* __restrict__ ts, const NodeDir (&d)[QL],
                                              const bool (&pres)[QL], const double (&t)[QL],
@@ -265,6 +294,20 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
     } else {
       lo[j] = 1;
       hi[j] = n - 1;
+    }
+  }
+  // time buckets: [lo, hi] narrows to [bkt[j], bkt[j + 1]] (typically ~R entries, one or two
+  // lines); the interpolation hints become the bucket's edges
+  // (ts[bkt[j] - 1] < t < ts[bkt[j + 1]], so the invariant ts[lo - 1] < t <= ts[hi] holds)
+#pragma unroll
+  for (int j = 0; j < QL; ++j) {
+    if (lo[j] < hi[j] && d[j].bkt) {
+      const int64_t jb = bucket_of(t[j], d[j].t_first, d[j].scale, d[j].nb);
+      const int64_t b0 = __ldg(d[j].bkt + jb), b1 = __ldg(d[j].bkt + jb + 1);
+      lo[j] = max(b0, lo[j]);
+      hi[j] = min(b1, hi[j]);
+      vlo[j] = d[j].t_first + static_cast<double>(jb) * d[j].width;  // interpolation hints
+      vhi[j] = vlo[j] + d[j].width;
     }
   }
   while (true) {
@@ -365,19 +408,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
     }
 #pragma unroll
-    for (int j = 0; j < QL; ++j) {  // one 32-byte directory record: bounds + bracket
-      if (pres[j]) {
-        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[j]);
-        const longlong2 x = __ldg(p), y = __ldg(p + 1);
-        d[j].start = x.x;
-        d[j].end = x.y;
-        d[j].t_first = __longlong_as_double(y.x);
-        d[j].t_last = __longlong_as_double(y.y);
-      } else {
-        d[j].start = d[j].end = 0;
-        d[j].t_first = d[j].t_last = 0.0;
-      }
-    }
+    for (int j = 0; j < QL; ++j) d[j] = load_dir(dir, u[j], pres[j]);  // bounds + bracket + buckets
     search_lines<W, QL>(ts, d, pres, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
@@ -533,17 +564,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
       const bool pres[1] = {present};
       const double t1[1] = {t};
       int64_t m1[1];
-      if (present) {
-        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u);
-        const longlong2 x = __ldg(p), y = __ldg(p + 1);
-        d[0].start = x.x;
-        d[0].end = x.y;
-        d[0].t_first = __longlong_as_double(y.x);
-        d[0].t_last = __longlong_as_double(y.y);
-      } else {
-        d[0].start = d[0].end = 0;
-        d[0].t_first = d[0].t_last = 0.0;
-      }
+      d[0] = load_dir(dir, u, present);
       search_lines<8, 1>(ts, d, pres, t1, m1);
       m = m1[0];
     }
@@ -772,17 +793,7 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
       bool pres[1];
       pres[0] = q < Q && fetch_query(in, q, u[0], t[0]);
       NodeDir d[1];
-      if (pres[0]) {
-        const longlong2* p = reinterpret_cast<const longlong2*>(dir + u[0]);
-        const longlong2 x = __ldg(p), y = __ldg(p + 1);
-        d[0].start = x.x;
-        d[0].end = x.y;
-        d[0].t_first = __longlong_as_double(y.x);
-        d[0].t_last = __longlong_as_double(y.y);
-      } else {
-        d[0].start = d[0].end = 0;
-        d[0].t_first = d[0].t_last = 0.0;
-      }
+      d[0] = load_dir(dir, u[0], pres[0]);
       search_lines<8, 1>(ts, d, pres, t, m);
       s_lo[warp][lane] = d[0].start;
       s_m[warp][lane] = m[0];
@@ -987,7 +998,7 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
       const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
       k_recent_line<true, false, 8, 1, 4, true><<<gq, kThreads, sm, s>>>(
-          g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
       after_launch("k_recent_line");
       return;
     }

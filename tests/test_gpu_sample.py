@@ -292,3 +292,64 @@ def test_batched_launch_equals_one_call_per_batch(T, oracle_mod):
                                               int(seeds[b].item()), l, E + 1)
             got = {kk: v[s:e].cpu().numpy() for kk, v in out.items()}
             check_rows(got, want, (strat, b))
+
+
+def test_time_buckets_on_adversarial_slices(T, oracle_mod):
+    """The per-slice time buckets (build_node_dir) narrow each search to [bkt[j], bkt[j+1]];
+    exactness rests on bucket_of being monotone and evaluated identically by the builder and
+    the sampler.  Slices built to stress that: uniform, bursty tie clusters, all ties, a
+    geometric 1.5^i spread up to 1e264, a span of a few ulps, negative times, +-inf ends,
+    subnormal spans, -0.0/0.0 ties, slices just under / over the bucket threshold; queries at
+    every entry time, its neighbours one ulp away, midpoints, and the bucket edges."""
+    rng = np.random.default_rng(12)
+    slices = [
+        np.sort(rng.uniform(0, 1e4, 5000)),
+        np.sort(np.concatenate([np.full(1000, 10.0), np.full(1000, 20.0), np.full(1000, 30.5),
+                                rng.uniform(0, 40, 300)])),
+        np.full(2000, 7.0),
+        1.5 ** np.arange(1500, dtype=np.float64),
+        1.0 + np.arange(100) * np.spacing(1.0),
+        np.sort(rng.uniform(-1e6, -1, 3000)),
+        np.concatenate([[-np.inf], np.sort(rng.uniform(0, 5, 200)), [np.inf]]),
+        np.arange(64, dtype=np.float64) * 5e-324,
+        np.sort(rng.uniform(0, 1, 31)),
+        np.sort(rng.uniform(0, 1, 33)),
+        np.array([-0.0, 0.0] * 40),
+        np.zeros(0),
+        np.sort(rng.exponential(1.0, 4000)) * 1e-300,
+        np.sort(np.round(rng.uniform(0, 50, 6000))),
+    ]
+    V = len(slices)
+    lens = np.array([len(s) for s in slices])
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    m = int(indptr[-1])
+    ts = np.concatenate(slices).astype(np.float64)
+    nbr = rng.integers(0, V, m).astype(np.int64)
+    eid = rng.permutation(m).astype(np.int64)
+    g = T.TCsr.from_host(V, m, False, indptr, nbr, eid, ts)
+    og = {"indptr": indptr, "nbr": nbr, "eid": eid, "ts": ts, "num_nodes": V, "num_edges": m}
+    qn, qt = [], []
+    for u, s in enumerate(slices):
+        fin = s[np.isfinite(s)]
+        cand = [s, np.nextafter(s, np.inf), np.nextafter(s, -np.inf), [np.inf, -np.inf, np.nan]]
+        if len(fin) > 1:
+            cand.append((fin[1:] + fin[:-1]) / 2)
+            for R in (4, 8, 16):  # bucket edges for the bucket sizes the sampler may use
+                nb = -(-len(s) // R)
+                w = (fin[-1] - fin[0]) / nb
+                e = fin[0] + np.arange(nb + 1) * w
+                cand += [e, np.nextafter(e, np.inf), np.nextafter(e, -np.inf)]
+        c = np.concatenate([np.asarray(x, np.float64) for x in cand])
+        qn.append(np.full(len(c), u, np.int64))
+        qt.append(c)
+    nodes, times = np.concatenate(qn), np.concatenate(qt)
+    for strat, k, l in (("recent", 10, 11), ("random", 12, 13), ("recent", 40, 33)):
+        want = oracle_mod.sample_assemble(og, nodes, times, k, strat, 5, l, m + 1)
+        got = T.sample_assemble(g, nodes, times, k, strat, 5, l, m + 1, dt64=True)
+        assert np.array_equal(got["node_index"].astype(np.int64), want["node_index"]), strat
+        assert np.array_equal(got["edge_index"].astype(np.int64), want["edge_index"]), strat
+        assert np.array_equal(got["valid_len"].astype(np.int64), want["valid_len"]), strat
+        assert np.array_equal(got["time_delta64"], want["time_delta"], equal_nan=True), strat
+    c, nb, ed, tsr = T.sample_batch_arrays(g, nodes, times, 10, "recent", 5)
+    cw, nw, ew, tw = oracle_mod.sample_batch(og, nodes, times, 10, "recent", 5)
+    assert np.array_equal(c, cw) and np.array_equal(nb, nw) and np.array_equal(ed, ew)
