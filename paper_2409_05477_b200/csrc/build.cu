@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
     const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev, int passes,
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
     const int64_t* __restrict__ cdelta, ulonglong2* __restrict__ cold_img,
-    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out) {
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, double* __restrict__ ts_out,
+    uint4* __restrict__ rec_out) {
   constexpr int kTW = kTT / 32;
   constexpr int NE = kTE * R;       // entries per tile
   constexpr int KPT = NE / kTT;     // keys per thread
@@ -610,6 +611,10 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
         nbr_out[pos[k]] = other;
         eid_out[pos[k]] = a.x;
         ts_out[pos[k]] = __longlong_as_double(b.y);
+        if (rec_out)
+          rec_out[pos[k]] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
+                                       static_cast<uint32_t>(b.y),
+                                       static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
       }
     }
     __syncthreads();  // stage buffer consumed, cursors final for this tile
@@ -645,7 +650,8 @@ __global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ i
                                                 const int64_t* __restrict__ cdelta,
                                                 int64_t* __restrict__ nbr_out,
                                                 int64_t* __restrict__ eid_out,
-                                                double* __restrict__ ts_out) {
+                                                double* __restrict__ ts_out,
+                                                uint4* __restrict__ rec_out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncold;
        i += (int64_t)gridDim.x * blockDim.x) {
     const ulonglong2 a = __ldg(img + 2 * i);
@@ -654,6 +660,9 @@ __global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ i
     nbr_out[pos] = static_cast<int64_t>(a.x);
     eid_out[pos] = static_cast<int64_t>(a.y);
     ts_out[pos] = __longlong_as_double(static_cast<long long>(b.x));
+    if (rec_out)
+      rec_out[pos] = make_uint4(static_cast<uint32_t>(a.x), static_cast<uint32_t>(a.y),
+                                static_cast<uint32_t>(b.x), static_cast<uint32_t>(b.x >> 32));
   }
 }
 
@@ -748,7 +757,7 @@ constexpr int64_t kBucketMinSlice = 32;
 
 __device__ __forceinline__ int64_t bucket_count(int64_t n, double t_first, double t_last,
                                                 int64_t R, double* scale) {
-  if (R <= 0 || n < kBucketMinSlice || n > 0xffffffffLL) return 0;
+  if (R <= 0 || n < kBucketMinSlice || n > 0x7fffffffLL) return 0;  // int bucket indices
   if (!(t_first < t_last) || isinf(t_first) || isinf(t_last)) return 0;
   const int64_t nb = ceil_div(n, R);
   const double sc = static_cast<double>(nb) / (t_last - t_first);
@@ -796,13 +805,33 @@ __global__ void k_node_dir_bkt(const int64_t* __restrict__ off, int64_t V, uint3
 // t's node range starts at tile_node[t] and ends at or before tile_node[t + 1]; within it
 // an entry's node is found by a bisection of indptr (tiles spanning several slices only).
 __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__ indptr,
+                                                     const int64_t* __restrict__ nbr,
+                                                     const int64_t* __restrict__ eid,
                                                      const double* __restrict__ ts,
                                                      const NodeDir* __restrict__ dir,
                                                      const int32_t* __restrict__ tile_node,
-                                                     int64_t V, int64_t m) {
+                                                     int64_t V, int64_t m, bool buckets,
+                                                     uint4* __restrict__ rec) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kFillTile;
   if (i0 >= m) return;
   const int64_t i1 = min(i0 + kFillTile, m) - 1;
+  double x[kFillPer];
+#pragma unroll
+  for (int k = 0; k < kFillPer; ++k) {
+    const int64_t i = i0 + k * 256 + threadIdx.x;
+    x[k] = i <= i1 ? ts[i] : 0.0;
+  }
+  if (rec) {  // gather records of the tile's entries (coalesced 16-byte stores)
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) {
+      const int64_t i = i0 + k * 256 + threadIdx.x;
+      if (i > i1) break;
+      const unsigned long long tb = static_cast<unsigned long long>(__double_as_longlong(x[k]));
+      __stcs(rec + i, make_uint4(static_cast<uint32_t>(nbr[i]), static_cast<uint32_t>(eid[i]),
+                                 static_cast<uint32_t>(tb), static_cast<uint32_t>(tb >> 32)));
+    }
+  }
+  if (!buckets) return;
   const int64_t v0 = tile_node[blockIdx.x];
   const int64_t v1 = i1 + 1 < m ? tile_node[blockIdx.x + 1] : V - 1;
   if (dir[v0].end > i1) {  // the whole tile lies in one slice (hub slices): no node search
@@ -813,14 +842,15 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
 #pragma unroll
     for (int k = 0; k < kFillPer; ++k) {
       const int64_t i = i0 + k * 256 + threadIdx.x;
-      const double x = i <= i1 ? ts[i] : 0.0;
-      double xp = __shfl_up_sync(0xffffffffu, x, 1);  // every lane runs every iteration
-      if (lane == 0 && i > d.start && i <= i1) xp = ts[i - 1];
-      if (i > i1) continue;
-      const int64_t r = i - d.start;
-      const int64_t jr = bucket_of(x, d.t_first, d.scale, d.nb);
-      const int64_t jp = r ? bucket_of(xp, d.t_first, d.scale, d.nb) : -1;
-      for (int64_t j = jp + 1; j <= jr; ++j) bkt[j] = static_cast<uint32_t>(r);
+      const bool live = i <= i1;
+      const uint32_t jr = live ? bucket_of(x[k], d.t_first, d.scale, d.nb) : 0u;
+      int jp = static_cast<int>(__shfl_up_sync(0xffffffffu, jr, 1));  // every lane, every k
+      if (!live) continue;
+      const uint32_t r = static_cast<uint32_t>(i - d.start);
+      if (lane == 0) jp = r ? static_cast<int>(bucket_of(ts[i - 1], d.t_first, d.scale, d.nb)) : -1;
+      if (r == 0) jp = -1;
+#pragma unroll 1
+      for (int j = jp + 1; j <= static_cast<int>(jr); ++j) bkt[j] = r;
       if (i == d.end - 1) bkt[d.nb] = static_cast<uint32_t>(d.end - d.start);
     }
     return;
@@ -842,10 +872,11 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
     const NodeDir& d = dir[lo - 1];
     if (!d.nb) continue;
     uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
-    const int64_t r = i - d.start;
-    const int64_t jr = bucket_of(ts[i], d.t_first, d.scale, d.nb);
-    const int64_t jp = r ? bucket_of(ts[i - 1], d.t_first, d.scale, d.nb) : -1;
-    for (int64_t j = jp + 1; j <= jr; ++j) bkt[j] = static_cast<uint32_t>(r);
+    const uint32_t r = static_cast<uint32_t>(i - d.start);
+    const int jr = static_cast<int>(bucket_of(x[k], d.t_first, d.scale, d.nb));
+    const int jp = r ? static_cast<int>(bucket_of(ts[i - 1], d.t_first, d.scale, d.nb)) : -1;
+#pragma unroll 1
+    for (int j = jp + 1; j <= jr; ++j) bkt[j] = r;
     if (i == d.end - 1) bkt[d.nb] = static_cast<uint32_t>(d.end - d.start);
   }
 }
@@ -886,6 +917,32 @@ int grid_for(int64_t work, int threads, int per_sm = 8) {
   const int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
   return static_cast<int>(std::min<int64_t>(g, static_cast<int64_t>(device_info().sms) * per_sm));
 }
+
+// gather records (tgfx_graph::rec) unless TGFX_GATHER_REC=0; ids must fit 31 bits
+static bool rec_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_GATHER_REC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static uint4* ensure_rec(tgfx_graph* g, cudaStream_t s) {
+  if (!rec_enabled() || g->m <= 0 || g->other_limit >= (1LL << 31) ||
+      g->eid_limit >= (1LL << 31)) {
+    if (g->rec) dfree(g->rec, s);
+    g->rec = nullptr;
+    g->rec_cap = 0;
+    return nullptr;
+  }
+  if (g->rec_cap < g->m) {
+    if (g->rec) dfree(g->rec, s);
+    g->rec = static_cast<uint4*>(dmalloc(sizeof(uint4) * g->m, s));
+    g->rec_cap = g->m;
+  }
+  return g->rec;
+}
+
 
 size_t scatter_smem(int64_t V) {
   const int64_t vpad = (V + 31) & ~31LL;
@@ -1097,6 +1154,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
   if (use_tile_scatter(V)) {
+    uint4* rec = nullptr;  // (writing the gather records here costs more than a separate pass)
     const size_t tsm = tile_smem_for(V);
     int bits = 1;
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
@@ -1107,18 +1165,18 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
     if (g->reverse)                                                                          \
       k_scatter_tile<2, TT, TE><<<C, TT, tsm, s>>>(d_ev, g->n, V, chunk_ev, passes, cnt,     \
                                                    coldbits, cdelta, img, g->nbr, g->eid,    \
-                                                   g->ts);                                   \
+                                                   g->ts, rec);                              \
     else                                                                                     \
       k_scatter_tile<1, TT, TE><<<C, TT, tsm, s>>>(d_ev, g->n, V, chunk_ev, passes, cnt,     \
                                                    coldbits, cdelta, img, g->nbr, g->eid,    \
-                                                   g->ts);                                   \
+                                                   g->ts, rec);                              \
   }
     TGFX_TILE_SHAPES(X)
 #undef X
     after_launch("k_scatter_tile");
     if (ncold > 0) {
       k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
-                                                                      g->eid, g->ts);
+                                                                      g->eid, g->ts, rec);
       after_launch("k_cold_u");
     }
     return;
@@ -1210,6 +1268,7 @@ void graph_release(tgfx_graph* g) {
   if (g->dflags) dfree(g->dflags, s);
   if (g->dir) dfree(g->dir, s);
   if (g->bkt) dfree(g->bkt, s);
+  if (g->rec) dfree(g->rec, s);
   if (g->ws) dfree(g->ws, s);
   if (g->ws_small) dfree(g->ws_small, s);
   if (g->ws_rec) dfree(g->ws_rec, s);
@@ -1219,6 +1278,8 @@ void graph_release(tgfx_graph* g) {
   g->dir = nullptr;
   g->bkt = nullptr;
   g->bkt_cap = 0;
+  g->rec = nullptr;
+  g->rec_cap = 0;
   g->dflags = nullptr;
   g->hflags = nullptr;
   g->ws = g->ws_small = g->ws_rec = nullptr;
@@ -1287,9 +1348,17 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   if (g->V <= 0) return;
   const int64_t R = g->search_exact ? 0 : bucket_entries();
   const int vb = static_cast<int>(ceil_div(g->V, 256));
+  uint4* rec = ensure_rec(g, s);
+  const int64_t tiles = ceil_div(g->m, kFillTile);
   if (R <= 0) {
     k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr, nullptr);
     after_launch("k_node_dir");
+    if (rec) {
+      k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
+                                                            g->dir, nullptr, g->V, g->m, false,
+                                                            rec);
+      after_launch("k_bucket_fill");
+    }
     return;
   }
   // table size <= sum over slices of (n / R + 2) = m / R + 2V: allocated without a sync
@@ -1301,7 +1370,6 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   }
   uint32_t* cnt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->V, s));
   int64_t* off = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (g->V + 1), s));
-  const int64_t tiles = ceil_div(g->m, kFillTile);
   int32_t* tile_node = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * std::max<int64_t>(tiles, 1), s));
   k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, cnt, tile_node);
   after_launch("k_node_dir");
@@ -1309,8 +1377,9 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   k_node_dir_bkt<<<vb, 256, 0, s>>>(off, g->V, g->bkt, g->dir);
   after_launch("k_node_dir_bkt");
   if (g->m > 0) {
-    k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->ts, g->dir, tile_node,
-                                                          g->V, g->m);
+    k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
+                                                          g->dir, tile_node, g->V, g->m, true,
+                                                          rec);
     after_launch("k_bucket_fill");
   }
   dfree(tile_node, s);

@@ -25,17 +25,17 @@ struct __align__(32) NodeDir {
 };
 
 // bucket of time t in a slice with a bucket table: floor((t - t_first) * scale) clamped to
-// nb - 1.  Monotone non-decreasing in t; the builder and the sampler evaluate this same
-// expression (explicitly rounded, never contracted), which is all exactness needs.
-__host__ __device__ __forceinline__ int64_t bucket_of(double t, double t_first, double scale,
-                                                      int64_t nb) {
+// nb - 1 (nb < 2^32).  Monotone non-decreasing in t; the builder and the sampler evaluate this
+// same expression (explicitly rounded, never contracted), which is all exactness needs.
+__host__ __device__ __forceinline__ uint32_t bucket_of(double t, double t_first, double scale,
+                                                       int64_t nb) {
 #ifdef __CUDA_ARCH__
   const double x = __dmul_rn(__dsub_rn(t, t_first), scale);
 #else
   volatile double dx = t - t_first;
   const double x = dx * scale;
 #endif
-  return x < static_cast<double>(nb - 1) ? static_cast<int64_t>(x) : nb - 1;
+  return x < static_cast<double>(nb - 1) ? static_cast<uint32_t>(x) : static_cast<uint32_t>(nb - 1);
 }
 
 // proj/include/tgformer/tcsr.hpp:20-33 (TCsr), resident on one device.  SoA columns in HBM:
@@ -59,6 +59,10 @@ struct tgfx_graph {
   // time bucket tables of the slices (uint32, ~m / bucket_entries + 2V), see NodeDir
   uint32_t* bkt = nullptr;
   int64_t bkt_cap = 0;
+  // sampler gather records, 16 B per entry {u32 nbr, u32 eid, f64 ts} (ids < 2^31 only):
+  // one 16-byte load per window slot instead of three 8-byte column loads
+  uint4* rec = nullptr;
+  int64_t rec_cap = 0;
   // bound on the other endpoint (nbr ids): V for an ordinary build; the global node count for
   // one node range of a partitioned build (reverse = 0, nbr ids stay global)
   int64_t other_limit = 0;

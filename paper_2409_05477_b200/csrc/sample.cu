@@ -101,6 +101,27 @@ __device__ __forceinline__ void write_vlen(const Outs& o, int64_t q, int64_t v) 
     st<int32_t>(o.vlen, q, static_cast<int32_t>(v));
 }
 
+// one slice entry for the window / sample gathers: from the 16-byte gather record when the
+// graph has them (ids < 2^31, so the widening is exact), else from the three columns
+__device__ __forceinline__ void fetch_entry(const uint4* __restrict__ rec,
+                                            const int64_t* __restrict__ nbr,
+                                            const int64_t* __restrict__ eid,
+                                            const double* __restrict__ ts, int64_t p,
+                                            int64_t& ni, int64_t& ei, double& tv) {
+  if (rec) {
+    uint32_t a, b, c, e;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "l"(rec + p));
+    ni = a;
+    ei = b;
+    tv = __hiloint2double(static_cast<int>(e), static_cast<int>(c));
+  } else {
+    ni = ldg_i64(nbr + p);
+    ei = ldg_i64(eid + p);
+    tv = ldg_f64(ts + p);
+  }
+}
+
 // ------------------------------------------------------------------ recent-k
 // QL queries per lane: their binary searches are interleaved step by step so each lane keeps
 // QL independent loads in flight (the search is a chain of dependent L2/HBM round trips).
@@ -380,11 +401,14 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
 // strided store instructions per lane; l <= kBulkMaxL, int32/fp32 outputs, 16-byte aligned.
 constexpr int kBulkMaxL = 16;
 
-template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false>
+// REC: the window gather reads the graph's 16-byte records (tgfx_graph::rec) instead of the
+// three columns: one 16-byte load per slot
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false, bool REC = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o,
+    const uint4* __restrict__ rec = nullptr) {
   constexpr int GQ = 32 * QL;
   // BULK staging: per warp [3][32 * l] 32-bit words (node, edge, dt)
   extern __shared__ __align__(16) uint32_t s_out[];
@@ -451,9 +475,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
         if (j < kbq) {
           const longlong2 st = s_st[warp][qi];
           const int64_t p = st.x + j;
-          ni = static_cast<uint32_t>(ldg_i64(nbr + p) + 1);
-          ei = static_cast<uint32_t>(ldg_i64(eid + p) + 1);
-          df = __double2float_rn(__longlong_as_double(st.y) - ldg_f64(ts + p));
+          if (REC) {
+            uint32_t a, b, c, e;
+            asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "l"(rec + p));
+            ni = a + 1u;
+            ei = b + 1u;
+            df = __double2float_rn(__longlong_as_double(st.y) -
+                                   __hiloint2double(static_cast<int>(e), static_cast<int>(c)));
+          } else {
+            ni = static_cast<uint32_t>(ldg_i64(nbr + p) + 1);
+            ei = static_cast<uint32_t>(ldg_i64(eid + p) + 1);
+            df = __double2float_rn(__longlong_as_double(st.y) - ldg_f64(ts + p));
+          }
         } else if (j == kbq) {
           ni = static_cast<uint32_t>(s_u[warp][qi] + 1);
           ei = static_cast<uint32_t>(self_idx);
@@ -539,7 +573,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
     const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, int exact,
-    Outs o) {
+    Outs o, const uint4* __restrict__ rec) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ngroups = ceil_div(Q, 32);
   const int kk = static_cast<int>(k);
@@ -592,9 +626,11 @@ __global__ void __launch_bounds__(kThreads) k_random(
             int64_t ni = 0, ei = 0;
             double dt = 0.0;
             if (j < kb) {
-              ni = ldg_i64(nbr + start + j) + 1;
-              ei = ldg_i64(eid + start + j) + 1;
-              dt = qt - ldg_f64(ts + start + j);
+              double tv;
+              fetch_entry(rec, nbr, eid, ts, start + j, ni, ei, tv);
+              ++ni;
+              ++ei;
+              dt = qt - tv;
             } else if (j == kb) {
               ni = qu + 1;
               ei = self_idx;
@@ -657,9 +693,10 @@ __global__ void __launch_bounds__(kThreads) k_random(
         for (int p = 0; p < P; ++p) {
           const int d = p * 32 + lane;
           if (d < kk && rank[p] >= drop) {
-            const int64_t pos = qlo + c[p];
-            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ldg_i64(nbr + pos) + 1,
-                              ldg_i64(eid + pos) + 1, qt - ldg_f64(ts + pos));
+            int64_t ni, ei;
+            double tv;
+            fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
+            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ni + 1, ei + 1, qt - tv);
           }
         }
         for (int j = kb + lane; j < l; j += 32) {
@@ -674,10 +711,12 @@ __global__ void __launch_bounds__(kThreads) k_random(
         for (int p = 0; p < P; ++p) {
           const int d = p * 32 + lane;
           if (d < kk) {
-            const int64_t pos = qlo + c[p];
-            o.e_nbr[qq * k + rank[p]] = ldg_i64(nbr + pos);
-            o.e_eid[qq * k + rank[p]] = ldg_i64(eid + pos);
-            o.e_ts[qq * k + rank[p]] = ldg_f64(ts + pos);
+            int64_t ni, ei;
+            double tv;
+            fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
+            o.e_nbr[qq * k + rank[p]] = ni;
+            o.e_eid[qq * k + rank[p]] = ei;
+            o.e_ts[qq * k + rank[p]] = tv;
           }
         }
         if (lane == 0) o.counts[qq] = kk;
@@ -772,7 +811,8 @@ template <int P, bool ASSEMBLE, bool IDX64>
 __global__ void __launch_bounds__(kThreads) k_random_g(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, Outs o,
+    const uint4* __restrict__ rec) {
   constexpr int G = 8;                      // lanes per query
   constexpr int NG = 32 / G;                // queries per warp round
   __shared__ int64_t s_lo[kWarps][32], s_m[kWarps][32], s_u[kWarps][32];
@@ -862,9 +902,11 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
             int64_t ni = 0, ei = 0;
             double dt = 0.0;
             if (j < kb) {
-              ni = ldg_i64(nbr + start + j) + 1;
-              ei = ldg_i64(eid + start + j) + 1;
-              dt = qt - ldg_f64(ts + start + j);
+              double tv;
+              fetch_entry(rec, nbr, eid, ts, start + j, ni, ei, tv);
+              ++ni;
+              ++ei;
+              dt = qt - tv;
             } else if (j == kb) {
               ni = qu + 1;
               ei = self_idx;
@@ -880,9 +922,10 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
         for (int p = 0; p < P; ++p) {
           const int dd = p * G + r;
           if (dd < kk && rank[p] >= drop) {
-            const int64_t pos = qlo + c[p];
-            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ldg_i64(nbr + pos) + 1,
-                              ldg_i64(eid + pos) + 1, qt - ldg_f64(ts + pos));
+            int64_t ni, ei;
+            double tv;
+            fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
+            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ni + 1, ei + 1, qt - tv);
           }
         }
         for (int j = kb + r; j < l; j += G)
@@ -904,10 +947,12 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
         for (int p = 0; p < P; ++p) {
           const int dd = p * G + r;
           if (dd < kk) {
-            const int64_t pos = qlo + c[p];
-            o.e_nbr[qq * k + rank[p]] = ldg_i64(nbr + pos);
-            o.e_eid[qq * k + rank[p]] = ldg_i64(eid + pos);
-            o.e_ts[qq * k + rank[p]] = ldg_f64(ts + pos);
+            int64_t ni, ei;
+            double tv;
+            fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
+            o.e_nbr[qq * k + rank[p]] = ni;
+            o.e_eid[qq * k + rank[p]] = ei;
+            o.e_ts[qq * k + rank[p]] = tv;
           }
         }
         if (r == 0) o.counts[qq] = kk;
@@ -925,7 +970,7 @@ void launch_random_g(const SampleArgs& a, const QueryIn& in, const Outs& o, int 
 #define TGFX_RANDOM_G(PP)                                                                      \
   k_random_g<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, \
                                                      l, a.self_edge_index, a.seed,             \
-                                                     a.stream_base, o);
+                                                     a.stream_base, o, g->rec);
   if (a.k <= 8)
     TGFX_RANDOM_G(1)
   else if (a.k <= 16)
@@ -945,7 +990,8 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
   case PP:                                                                                   \
     k_random<PP, ASM, I64><<<grid, kThreads, 0, s>>>(g->indptr, g->dir, g->nbr, g->eid, g->ts, in, a.q, \
                                                      a.k, l, a.self_edge_index, a.seed,      \
-                                                     a.stream_base, g->search_exact, o);    \
+                                                     a.stream_base, g->search_exact, o,     \
+                                                     g->rec);                               \
     break;
   switch (P) {
     TGFX_RANDOM_CASE(1)
@@ -997,6 +1043,12 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                       bulk_enabled();
     if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
       const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
+      if (g->rec) {
+        k_recent_line<true, false, 8, 1, 4, true, true><<<gq, kThreads, sm, s>>>(
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o, g->rec);
+        after_launch("k_recent_line");
+        return;
+      }
       k_recent_line<true, false, 8, 1, 4, true><<<gq, kThreads, sm, s>>>(
             g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
       after_launch("k_recent_line");
