@@ -109,6 +109,25 @@ __device__ __forceinline__ void fetch_entry(const uint4* __restrict__ rec,
                                             const double* __restrict__ ts, int64_t p,
                                             int64_t& ni, int64_t& ei, double& tv) {
   if (rec) {
+    const uint4 r = __ldg(rec + p);
+    ni = r.x;
+    ei = r.y;
+    tv = __hiloint2double(static_cast<int>(r.w), static_cast<int>(r.z));
+  } else {
+    ni = ldg_i64(nbr + p);
+    ei = ldg_i64(eid + p);
+    tv = ldg_f64(ts + p);
+  }
+}
+
+// the same as fetch_entry, as volatile asm: the loads stay where they are written (issued
+// together ahead of their uses) instead of being sunk into the uses' branches
+__device__ __forceinline__ void fetch_entry_v(const uint4* __restrict__ rec,
+                                              const int64_t* __restrict__ nbr,
+                                              const int64_t* __restrict__ eid,
+                                              const double* __restrict__ ts, int64_t p,
+                                              int64_t& ni, int64_t& ei, double& tv) {
+  if (rec) {
     uint32_t a, b, c, e;
     asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "l"(rec + p));
@@ -116,10 +135,43 @@ __device__ __forceinline__ void fetch_entry(const uint4* __restrict__ rec,
     ei = b;
     tv = __hiloint2double(static_cast<int>(e), static_cast<int>(c));
   } else {
-    ni = ldg_i64(nbr + p);
-    ei = ldg_i64(eid + p);
-    tv = ldg_f64(ts + p);
+    long long a, b;
+    asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(a) : "l"(nbr + p));
+    asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(b) : "l"(eid + p));
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(tv) : "l"(ts + p));
+    ni = a;
+    ei = b;
   }
+}
+
+// write_slot under a predicate, as predicated stores (no branch for ptxas to sink loads into)
+template <bool IDX64>
+__device__ __forceinline__ void write_slot_if(const Outs& o, int64_t i, int64_t ni, int64_t ei,
+                                              double dt, bool pred) {
+  const int pi = pred ? 1 : 0;
+  if (IDX64) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.s64 [%0], %1;\n\t}"
+                 ::"l"(reinterpret_cast<long long*>(o.node) + i), "l"(static_cast<long long>(ni)), "r"(pi)
+                 : "memory");
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.s64 [%0], %1;\n\t}"
+                 ::"l"(reinterpret_cast<long long*>(o.edge) + i), "l"(static_cast<long long>(ei)), "r"(pi)
+                 : "memory");
+  } else {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.s32 [%0], %1;\n\t}"
+                 ::"l"(static_cast<int*>(o.node) + i), "r"(static_cast<int>(ni)), "r"(pi)
+                 : "memory");
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.s32 [%0], %1;\n\t}"
+                 ::"l"(static_cast<int*>(o.edge) + i), "r"(static_cast<int>(ei)), "r"(pi)
+                 : "memory");
+  }
+  if (o.dt32)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
+                 ::"l"(o.dt32 + i), "f"(__double2float_rn(dt)), "r"(pi)
+                 : "memory");
+  if (o.dt64)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f64 [%0], %1;\n\t}"
+                 ::"l"(o.dt64 + i), "d"(dt), "r"(pi)
+                 : "memory");
 }
 
 // ------------------------------------------------------------------ recent-k
@@ -403,7 +455,8 @@ constexpr int kBulkMaxL = 16;
 
 // REC: the window gather reads the graph's 16-byte records (tgfx_graph::rec) instead of the
 // three columns: one 16-byte load per slot
-template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false, bool REC = false>
+template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false, bool REC = false,
+          int UNR = 4>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
@@ -464,42 +517,58 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     int j = lane - qi * width;
     const int dq = div_slot(32, width, magic), dj = 32 - dq * width;
     if (BULK && nq == GQ) {
-      uint32_t* sn = s_out + static_cast<size_t>(warp) * 3 * GQ * l;
-      uint32_t* se = sn + GQ * l;
-      float* sd = reinterpret_cast<float*>(se + GQ * l);
-#pragma unroll 4
-      for (int s = lane; s < total; s += 32) {
-        const int kbq = s_kb[warp][qi];
-        uint32_t ni = 0, ei = 0;
-        float df = 0.0f;
-        if (j < kbq) {
+      // staging arrays padded to lp = l rounded up to UNR slots per lane: phase B stores every
+      // slot of a chunk unconditionally (a conditional store lets ptxas sink its load into the
+      // branch, which serialises the chunk's loads again); the padding is never copied out
+      const int lp = (l + UNR - 1) / UNR * UNR;
+      uint32_t* sn = s_out + static_cast<size_t>(warp) * 3 * GQ * lp;
+      uint32_t* se = sn + GQ * lp;
+      float* sd = reinterpret_cast<float*>(se + GQ * lp);
+      // each lane fills slots s = lane + 32 it, it < l, in chunks of UNR: all of a chunk's
+      // loads are issued (phase A) before any result is stored (phase B) -- the compiler will
+      // not hoist a slot's loads above the previous slot's shared-memory stores by itself
+      for (int it0 = 0; it0 < l; it0 += UNR) {
+        uint32_t rn[UNR], re[UNR];
+        double tv[UNR], tq[UNR];
+        uint32_t sf[UNR];  // self-slot node id + 1, or 0
+        bool tk[UNR];
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const bool valid = it0 + uu < l;
+          const int kbq = s_kb[warp][qi];
           const longlong2 st = s_st[warp][qi];
-          const int64_t p = st.x + j;
+          tk[uu] = valid && j < kbq;
+          sf[uu] = (valid && j == kbq) ? static_cast<uint32_t>(s_u[warp][qi] + 1) : 0u;
+          tq[uu] = __longlong_as_double(st.y);
+          const int64_t p = tk[uu] ? st.x + j : 0;
+          // volatile: keeps the loads here, unconditional, instead of sunk into phase B's
+          // per-slot branches (which would serialise them again)
           if (REC) {
-            uint32_t a, b, c, e;
-            asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(a), "=r"(b), "=r"(c), "=r"(e) : "l"(rec + p));
-            ni = a + 1u;
-            ei = b + 1u;
-            df = __double2float_rn(__longlong_as_double(st.y) -
-                                   __hiloint2double(static_cast<int>(e), static_cast<int>(c)));
+            uint32_t c, e;
+            asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(rn[uu]), "=r"(re[uu]), "=r"(c), "=r"(e) : "l"(rec + p));
+            tv[uu] = __hiloint2double(static_cast<int>(e), static_cast<int>(c));
           } else {
-            ni = static_cast<uint32_t>(ldg_i64(nbr + p) + 1);
-            ei = static_cast<uint32_t>(ldg_i64(eid + p) + 1);
-            df = __double2float_rn(__longlong_as_double(st.y) - ldg_f64(ts + p));
+            unsigned long long a, b;
+            asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(a) : "l"(nbr + p));
+            asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(b) : "l"(eid + p));
+            asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(tv[uu]) : "l"(ts + p));
+            rn[uu] = static_cast<uint32_t>(a);
+            re[uu] = static_cast<uint32_t>(b);
           }
-        } else if (j == kbq) {
-          ni = static_cast<uint32_t>(s_u[warp][qi] + 1);
-          ei = static_cast<uint32_t>(self_idx);
+          j += dj;
+          qi += dq;
+          if (j >= width) {
+            j -= width;
+            ++qi;
+          }
         }
-        sn[s] = ni;
-        se[s] = ei;
-        sd[s] = df;
-        j += dj;
-        qi += dq;
-        if (j >= width) {
-          j -= width;
-          ++qi;
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int s = lane + 32 * (it0 + uu);
+          sn[s] = tk[uu] ? rn[uu] + 1u : sf[uu];
+          se[s] = tk[uu] ? re[uu] + 1u : (sf[uu] ? static_cast<uint32_t>(self_idx) : 0u);
+          sd[s] = tk[uu] ? __double2float_rn(tq[uu] - tv[uu]) : 0.0f;
         }
       }
       __syncwarp();
@@ -528,32 +597,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
 #pragma unroll 4
     for (int s = lane; s < total; s += 32) {
       const int kbq = s_kb[warp][qi];
+      const longlong2 st = s_st[warp][qi];
+      const bool take = j < kbq;
+      int64_t ni, ei;
+      double tv;
+      fetch_entry(rec, nbr, eid, ts, take ? st.x + j : 0, ni, ei, tv);  // branch-free loads
       if (ASSEMBLE) {
-        int64_t ni = 0, ei = 0;
-        double dt = 0.0;
-        if (j < kbq) {
-          const longlong2 st = s_st[warp][qi];
-          const int64_t p = st.x + j;
-          ni = ldg_i64(nbr + p) + 1;
-          ei = ldg_i64(eid + p) + 1;
-          dt = __longlong_as_double(st.y) - ldg_f64(ts + p);
-        } else if (j == kbq) {
-          ni = s_u[warp][qi] + 1;
-          ei = self_idx;
-        }
-        write_slot<IDX64>(o, obase + s, ni, ei, dt);
+        const bool self = j == kbq;
+        const int64_t su = s_u[warp][qi];
+        write_slot<IDX64>(o, obase + s, take ? ni + 1 : self ? su + 1 : 0,
+                          take ? ei + 1 : self ? self_idx : 0,
+                          take ? __longlong_as_double(st.y) - tv : 0.0);
       } else {
-        int64_t a = 0, b = 0;
-        double c = 0.0;
-        if (j < kbq) {
-          const int64_t p = s_st[warp][qi].x + j;
-          a = ldg_i64(nbr + p);
-          b = ldg_i64(eid + p);
-          c = ldg_f64(ts + p);
-        }
-        o.e_nbr[obase + s] = a;
-        o.e_eid[obase + s] = b;
-        o.e_ts[obase + s] = c;
+        o.e_nbr[obase + s] = take ? ni : 0;
+        o.e_eid[obase + s] = take ? ei : 0;
+        o.e_ts[obase + s] = take ? tv : 0.0;
       }
       j += dj;
       qi += dq;
@@ -918,16 +976,21 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
         }
         const int kb = min(kk, l - 1);
         const int drop = kk - kb;  // keep the most recent l-1 (sequence.cpp:70-71)
+        // all P samples' loads first (an unused one reads the slice's first entry), then
+        // predicated stores: the loads are in flight together
+        int64_t ni[P], ei[P];
+        double tv[P];
+        bool use[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const int dd = p * G + r;
-          if (dd < kk && rank[p] >= drop) {
-            int64_t ni, ei;
-            double tv;
-            fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
-            write_slot<IDX64>(o, qq * l + (rank[p] - drop), ni + 1, ei + 1, qt - tv);
-          }
+          use[p] = dd < kk && rank[p] >= drop;
+          fetch_entry_v(rec, nbr, eid, ts, qlo + (use[p] ? c[p] : 0), ni[p], ei[p], tv[p]);
         }
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          write_slot_if<IDX64>(o, qq * l + (use[p] ? rank[p] - drop : 0), ni[p] + 1, ei[p] + 1,
+                               qt - tv[p], use[p]);
         for (int j = kb + r; j < l; j += G)
           write_slot<IDX64>(o, qq * l + j, j == kb ? qu + 1 : 0, j == kb ? self_idx : 0, 0.0);
         if (r == 0) write_vlen<IDX64>(o, qq, kb + 1);
@@ -1042,28 +1105,40 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                         reinterpret_cast<uintptr_t>(a.dt32)) & 15) == 0 &&
                       bulk_enabled();
     if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
-      const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
       if (g->rec) {
-        k_recent_line<true, false, 8, 1, 4, true, true><<<gq, kThreads, sm, s>>>(
-            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o, g->rec);
+#define TGFX_BULK_LAUNCH(REC, U)                                                               \
+  do {                                                                                         \
+    const auto kern = k_recent_line<true, false, 8, 1, 4, true, REC, U>;                       \
+    static const bool attr = [&] {                                                             \
+      TGFX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                     kWarps * 3 * 32 * ((kBulkMaxL + U - 1) / U * U) * 4));    \
+      return true;                                                                             \
+    }();                                                                                       \
+    (void)attr;                                                                                \
+    const size_t smu = static_cast<size_t>(kWarps) * 3 * 32 * ((l + U - 1) / U * U) * 4;       \
+    kern<<<gq, kThreads, smu, s>>>(g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l,             \
+                                   a.self_edge_index, magic, o, g->rec);                       \
+  } while (0)
+        // 2 slots per lane per load round (measured: 35.8 ms/step vs 37.6 for 4, 38.2 for 1)
+        TGFX_BULK_LAUNCH(true, 2);
         after_launch("k_recent_line");
         return;
       }
-      k_recent_line<true, false, 8, 1, 4, true><<<gq, kThreads, sm, s>>>(
-            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+      TGFX_BULK_LAUNCH(false, 2);
+#undef TGFX_BULK_LAUNCH
       after_launch("k_recent_line");
       return;
     }
     if (!g->search_exact) {  // line probes through the node directory
       if (assemble && a.index64)
         k_recent_line<true, true, 8, 1, 4><<<gq, kThreads, 0, s>>>(
-            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o, g->rec);
       else if (assemble)
         k_recent_line<true, false, 8, 1, 4><<<gq, kThreads, 0, s>>>(
-            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o);
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, magic, o, g->rec);
       else
         k_recent_line<false, false, 8, 1, 4><<<gq, kThreads, 0, s>>>(
-            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o);
+            g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, 0, 0, magic, o, g->rec);
       after_launch("k_recent_line");
       return;
     }
