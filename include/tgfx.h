@@ -104,6 +104,9 @@ int tgfx_graph_info(const tgfx_graph* g, int64_t* num_nodes, int64_t* num_edges,
 /* copy the T-CSR columns to host: indptr[num_nodes+1], nbr/eid/ts[num_entries] */
 int tgfx_graph_export(const tgfx_graph* g, int64_t* indptr, int64_t* nbr, int64_t* eid,
                       double* ts);
+/* device pointers of the columns.  A build may leave nbr / eid unwritten (the sampler reads
+ * 16-byte gather records instead); asking for them materialises them first, and they stay
+ * valid until the next tgfx_rebuild_device of g -- ask again after a rebuild. */
 int tgfx_graph_device_arrays(const tgfx_graph* g, const int64_t** indptr, const int64_t** nbr,
                              const int64_t** eid, const double** ts);
 /* replaces TCsr::validate (tcsr.cpp:54-81), run on the device */

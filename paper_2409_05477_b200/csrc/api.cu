@@ -414,6 +414,7 @@ int tgfx_graph_export(const tgfx_graph* g, int64_t* indptr, int64_t* nbr, int64_
   return guarded([&] {
     check_graph(g);
     cudaStream_t s = 0;
+    ensure_columns(g, s);
     d2h(indptr, g->indptr, sizeof(int64_t) * (g->V + 1), s);
     d2h(nbr, g->nbr, sizeof(int64_t) * g->m, s);
     d2h(eid, g->eid, sizeof(int64_t) * g->m, s);
@@ -426,6 +427,10 @@ int tgfx_graph_device_arrays(const tgfx_graph* g, const int64_t** indptr, const 
                              const int64_t** eid, const double** ts) {
   return guarded([&] {
     check_graph(g);
+    if (nbr || eid) {
+      ensure_columns(g, 0);
+      TGFX_CUDA(cudaStreamSynchronize(0));
+    }
     if (indptr) *indptr = g->indptr;
     if (nbr) *nbr = g->nbr;
     if (eid) *eid = g->eid;

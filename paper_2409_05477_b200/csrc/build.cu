@@ -608,13 +608,15 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
         rec[0] = make_ulonglong2(static_cast<unsigned long long>(other), static_cast<unsigned long long>(a.x));
         rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u[k]));
       } else {
-        nbr_out[pos[k]] = other;
-        eid_out[pos[k]] = a.x;
         ts_out[pos[k]] = __longlong_as_double(b.y);
-        if (rec_out)
+        if (rec_out) {  // gather record instead of the int64 columns (widened on demand)
           rec_out[pos[k]] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
                                        static_cast<uint32_t>(b.y),
                                        static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
+        } else {
+          nbr_out[pos[k]] = other;
+          eid_out[pos[k]] = a.x;
+        }
       }
     }
     __syncthreads();  // stage buffer consumed, cursors final for this tile
@@ -657,12 +659,14 @@ __global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ i
     const ulonglong2 a = __ldg(img + 2 * i);
     const ulonglong2 b = __ldg(img + 2 * i + 1);
     const int64_t pos = i - __ldg(reinterpret_cast<const long long*>(cdelta) + b.y);
-    nbr_out[pos] = static_cast<int64_t>(a.x);
-    eid_out[pos] = static_cast<int64_t>(a.y);
     ts_out[pos] = __longlong_as_double(static_cast<long long>(b.x));
-    if (rec_out)
+    if (rec_out) {
       rec_out[pos] = make_uint4(static_cast<uint32_t>(a.x), static_cast<uint32_t>(a.y),
                                 static_cast<uint32_t>(b.x), static_cast<uint32_t>(b.x >> 32));
+    } else {
+      nbr_out[pos] = static_cast<int64_t>(a.x);
+      eid_out[pos] = static_cast<int64_t>(a.y);
+    }
   }
 }
 
@@ -1154,7 +1158,10 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   if (g->n == 0) return;
   if (use_tile_scatter(V)) {
-    uint4* rec = nullptr;  // (writing the gather records here costs more than a separate pass)
+    // with gather records the scatter writes {rec, ts} instead of {nbr, eid, ts}; the int64
+    // columns are widened from the records when something asks for them (ensure_columns)
+    uint4* rec = ensure_rec(g, s);
+    g->cols_valid = rec == nullptr;
     const size_t tsm = tile_smem_for(V);
     int bits = 1;
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
@@ -1286,6 +1293,7 @@ void graph_release(tgfx_graph* g) {
 }
 
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted) {
+  g->cols_valid = true;  // every path writes the columns, except the tile scatter with records
   (void)trusted;
   const int64_t n = g->n, V = g->V;
   const int R = g->reverse ? 2 : 1;
@@ -1335,6 +1343,27 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   build_node_dir(g, s);
 }
 
+__global__ void __launch_bounds__(256) k_widen(const uint4* __restrict__ rec, int64_t m,
+                                               int64_t* __restrict__ nbr,
+                                               int64_t* __restrict__ eid) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 r = __ldg(rec + i);
+    nbr[i] = static_cast<int64_t>(r.x);
+    eid[i] = static_cast<int64_t>(r.y);
+  }
+}
+
+void ensure_columns(const tgfx_graph* cg, cudaStream_t s) {
+  tgfx_graph* g = const_cast<tgfx_graph*>(cg);
+  if (g->cols_valid) return;
+  if (g->m > 0) {
+    k_widen<<<grid_for(g->m, 256), 256, 0, s>>>(g->rec, g->m, g->nbr, g->eid);
+    after_launch("k_widen");
+  }
+  g->cols_valid = true;
+}
+
 // entries per time bucket (TGFX_BUCKET_ENTRIES, default 8; 0 disables the tables)
 static int64_t bucket_entries() {
   static const int64_t r = [] {
@@ -1348,7 +1377,8 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   if (g->V <= 0) return;
   const int64_t R = g->search_exact ? 0 : bucket_entries();
   const int vb = static_cast<int>(ceil_div(g->V, 256));
-  uint4* rec = ensure_rec(g, s);
+  // gather records from the columns, unless the build's scatter already wrote them
+  uint4* rec = g->cols_valid ? ensure_rec(g, s) : nullptr;
   const int64_t tiles = ceil_div(g->m, kFillTile);
   if (R <= 0) {
     k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr, nullptr);
@@ -1388,6 +1418,7 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
 }
 
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {
+  ensure_columns(g, s);
   int* err = static_cast<int*>(dmalloc(sizeof(int), s));
   const int big = 1 << 30;
   TGFX_CUDA(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, s));

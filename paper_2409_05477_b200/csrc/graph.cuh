@@ -63,6 +63,9 @@ struct tgfx_graph {
   // one 16-byte load per window slot instead of three 8-byte column loads
   uint4* rec = nullptr;
   int64_t rec_cap = 0;
+  // false: the last build wrote rec (+ ts) instead of the int64 nbr / eid columns; they are
+  // widened from rec by ensure_columns before anything outside the sampler reads them
+  bool cols_valid = true;
   // bound on the other endpoint (nbr ids): V for an ordinary build; the global node count for
   // one node range of a partitioned build (reverse = 0, nbr ids stay global)
   int64_t other_limit = 0;
@@ -103,6 +106,9 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s);
 
 // Full build into g from device events; throws tgfx::Error on invalid input.
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted);
+
+// Materialises the int64 nbr / eid columns from the gather records if the build skipped them.
+void ensure_columns(const tgfx_graph* g, cudaStream_t s);
 
 // TCsr::validate on device (tcsr.cpp:54-81); returns empty string if valid.
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s);

@@ -216,7 +216,7 @@ template <bool ASSEMBLE, bool IDX64, int QL, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent(
     const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
-    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o) {
+    int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o, const uint4* __restrict__ rec) {
   constexpr int GQ = 32 * QL;  // queries per warp group
   __shared__ int64_t s_start[kWarps][GQ];
   __shared__ int64_t s_u[kWarps][GQ];
@@ -277,10 +277,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
         int64_t ni = 0, ei = 0;
         double dt = 0.0;
         if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
-          ni = ldg_i64(nbr + p) + 1;
-          ei = ldg_i64(eid + p) + 1;
-          dt = s_t[warp][qi] - ldg_f64(ts + p);
+          double tv;
+          fetch_entry(rec, nbr, eid, ts, s_start[warp][qi] + j, ni, ei, tv);
+          ++ni;
+          ++ei;
+          dt = s_t[warp][qi] - tv;
         } else if (j == kbq) {
           ni = s_u[warp][qi] + 1;
           ei = self_idx;
@@ -289,12 +290,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
       } else {
         int64_t a = 0, b = 0;
         double c = 0.0;
-        if (j < kbq) {
-          const int64_t p = s_start[warp][qi] + j;
-          a = ldg_i64(nbr + p);
-          b = ldg_i64(eid + p);
-          c = ldg_f64(ts + p);
-        }
+        if (j < kbq) fetch_entry(rec, nbr, eid, ts, s_start[warp][qi] + j, a, b, c);
         o.e_nbr[obase + s] = a;
         o.e_eid[obase + s] = b;
         o.e_ts[obase + s] = c;
@@ -699,9 +695,12 @@ __global__ void __launch_bounds__(kThreads) k_random(
         } else {
           for (int j = lane; j < kk; j += 32) {
             const bool h = j < qm;
-            o.e_nbr[qq * k + j] = h ? ldg_i64(nbr + qlo + j) : 0;
-            o.e_eid[qq * k + j] = h ? ldg_i64(eid + qlo + j) : 0;
-            o.e_ts[qq * k + j] = h ? ldg_f64(ts + qlo + j) : 0.0;
+            int64_t a = 0, b = 0;
+            double c = 0.0;
+            if (h) fetch_entry(rec, nbr, eid, ts, qlo + j, a, b, c);
+            o.e_nbr[qq * k + j] = a;
+            o.e_eid[qq * k + j] = b;
+            o.e_ts[qq * k + j] = c;
           }
           if (lane == 0) o.counts[qq] = qm;
         }
@@ -999,9 +998,12 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
           const int64_t take = pr ? qm : 0;
           for (int j = r; j < kk; j += G) {
             const bool h = j < take;
-            o.e_nbr[qq * k + j] = h ? ldg_i64(nbr + qlo + j) : 0;
-            o.e_eid[qq * k + j] = h ? ldg_i64(eid + qlo + j) : 0;
-            o.e_ts[qq * k + j] = h ? ldg_f64(ts + qlo + j) : 0.0;
+            int64_t a = 0, b = 0;
+            double c = 0.0;
+            if (h) fetch_entry(rec, nbr, eid, ts, qlo + j, a, b, c);
+            o.e_nbr[qq * k + j] = a;
+            o.e_eid[qq * k + j] = b;
+            o.e_ts[qq * k + j] = c;
           }
           if (r == 0) o.counts[qq] = take;
           continue;
@@ -1147,13 +1149,15 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
         std::min<int64_t>(ceil_div(ceil_div(a.q, 32 * 4), kWarps), INT32_MAX));
     if (assemble && a.index64)
       k_recent<true, true, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
-                                                          a.q, a.k, l, a.self_edge_index, magic, o);
+                                                          a.q, a.k, l, a.self_edge_index, magic, o,
+                                                          g->rec);
     else if (assemble)
       k_recent<true, false, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
-                                                           a.q, a.k, l, a.self_edge_index, magic, o);
+                                                           a.q, a.k, l, a.self_edge_index, magic, o,
+                                                           g->rec);
     else
       k_recent<false, false, 4, 3><<<gb, kThreads, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, in,
-                                                            a.q, a.k, 0, 0, magic, o);
+                                                            a.q, a.k, 0, 0, magic, o, g->rec);
     after_launch("k_recent");
     return;
   }

@@ -63,7 +63,8 @@ def rebuild(g, ev, trusted=True, stream=None):
 
 
 def graph_tensors(g):
-    """Zero-copy torch views (indptr, nbr, eid, ts) of the device T-CSR."""
+    """Zero-copy torch views (indptr, nbr, eid, ts) of the device T-CSR (nbr / eid are
+    materialised from the gather records on first request; call again after a rebuild)."""
     ip, nb, ed, ts = g.device_arrays()
     m = g.num_entries()
     mk = lambda p, n, t, dt: torch.as_tensor(_CAI(p, n, t, g), device="cuda")  # noqa: E731
