@@ -493,21 +493,12 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
       int rank[KPT];
       uint32_t dig[KPT];
       unsigned peers[KPT];
-      // lanes with the same 8-bit digit: intersect the 8 bit-plane ballots (fixed cost,
-      // unlike MATCH whose latency grows with the number of distinct values); all keys'
-      // ballots first, so the chains interleave, then the counter updates in key order
+      // lanes with the same 8-bit digit: one MATCH.ANY per key (measured faster here than
+      // intersecting 8 bit-plane ballots: build 11.4 vs 11.9 ms on the GDELT shape)
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         dig[k] = (key[k] >> shift) & 0xffu;
-        peers[k] = kFull;
-      }
-#pragma unroll
-      for (int bit = 0; bit < 8; ++bit) {
-#pragma unroll
-        for (int k = 0; k < KPT; ++k) {
-          const unsigned m = __ballot_sync(kFull, (dig[k] >> bit) & 1u);
-          peers[k] &= ((dig[k] >> bit) & 1u) ? m : ~m;
-        }
+        peers[k] = __match_any_sync(kFull, dig[k]);
       }
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
@@ -536,8 +527,9 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
         }
         if (lane == 31) scr[warp] = static_cast<int>(x);
         __syncthreads();
-        uint32_t before = 0;  // totals of the earlier warps, summed redundantly per warp
-        for (int w = 0; w < warp; ++w) before += static_cast<uint32_t>(scr[w]);
+        // totals of the earlier warps: lane w < warp reads scr[w], one warp reduction
+        const uint32_t before = __reduce_add_sync(
+            kFull, lane < warp ? static_cast<uint32_t>(scr[lane]) : 0u);
         uint32_t run = before + x - s;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -579,8 +571,8 @@ __global__ void __launch_bounds__(kTT) k_scatter_tile(
       }
       if (lane == 31) scr[warp] = carry;
       __syncthreads();
-      int prev = 0;
-      for (int w = 0; w < warp; ++w) prev = max(prev, scr[w]);
+      const int prev = static_cast<int>(
+          __reduce_max_sync(kFull, lane < warp ? static_cast<unsigned>(scr[lane]) : 0u));
 #pragma unroll
       for (int k = 0; k < KPT; ++k) hp[k] = max(hp[k], prev);
     }
@@ -776,13 +768,10 @@ constexpr int64_t kFillTile = 256 * kFillPer;
 
 __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __restrict__ ts,
                            int64_t V, int64_t R, NodeDir* __restrict__ dir,
-                           uint32_t* __restrict__ cnt, int32_t* __restrict__ tile_node) {
+                           uint32_t* __restrict__ cnt) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= V) return;
   const int64_t a = indptr[u], b = indptr[u + 1];
-  if (tile_node)  // the node holding the first entry of each k_bucket_fill tile
-    for (int64_t t = ceil_div(a, kFillTile); t * kFillTile < b; ++t)
-      tile_node[t] = static_cast<int32_t>(u);
   NodeDir d;
   d.start = a;
   d.end = b;
@@ -794,6 +783,25 @@ __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __r
   d.width = d.nb ? (d.t_last - d.t_first) / static_cast<double>(d.nb) : 0.0;
   dir[u] = d;
   if (cnt) cnt[u] = d.nb ? static_cast<uint32_t>(d.nb + 1) : 0u;
+}
+
+// the node holding the first entry of each k_bucket_fill tile: last u with indptr[u] <= t * tile
+__global__ void k_tile_node(const int64_t* __restrict__ indptr, int64_t V, int64_t tiles,
+                            int32_t* __restrict__ tile_node) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= tiles) return;
+  const int64_t i = t * kFillTile;
+  int64_t lo = 0, n = V + 1;  // upper_bound over indptr[0..V]
+  while (n > 0) {
+    const int64_t h = n >> 1;
+    if (__ldg(reinterpret_cast<const long long*>(indptr) + lo + h) <= i) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  tile_node[t] = static_cast<int32_t>(lo - 1);
 }
 
 // pass 2: bucket table offsets (exclusive scan of the sizes) -> pointers
@@ -1381,7 +1389,7 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   uint4* rec = g->cols_valid ? ensure_rec(g, s) : nullptr;
   const int64_t tiles = ceil_div(g->m, kFillTile);
   if (R <= 0) {
-    k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr, nullptr);
+    k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr);
     after_launch("k_node_dir");
     if (rec) {
       k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
@@ -1401,8 +1409,13 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   uint32_t* cnt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->V, s));
   int64_t* off = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (g->V + 1), s));
   int32_t* tile_node = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * std::max<int64_t>(tiles, 1), s));
-  k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, cnt, tile_node);
+  k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, cnt);
   after_launch("k_node_dir");
+  if (tiles > 0) {
+    k_tile_node<<<static_cast<int>(ceil_div(tiles, 256)), 256, 0, s>>>(g->indptr, g->V, tiles,
+                                                                        tile_node);
+    after_launch("k_tile_node");
+  }
   scan_u32_to_i64(cnt, g->V, off, s);
   k_node_dir_bkt<<<vb, 256, 0, s>>>(off, g->V, g->bkt, g->dir);
   after_launch("k_node_dir_bkt");
