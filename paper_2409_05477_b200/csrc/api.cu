@@ -1,3 +1,5 @@
+#include <chrono>
+#include <cstdio>
 // api.cu -- the extern "C" boundary (include/tgfx.h): argument checks with the reference's
 // error texts, host<->device staging for the synchronous host-buffer calls, and the
 // process-wide runtime bits (thread-local error, launch counter, stream-ordered pool).
@@ -172,11 +174,26 @@ tgfx_graph* new_graph(int64_t n, int64_t V, int reverse, cudaStream_t s) {
   return g;
 }
 
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void free_graph(tgfx_graph* g) {
   if (!g) return;
+  const double t0 = now_ms();
   g_bytes.fetch_sub(static_cast<int64_t>(sizeof(int64_t) * (g->V + 1) + 24 * g->m));
   graph_release(g);
   delete g;
+  if (trace_on()) fprintf(stderr, "[tgfx] free_graph: %.1f ms\n", now_ms() - t0);
 }
 
 int build_host(const tgfx_event* events, int64_t n, int64_t V, int reverse, tgfx_graph** out) {
@@ -186,12 +203,20 @@ int build_host(const tgfx_event* events, int64_t n, int64_t V, int reverse, tgfx
     *out = nullptr;
     cudaStream_t s = 0;
     device_info();
+    const double t0 = now_ms();
     DBuf dev(sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 1)), s);
     h2d(dev.p, events, sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 0)), s);
+    if (trace_on()) TGFX_CUDA(cudaStreamSynchronize(s));
+    const double t1 = now_ms();
     g = new_graph(n, V, reverse, s);
+    if (trace_on()) TGFX_CUDA(cudaStreamSynchronize(s));
+    const double t2 = now_ms();
     try {
       build_graph(g, dev.as<tgfx_event>(), s, false);
       TGFX_CUDA(cudaStreamSynchronize(s));
+      if (trace_on())
+        fprintf(stderr, "[tgfx] build_host: upload %.1f ms, alloc %.1f ms, build %.1f ms\n",
+                t1 - t0, t2 - t1, now_ms() - t2);
     } catch (...) {
       free_graph(g);
       throw;

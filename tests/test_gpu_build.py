@@ -160,3 +160,34 @@ def test_permuted_ids_and_reverse_settings(T, oracle_mod):
         ev["dst"] = perm[ev["dst"]]
         for rev in (True, False):
             assert_same(T.build_parallel(T.EventStream(ev, V), rev, 4), oracle_mod.build(ev, V, rev))
+
+
+def test_rebuild_refreshes_lazily_widened_columns(oracle_mod):
+    """The tile scatter writes 16-byte gather records instead of the int64 nbr / eid columns;
+    those are widened on demand (export, device views, validate).  A rebuild from another
+    stream of the same shape must invalidate them: views taken after the rebuild, the export
+    and the sampler all see the new graph."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V = 400_000, 3000
+    ev1 = D.random_stream(E, V, 21)
+    ev2 = D.random_stream(E, V, 22)
+    g = D.build(ev1, V, True)
+    for seed, ev in ((21, ev1), (22, ev2), (21, ev1)):
+        D.rebuild(g, ev, trusted=True)
+        og = oracle_mod.build(oracle_mod.make_random_stream(E, V, seed), V, True)
+        ip, nb, ed, ts = D.graph_tensors(g)
+        assert np.array_equal(ip.cpu().numpy(), og["indptr"])
+        assert np.array_equal(nb.cpu().numpy(), og["nbr"])
+        assert np.array_equal(ed.cpu().numpy(), og["eid"])
+        assert np.array_equal(ts.cpu().numpy(), og["ts"])
+        g.validate()
+        nodes, times = D.make_queries(ev, 0, 20_000, 600, V)
+        out = D.sample_assemble(g, nodes, times, 10, "recent", 9, 11, E + 1, index64=True,
+                                dt64=True)
+        want = oracle_mod.sample_assemble(og, nodes.cpu().numpy(), times.cpu().numpy(), 10,
+                                          "recent", 9, 11, E + 1)
+        assert np.array_equal(out["node_index"].cpu().numpy(), want["node_index"])
+        assert np.array_equal(out["edge_index"].cpu().numpy(), want["edge_index"])
+        assert np.array_equal(out["time_delta64"].cpu().numpy(), want["time_delta"])
+    torch.cuda.synchronize()
