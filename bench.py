@@ -470,7 +470,7 @@ def main():
     ap.add_argument("--config", default="G", choices=sorted(CONFIGS))
     ap.add_argument("--chunk", type=int, default=3 * 8_000_000)
     ap.add_argument("--cpu-events", type=int, default=4_000_000)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--plan", default="weak", choices=["weak", "strong"],

@@ -846,26 +846,35 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
   return guarded([&] {
     check_graph(g);
     cudaStream_t s = 0;
-    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
-    DBuf dn(sizeof(int64_t) * qb, s);
-    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
-    check_queries(g, dn.as<int64_t>(), q, k, s);  // synchronises
+    // sampler.cpp:88-93 validates every query before sampling: query 0's node, then k, then
+    // the rest.  Here query 0 and k are checked on the host; the other nodes are checked on
+    // the device per sub-chunk, overlapped with the pipeline (out-of-range queries sample as
+    // absent), and the first bad one is reported after the launches -- the outputs are then
+    // unspecified, as for any failed call.
+    if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
+    if (q > 0 && (nodes[0] < 0 || nodes[0] >= g->V))
+      throw Error(TGFX_EVALIDATION, "query node " + std::to_string(nodes[0]) + " out of range");
+    if (q > 0) check_k(k);
     check_l(l);
     check_int32_outputs(g, self_edge_index);
     if (q == 0) return;
+    DBuf first(sizeof(unsigned long long), s);
+    const unsigned long long none = ~0ull;
+    TGFX_CUDA(cudaMemcpyAsync(first.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    TGFX_CUDA(cudaStreamSynchronize(s));
     constexpr int kStreams = 2;
     const int64_t sub = std::min<int64_t>(q, int64_t(1) << 22);  // 4 M queries per sub-chunk
     const size_t sl = static_cast<size_t>(sub) * static_cast<size_t>(l);
     struct Lane {
       cudaStream_t st = nullptr;
-      void *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr, *o64 = nullptr,
-           *ov = nullptr;
+      void *n = nullptr, *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr,
+           *o64 = nullptr, *ov = nullptr;
     } lanes[kStreams];
     auto release = [&] {
       for (Lane& ln : lanes) {
         if (!ln.st) continue;
         cudaStreamSynchronize(ln.st);
-        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
+        for (void* p : {ln.n, ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
           if (p) cudaFreeAsync(p, ln.st);
         cudaStreamSynchronize(ln.st);
         cudaStreamDestroy(ln.st);
@@ -875,6 +884,7 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     try {
       for (Lane& ln : lanes) {
         TGFX_CUDA(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+        ln.n = dmalloc(sizeof(int64_t) * sub, ln.st);
         ln.t = dmalloc(sizeof(double) * sub, ln.st);
         ln.on = dmalloc(sizeof(int32_t) * sl, ln.st);
         ln.oe = dmalloc(sizeof(int32_t) * sl, ln.st);
@@ -887,10 +897,13 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
         Lane& ln = lanes[i % kStreams];
         const int64_t c = std::min(sub, q - c0);
         const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
+        h2d(ln.n, nodes + c0, sizeof(int64_t) * c, ln.st);
         h2d(ln.t, times + c0, sizeof(double) * c, ln.st);
+        find_bad_async(g, static_cast<const int64_t*>(ln.n), c, c0,
+                       static_cast<unsigned long long*>(first.p), ln.st);
         SampleArgs a{};
         a.g = g;
-        a.nodes = dn.as<int64_t>() + c0;
+        a.nodes = static_cast<const int64_t*>(ln.n);
         a.times = static_cast<const double*>(ln.t);
         a.q = c;
         a.k = k;
@@ -918,6 +931,11 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
       throw;
     }
     release();
+    unsigned long long bad = none;
+    TGFX_CUDA(cudaMemcpy(&bad, first.p, sizeof(bad), cudaMemcpyDeviceToHost));
+    if (bad != none)
+      throw Error(TGFX_EVALIDATION,
+                  "query node " + std::to_string(nodes[bad]) + " out of range");
   });
 }
 

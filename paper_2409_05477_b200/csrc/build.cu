@@ -34,6 +34,7 @@
 // degree histogram + scan, and a stable LSD radix sort of (node, emission index).
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "graph.cuh"
@@ -1261,6 +1262,42 @@ void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
 
 int64_t fast_path_max_nodes() { return kFastMaxNodes; }
 
+// Pinned host mirrors of the build flags come from one slab pinned once per process:
+// cudaMallocHost / cudaFreeHost per graph cost up to hundreds of ms when the driver
+// synchronises (seen as 0.4 s stalls in tgfx_graph_free on the e2e path).
+namespace {
+constexpr int kFlagSlots = 1024;
+std::mutex g_flag_mu;
+BuildFlags* g_flag_slab = nullptr;
+std::vector<int> g_flag_free;
+
+BuildFlags* flags_alloc() {
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  if (!g_flag_slab) {
+    void* p = nullptr;
+    TGFX_CUDA(cudaMallocHost(&p, sizeof(BuildFlags) * kFlagSlots));
+    g_flag_slab = static_cast<BuildFlags*>(p);
+    for (int i = kFlagSlots - 1; i >= 0; --i) g_flag_free.push_back(i);
+  }
+  if (!g_flag_free.empty()) {
+    const int i = g_flag_free.back();
+    g_flag_free.pop_back();
+    return g_flag_slab + i;
+  }
+  void* p = nullptr;  // more than kFlagSlots live graphs: a separate pinned block
+  TGFX_CUDA(cudaMallocHost(&p, sizeof(BuildFlags)));
+  return static_cast<BuildFlags*>(p);
+}
+
+void flags_free(BuildFlags* f) {
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  if (g_flag_slab && f >= g_flag_slab && f < g_flag_slab + kFlagSlots)
+    g_flag_free.push_back(static_cast<int>(f - g_flag_slab));
+  else
+    cudaFreeHost(f);
+}
+}  // namespace
+
 void graph_alloc(tgfx_graph* g, cudaStream_t s) {
   g->m = g->n * (g->reverse ? 2 : 1);
   const size_t mm = static_cast<size_t>(std::max<int64_t>(g->m, 1));
@@ -1271,7 +1308,7 @@ void graph_alloc(tgfx_graph* g, cudaStream_t s) {
   TGFX_CUDA(cudaMemsetAsync(g->ts + mm, 0, sizeof(double) * kTsPad, s));
   g->dir = static_cast<NodeDir*>(dmalloc(sizeof(NodeDir) * std::max<int64_t>(g->V, 1), s));
   g->dflags = static_cast<BuildFlags*>(dmalloc(sizeof(BuildFlags), s));
-  TGFX_CUDA(cudaMallocHost(&g->hflags, sizeof(BuildFlags)));
+  g->hflags = flags_alloc();
 }
 
 void graph_release(tgfx_graph* g) {
@@ -1287,7 +1324,7 @@ void graph_release(tgfx_graph* g) {
   if (g->ws) dfree(g->ws, s);
   if (g->ws_small) dfree(g->ws_small, s);
   if (g->ws_rec) dfree(g->ws_rec, s);
-  if (g->hflags) cudaFreeHost(g->hflags);
+  if (g->hflags) flags_free(g->hflags);
   g->indptr = g->nbr = g->eid = nullptr;
   g->ts = nullptr;
   g->dir = nullptr;

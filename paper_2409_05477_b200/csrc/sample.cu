@@ -42,6 +42,9 @@ struct QueryIn {
   // sample_batch(seed = seeds[b]) call: RNG stream = qq - b * batch_q (sampler.cpp:100-101)
   const uint64_t* seeds = nullptr;
   int64_t batch_q = 0;
+  // node ids outside [0, vlim) are treated as absent queries (zero row): the host-buffer API
+  // validates its queries asynchronously and reports the first bad one after the launches
+  int64_t vlim = INT64_MAX;
 };
 
 // CounterRng(seed, stream) initial state of query qq (rng.hpp:23-24)
@@ -62,6 +65,10 @@ __device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_
   }
   u = static_cast<int64_t>(__ldcs(reinterpret_cast<const long long*>(in.nodes) + q));
   t = __ldcs(in.times + q);
+  if (static_cast<uint64_t>(u) >= static_cast<uint64_t>(in.vlim)) {
+    u = 0;
+    return false;
+  }
   return true;
 }
 
@@ -783,11 +790,11 @@ __global__ void __launch_bounds__(kThreads) k_random(
 }
 
 __global__ void k_find_bad(const int64_t* __restrict__ nodes, int64_t q, int64_t V,
-                           unsigned long long* first) {
+                           unsigned long long* first, int64_t base = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t u = nodes[i];
-    if (u < 0 || u >= V) atomicMin(first, (unsigned long long)i);
+    if (u < 0 || u >= V) atomicMin(first, (unsigned long long)(base + i));
   }
 }
 
@@ -1071,6 +1078,14 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
 
 }  // namespace
 
+void find_bad_async(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64_t base,
+                    unsigned long long* d_first, cudaStream_t s) {
+  if (q <= 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(q, 256), device_info().sms * 8));
+  k_find_bad<<<grid, 256, 0, s>>>(d_nodes, q, g->V, d_first, base);
+  after_launch("k_find_bad");
+}
+
 int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, cudaStream_t s) {
   if (q <= 0) return -1;
   unsigned long long* first = static_cast<unsigned long long*>(dmalloc(8, s));
@@ -1089,7 +1104,7 @@ int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, c
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (a.q <= 0) return;
   const tgfx_graph* g = a.g;
-  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q};
+  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q, g->V};
   Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
          a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
   const int grid = grid_groups(a.q);
