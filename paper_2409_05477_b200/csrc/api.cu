@@ -848,9 +848,9 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     cudaStream_t s = 0;
     // sampler.cpp:88-93 validates every query before sampling: query 0's node, then k, then
     // the rest.  Here query 0 and k are checked on the host; the other nodes are checked on
-    // the device per sub-chunk, overlapped with the pipeline (out-of-range queries sample as
-    // absent), and the first bad one is reported after the launches -- the outputs are then
-    // unspecified, as for any failed call.
+    // the device per sub-chunk, overlapped with the pipeline (an out-of-range node is replaced
+    // by node 0 in the device copy), and the first bad one is reported after the launches --
+    // the outputs are then unspecified, as for any failed call.
     if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
     if (q > 0 && (nodes[0] < 0 || nodes[0] >= g->V))
       throw Error(TGFX_EVALIDATION, "query node " + std::to_string(nodes[0]) + " out of range");
@@ -899,7 +899,7 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
         const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
         h2d(ln.n, nodes + c0, sizeof(int64_t) * c, ln.st);
         h2d(ln.t, times + c0, sizeof(double) * c, ln.st);
-        find_bad_async(g, static_cast<const int64_t*>(ln.n), c, c0,
+        find_bad_async(g, static_cast<int64_t*>(ln.n), c, c0,
                        static_cast<unsigned long long*>(first.p), ln.st);
         SampleArgs a{};
         a.g = g;

@@ -145,8 +145,9 @@ struct SampleArgs {
 
 // first invalid query index (or -1); validates node range on device (sampler.cpp:22-27)
 int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, cudaStream_t s);
-// atomicMin of (base + index) of every out-of-range node of d_nodes[0, q) into *d_first
-void find_bad_async(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64_t base,
+// atomicMin of (base + index) of every out-of-range node of d_nodes[0, q) into *d_first; the
+// bad entries of d_nodes (a caller-owned copy) are replaced by node 0
+void find_bad_async(const tgfx_graph* g, int64_t* d_nodes, int64_t q, int64_t base,
                     unsigned long long* d_first, cudaStream_t s);
 void launch_sample(const SampleArgs& a, cudaStream_t s);
 void launch_two_hop(const tgfx_graph* g, const int64_t* roots, const double* times, int64_t q,

@@ -42,9 +42,6 @@ struct QueryIn {
   // sample_batch(seed = seeds[b]) call: RNG stream = qq - b * batch_q (sampler.cpp:100-101)
   const uint64_t* seeds = nullptr;
   int64_t batch_q = 0;
-  // node ids outside [0, vlim) are treated as absent queries (zero row): the host-buffer API
-  // validates its queries asynchronously and reports the first bad one after the launches
-  int64_t vlim = INT64_MAX;
 };
 
 // CounterRng(seed, stream) initial state of query qq (rng.hpp:23-24)
@@ -65,10 +62,6 @@ __device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_
   }
   u = static_cast<int64_t>(__ldcs(reinterpret_cast<const long long*>(in.nodes) + q));
   t = __ldcs(in.times + q);
-  if (static_cast<uint64_t>(u) >= static_cast<uint64_t>(in.vlim)) {
-    u = 0;
-    return false;
-  }
   return true;
 }
 
@@ -789,12 +782,17 @@ __global__ void __launch_bounds__(kThreads) k_random(
   }
 }
 
+// first out-of-range node index (atomicMin of base + i); with fix, a bad node is replaced by 0
+// in the (caller-owned, device) copy so the sampler can run on it unchecked
 __global__ void k_find_bad(const int64_t* __restrict__ nodes, int64_t q, int64_t V,
-                           unsigned long long* first, int64_t base = 0) {
+                           unsigned long long* first, int64_t base = 0, int64_t* fix = nullptr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t u = nodes[i];
-    if (u < 0 || u >= V) atomicMin(first, (unsigned long long)(base + i));
+    if (u < 0 || u >= V) {
+      atomicMin(first, (unsigned long long)(base + i));
+      if (fix) fix[i] = 0;
+    }
   }
 }
 
@@ -1078,11 +1076,11 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
 
 }  // namespace
 
-void find_bad_async(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64_t base,
+void find_bad_async(const tgfx_graph* g, int64_t* d_nodes, int64_t q, int64_t base,
                     unsigned long long* d_first, cudaStream_t s) {
   if (q <= 0) return;
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(q, 256), device_info().sms * 8));
-  k_find_bad<<<grid, 256, 0, s>>>(d_nodes, q, g->V, d_first, base);
+  k_find_bad<<<grid, 256, 0, s>>>(d_nodes, q, g->V, d_first, base, d_nodes);
   after_launch("k_find_bad");
 }
 
@@ -1104,7 +1102,7 @@ int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, c
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (a.q <= 0) return;
   const tgfx_graph* g = a.g;
-  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q, g->V};
+  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q};
   Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
          a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
   const int grid = grid_groups(a.q);
