@@ -852,19 +852,29 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
     if (!d.nb) return;
     uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
     const int lane = threadIdx.x & 31;
+    // 32-bit slice-relative indices (slices with buckets have < 2^31 entries)
+    const uint32_t r0 = static_cast<uint32_t>(i0 - d.start);
+    const int cnt = static_cast<int>(i1 - i0 + 1);
+    const uint32_t last = static_cast<uint32_t>(d.end - d.start - 1);
+    const double nbm1 = static_cast<double>(d.nb - 1);
+    const auto bucket = [&](double t) -> uint32_t {  // bucket_of, with nb - 1 hoisted
+      const double xx = __dmul_rn(__dsub_rn(t, d.t_first), d.scale);
+      return xx < nbm1 ? static_cast<uint32_t>(xx) : static_cast<uint32_t>(d.nb - 1);
+    };
+    // the bucket of the entry before the tile's first one (lane 0, k = 0 needs it)
+    const int jprev0 = r0 ? static_cast<int>(bucket(ts[i0 - 1])) : -1;
 #pragma unroll
     for (int k = 0; k < kFillPer; ++k) {
-      const int64_t i = i0 + k * 256 + threadIdx.x;
-      const bool live = i <= i1;
-      const uint32_t jr = live ? bucket_of(x[k], d.t_first, d.scale, d.nb) : 0u;
+      const int o = k * 256 + static_cast<int>(threadIdx.x);
+      const bool live = o < cnt;
+      const uint32_t jr = live ? bucket(x[k]) : 0u;
       int jp = static_cast<int>(__shfl_up_sync(0xffffffffu, jr, 1));  // every lane, every k
       if (!live) continue;
-      const uint32_t r = static_cast<uint32_t>(i - d.start);
-      if (lane == 0) jp = r ? static_cast<int>(bucket_of(ts[i - 1], d.t_first, d.scale, d.nb)) : -1;
-      if (r == 0) jp = -1;
+      const uint32_t r = r0 + static_cast<uint32_t>(o);
+      if (lane == 0) jp = o == 0 ? jprev0 : static_cast<int>(bucket(ts[i0 + o - 1]));
 #pragma unroll 1
       for (int j = jp + 1; j <= static_cast<int>(jr); ++j) bkt[j] = r;
-      if (i == d.end - 1) bkt[d.nb] = static_cast<uint32_t>(d.end - d.start);
+      if (r == last) bkt[d.nb] = last + 1;
     }
     return;
   }
