@@ -1032,6 +1032,128 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
   }
 }
 
+
+// Uniform-k, one query per lane (ASSEMBLE, int32/fp32 rows, gather records, k <= KM, l <= 32):
+// Floyd's draws (the same skip-ahead CounterRng draws and collision rule as k_random_g) kept
+// as 32-bit slice offsets in registers, each sample's rank among them counted in registers
+// (O(k^2) integer compares per lane, no shuffles or ballots), then the samples gathered in
+// chunks of CH loads issued together and the rows staged in shared memory and written out
+// coalesced.  Slice lengths are < 2^32 whenever gather records exist (m < 2^32).
+template <int KM, int CH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_random_lane(
+    const NodeDir* __restrict__ dir, const double* __restrict__ ts, const uint4* __restrict__ rec,
+    QueryIn in, int64_t Q, int k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base,
+    Outs o) {
+  extern __shared__ __align__(16) uint32_t s_rows[];  // per warp [3][32 * l]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t seed_mix = mix64(seed);
+  uint32_t* sn = s_rows + static_cast<size_t>(warp) * 3 * 32 * l;
+  uint32_t* se = sn + 32 * l;
+  float* sd = reinterpret_cast<float*>(se + 32 * l);
+  const int64_t ngroups = ceil_div(Q, 32);
+  for (int64_t gq = static_cast<int64_t>(blockIdx.x) * kWarps + warp; gq < ngroups;
+       gq += static_cast<int64_t>(gridDim.x) * kWarps) {
+    const int64_t q = gq * 32 + lane;
+    int64_t u[1] = {0}, m[1];
+    double t[1] = {0.0};
+    bool pres[1];
+    pres[0] = q < Q && fetch_query(in, q, u[0], t[0]);
+    NodeDir d[1];
+    d[0] = load_dir(dir, u[0], pres[0]);
+    search_lines<8, 1>(ts, d, pres, t, m);
+    const uint32_t qm = static_cast<uint32_t>(m[0]);
+    const bool floyd = pres[0] && qm > static_cast<uint32_t>(k);
+    const int kb = !pres[0] ? -1 : floyd ? min(k, l - 1) : min(static_cast<int>(qm), l - 1);
+    // Floyd (sampler.cpp:66-80): draw d picks j in [0, qm - k + d]; a repeat takes qm - k + d
+    uint32_t c[KM];
+    const uint64_t s0 = query_rng(in, seed_mix, stream_base, q);
+#pragma unroll
+    for (int dd = 0; dd < KM; ++dd) {
+      c[dd] = 0xffffffffu;
+      if (floyd && dd < k) {
+        const uint32_t top = qm - static_cast<uint32_t>(k) + static_cast<uint32_t>(dd);
+        const uint32_t j = static_cast<uint32_t>(mulhi64(rng_draw(s0, dd), static_cast<uint64_t>(top) + 1));
+        bool hit = false;
+#pragma unroll
+        for (int e = 0; e < dd; ++e) hit |= c[e] == j;
+        c[dd] = hit ? top : j;
+      }
+    }
+    // slots: Floyd sample dd goes to column rank(dd) - drop (the most recent l - 1 kept,
+    // sequence.cpp:70-71); the whole-prefix case takes the last kb entries in order
+    const int drop = floyd ? k - kb : 0;
+    const int64_t wbase = floyd ? d[0].start : d[0].start + qm - kb;
+    const uint32_t* cu = c;
+    // rows are staged per lane at [lane * l + column]
+#pragma unroll
+    for (int c0 = 0; c0 < KM; c0 += CH) {
+      uint32_t rn[CH], re[CH];
+      double tv[CH];
+      int col[CH];
+#pragma unroll
+      for (int h = 0; h < CH; ++h) {
+        const int dd = c0 + h;
+        int cc = -1;
+        int64_t p = 0;
+        if (floyd) {
+          if (dd < k) {
+            int rk = 0;
+#pragma unroll
+            for (int e = 0; e < KM; ++e) rk += cu[e] < cu[dd];
+            if (rk >= drop) {
+              cc = rk - drop;
+              p = wbase + cu[dd];
+            }
+          }
+        } else if (dd < kb) {
+          cc = dd;
+          p = wbase + dd;
+        }
+        col[h] = cc;
+        uint32_t a, b, x, y;
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(x), "=r"(y) : "l"(rec + p));
+        rn[h] = a;
+        re[h] = b;
+        tv[h] = __hiloint2double(static_cast<int>(y), static_cast<int>(x));
+      }
+#pragma unroll
+      for (int h = 0; h < CH; ++h) {  // predicated stores: no branch to sink the loads into
+        const int sidx = lane * l + max(col[h], 0);
+        const int pr = col[h] >= 0;
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sn + sidx))), "r"(rn[h] + 1u), "r"(pr)
+                     : "memory");
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(se + sidx))), "r"(re[h] + 1u), "r"(pr)
+                     : "memory");
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sd + sidx))),
+                     "f"(__double2float_rn(t[0] - tv[h])), "r"(pr)
+                     : "memory");
+      }
+    }
+    // self-edge token at column kb, zero padding after it; absent queries: an all-zero row
+    for (int j = max(kb, 0); j < l; ++j) {
+      const bool self = j == kb;
+      sn[lane * l + j] = self ? static_cast<uint32_t>(u[0] + 1) : 0u;
+      se[lane * l + j] = self ? static_cast<uint32_t>(self_idx) : 0u;
+      sd[lane * l + j] = 0.0f;
+    }
+    if (q < Q) write_vlen<false>(o, q, kb + 1);
+    __syncwarp();
+    // coalesced copy-out of the warp's [nq x l] block
+    const int nq = static_cast<int>(min(static_cast<int64_t>(32), Q - gq * 32));
+    const int64_t obase = gq * 32 * l;
+    for (int sidx = lane; sidx < nq * l; sidx += 32) {
+      __stcs(static_cast<int*>(o.node) + obase + sidx, static_cast<int>(sn[sidx]));
+      __stcs(static_cast<int*>(o.edge) + obase + sidx, static_cast<int>(se[sidx]));
+      __stcs(o.dt32 + obase + sidx, sd[sidx]);
+    }
+    __syncwarp();
+  }
+}
+
 template <bool ASM, bool I64>
 void launch_random_g(const SampleArgs& a, const QueryIn& in, const Outs& o, int grid,
                      cudaStream_t s) {
@@ -1174,7 +1296,39 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     after_launch("k_recent");
     return;
   }
-  if (!g->search_exact && a.k <= 32) {  // grouped Floyd (default for k <= 32)
+  static const bool lane_uniform = [] {
+    const char* e = getenv("TGFX_UNIFORM_LANE");
+    return !(e && e[0] == '0');
+  }();
+  if (lane_uniform && !g->search_exact && g->rec && assemble && !a.index64 && a.dt32 &&
+      !a.dt64 && a.k <= 32 && l <= 32) {  // one query per lane (default for k <= 32, l <= 32)
+    const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
+#define TGFX_RANDOM_LANE(KM)                                                                   \
+  do {                                                                                         \
+    static const bool attr = [] {                                                              \
+      TGFX_CUDA(cudaFuncSetAttribute(k_random_lane<KM, 4, (KM > 16 ? 2 : 3)>,                  \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                     kWarps * 3 * 32 * 32 * 4));                               \
+      return true;                                                                             \
+    }();                                                                                       \
+    (void)attr;                                                                                \
+    k_random_lane<KM, 4, (KM > 16 ? 2 : 3)><<<grid, kThreads, sm, s>>>(g->dir, g->ts, g->rec, in, a.q, \
+                                                    static_cast<int>(a.k), l, a.self_edge_index, \
+                                                    a.seed, a.stream_base, o);                 \
+  } while (0)
+    if (a.k <= 8)
+      TGFX_RANDOM_LANE(8);
+    else if (a.k <= 16)
+      TGFX_RANDOM_LANE(16);
+    else if (a.k <= 24)
+      TGFX_RANDOM_LANE(24);
+    else
+      TGFX_RANDOM_LANE(32);
+#undef TGFX_RANDOM_LANE
+    after_launch("k_random_lane");
+    return;
+  }
+  if (!g->search_exact && a.k <= 32) {  // grouped Floyd (k <= 32)
     if (assemble) {
       if (a.index64)
         launch_random_g<true, true>(a, in, o, grid, s);

@@ -353,3 +353,54 @@ def test_time_buckets_on_adversarial_slices(T, oracle_mod):
     c, nb, ed, tsr = T.sample_batch_arrays(g, nodes, times, 10, "recent", 5)
     cw, nw, ew, tw = oracle_mod.sample_batch(og, nodes, times, 10, "recent", 5)
     assert np.array_equal(c, cw) and np.array_equal(nb, nw) and np.array_equal(ed, ew)
+
+
+@pytest.mark.parametrize("k,l", [(1, 2), (5, 3), (8, 9), (16, 5), (20, 21), (24, 32), (31, 32),
+                                 (32, 11), (32, 32)])
+def test_uniform_lane_kernel_int32_rows_vs_oracle(T, oracle_mod, k, l):
+    """Uniform-k with int32 / fp32-only rows takes the one-query-per-lane kernel
+    (k_random_lane): Floyd draws, ranks and the keep-the-most-recent-l-1 rule must match the
+    oracle bit for bit, including whole-prefix queries (qm <= k), empty slices, times before
+    every entry and absent hop-2 slots."""
+    ev, nodes, times = _workload(oracle_mod, 120_000, 700, 13, 600, n_events=30_000)
+    og = oracle_mod.build(ev, 700, True)
+    graph = T.build_sequential(T.EventStream(ev, 700), True)
+    rng = np.random.default_rng(k * 100 + l)
+    nodes = np.concatenate([nodes, rng.integers(0, 700, 3000)])
+    times = np.concatenate([times, rng.uniform(-10, ev["timestamp"][-1] + 10, 3000)])
+    for b0, seed in ((0, 5), (60_000, 77)):
+        nn, tt = nodes[b0:b0 + 33_000], times[b0:b0 + 33_000]
+        want = oracle_mod.sample_assemble(og, nn, tt, k, "random", seed, l, 120_001,
+                                          stream_base=b0)
+        got = T.sample_assemble(graph, nn, tt, k, "random", seed, l, 120_001, stream_base=b0)
+        assert np.array_equal(got["node_index"].astype(np.int64), want["node_index"])
+        assert np.array_equal(got["edge_index"].astype(np.int64), want["edge_index"])
+        assert np.array_equal(got["valid_len"].astype(np.int64), want["valid_len"])
+        assert np.array_equal(got["time_delta"], want["time_delta"].astype(np.float32))
+
+
+def test_uniform_lane_kernel_device_batched(T, oracle_mod):
+    """The lane kernel under per-batch seeds (one launch for many forward_concat batches); its
+    hop-2 use (absent virtual queries) is covered by test_two_hop_matches_reference_golden,
+    whose rows are int32 / fp32."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V = 200_000, 4000
+    ev = D.random_stream(E, V, 31)
+    g = D.build(ev, V, True)
+    h_ev = oracle_mod.make_random_stream(E, V, 31)
+    og = oracle_mod.build(h_ev, V, True)
+    nodes, times = D.make_queries(ev, 0, 40_000, 600, V)
+    qb = 1800
+    nb = -(-nodes.numel() // qb)
+    seeds = torch.arange(100, 100 + nb, dtype=torch.int64, device="cuda")
+    out = D.sample_assemble_batched(g, nodes, times, qb, 20, "random", seeds, 21, E + 1)
+    hn, ht = nodes.cpu().numpy(), times.cpu().numpy()
+    for b in range(nb):
+        s, e = b * qb, min((b + 1) * qb, len(hn))
+        want = oracle_mod.sample_assemble(og, hn[s:e], ht[s:e], 20, "random", 100 + b, 21, E + 1)
+        assert np.array_equal(out["node_index"][s:e].cpu().numpy().astype(np.int64),
+                              want["node_index"]), b
+        assert np.array_equal(out["time_delta"][s:e].cpu().numpy(),
+                              want["time_delta"].astype(np.float32)), b
+    torch.cuda.synchronize()
