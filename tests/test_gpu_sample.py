@@ -404,3 +404,30 @@ def test_uniform_lane_kernel_device_batched(T, oracle_mod):
         assert np.array_equal(out["time_delta"][s:e].cpu().numpy(),
                               want["time_delta"].astype(np.float32)), b
     torch.cuda.synchronize()
+
+
+def test_host_sample_assemble_reports_the_first_bad_query(T):
+    """tgfx_sample_assemble validates query nodes on the device inside its copy pipeline
+    (4 M-query sub-chunks): the error must still name the first out-of-range query in query
+    order (sampler.cpp:88-93), wherever it falls, and query 0 / k keep the reference's order."""
+    ev = np.array([(1, 0, 2, 3.0), (2, 1, 2, 4.0), (0, 0, 1, 5.0)], dtype=T.EVENT_DTYPE)
+    g = T.build_sequential(T.EventStream(ev, 3), False)
+    q = 9_000_000
+    nodes = np.zeros(q, np.int64)
+    times = np.full(q, 4.5)
+    nodes[8_500_000] = 7        # third sub-chunk
+    nodes[4_200_000] = -3       # second sub-chunk: the first bad one
+    nodes[8_999_999] = 11
+    with pytest.raises(T.ValidationError, match="query node -3 out of range"):
+        T.sample_assemble(g, nodes, times, 3, "recent", 0, 4, 4)
+    nodes[4_200_000] = 0
+    with pytest.raises(T.ValidationError, match="query node 7 out of range"):
+        T.sample_assemble(g, nodes, times, 3, "random", 0, 4, 4)
+    nodes[:] = 0
+    out = T.sample_assemble(g, nodes[:1000], times[:1000], 3, "recent", 0, 4, 4)
+    assert out["valid_len"].tolist() == [2] * 1000  # usable after a failure: 1 entry + self
+    bad0 = np.array([5, 0], np.int64)  # query 0's node is checked before k (and before l)
+    with pytest.raises(T.ValidationError, match="query node 5 out of range"):
+        T.sample_assemble(g, bad0, [1.0, 1.0], 0, "recent", 0, 4, 4)
+    with pytest.raises(T.ValidationError, match="k must be at least 1"):
+        T.sample_assemble(g, [0, 9], [1.0, 1.0], 0, "recent", 0, 4, 4)
