@@ -1419,11 +1419,11 @@ void ensure_columns(const tgfx_graph* cg, cudaStream_t s) {
   g->cols_valid = true;
 }
 
-// entries per time bucket (TGFX_BUCKET_ENTRIES, default 8; 0 disables the tables)
+// entries per time bucket (TGFX_BUCKET_ENTRIES, default 4; 0 disables the tables)
 static int64_t bucket_entries() {
   static const int64_t r = [] {
     const char* e = getenv("TGFX_BUCKET_ENTRIES");
-    return e ? static_cast<int64_t>(atoll(e)) : static_cast<int64_t>(8);
+    return e ? static_cast<int64_t>(atoll(e)) : static_cast<int64_t>(4);
   }();
   return r;
 }
