@@ -846,11 +846,10 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
   return guarded([&] {
     check_graph(g);
     cudaStream_t s = 0;
-    // sampler.cpp:88-93 validates every query before sampling: query 0's node, then k, then
-    // the rest.  Here query 0 and k are checked on the host; the other nodes are checked on
-    // the device per sub-chunk, overlapped with the pipeline (an out-of-range node is replaced
-    // by node 0 in the device copy), and the first bad one is reported after the launches --
-    // the outputs are then unspecified, as for any failed call.
+    // sampler.cpp:88-93 validates every query before sampling (query 0's node, then k, then
+    // the rest) and nothing is written on failure.  Query 0 and k are checked on the host; the
+    // other nodes on the device while the first sub-chunks already sample (into device
+    // buffers only); the rows are copied out only once every query has passed.
     if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
     if (q > 0 && (nodes[0] < 0 || nodes[0] >= g->V))
       throw Error(TGFX_EVALIDATION, "query node " + std::to_string(nodes[0]) + " out of range");
@@ -858,33 +857,45 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     check_l(l);
     check_int32_outputs(g, self_edge_index);
     if (q == 0) return;
+    DBuf dn(sizeof(int64_t) * static_cast<size_t>(q), s);
     DBuf first(sizeof(unsigned long long), s);
     const unsigned long long none = ~0ull;
     TGFX_CUDA(cudaMemcpyAsync(first.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
-    TGFX_CUDA(cudaStreamSynchronize(s));
+    h2d(dn.p, nodes, sizeof(int64_t) * q, s);
+    // bad nodes are also replaced by node 0 in this device copy, so sampling can start on it
+    // before the host has seen the verdict
+    find_bad_async(g, dn.as<int64_t>(), q, 0, static_cast<unsigned long long*>(first.p), s);
+    unsigned long long bad = none;
+    TGFX_CUDA(cudaMemcpyAsync(&bad, first.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    cudaEvent_t nodes_ready = nullptr;
+    TGFX_CUDA(cudaEventCreateWithFlags(&nodes_ready, cudaEventDisableTiming));
+    TGFX_CUDA(cudaEventRecord(nodes_ready, s));
     constexpr int kStreams = 2;
     const int64_t sub = std::min<int64_t>(q, int64_t(1) << 22);  // 4 M queries per sub-chunk
     const size_t sl = static_cast<size_t>(sub) * static_cast<size_t>(l);
     struct Lane {
       cudaStream_t st = nullptr;
-      void *n = nullptr, *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr,
-           *o64 = nullptr, *ov = nullptr;
+      void *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr, *o64 = nullptr,
+           *ov = nullptr;
     } lanes[kStreams];
     auto release = [&] {
       for (Lane& ln : lanes) {
         if (!ln.st) continue;
         cudaStreamSynchronize(ln.st);
-        for (void* p : {ln.n, ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
+        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
           if (p) cudaFreeAsync(p, ln.st);
         cudaStreamSynchronize(ln.st);
         cudaStreamDestroy(ln.st);
         ln.st = nullptr;
       }
+      cudaStreamSynchronize(s);
+      if (nodes_ready) cudaEventDestroy(nodes_ready);
+      nodes_ready = nullptr;
     };
     try {
       for (Lane& ln : lanes) {
         TGFX_CUDA(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
-        ln.n = dmalloc(sizeof(int64_t) * sub, ln.st);
+        TGFX_CUDA(cudaStreamWaitEvent(ln.st, nodes_ready, 0));
         ln.t = dmalloc(sizeof(double) * sub, ln.st);
         ln.on = dmalloc(sizeof(int32_t) * sl, ln.st);
         ln.oe = dmalloc(sizeof(int32_t) * sl, ln.st);
@@ -892,18 +903,14 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
         if (dt64) ln.o64 = dmalloc(sizeof(double) * sl, ln.st);
         ln.ov = dmalloc(sizeof(int32_t) * sub, ln.st);
       }
-      int i = 0;
-      for (int64_t c0 = 0; c0 < q; c0 += sub, ++i) {
+      const int64_t nsub = ceil_div(q, sub);
+      auto compute = [&](int64_t i) {  // times upload + sampling of sub-chunk i on its lane
         Lane& ln = lanes[i % kStreams];
-        const int64_t c = std::min(sub, q - c0);
-        const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
-        h2d(ln.n, nodes + c0, sizeof(int64_t) * c, ln.st);
+        const int64_t c0 = i * sub, c = std::min(sub, q - c0);
         h2d(ln.t, times + c0, sizeof(double) * c, ln.st);
-        find_bad_async(g, static_cast<int64_t*>(ln.n), c, c0,
-                       static_cast<unsigned long long*>(first.p), ln.st);
         SampleArgs a{};
         a.g = g;
-        a.nodes = static_cast<const int64_t*>(ln.n);
+        a.nodes = dn.as<int64_t>() + c0;
         a.times = static_cast<const double*>(ln.t);
         a.q = c;
         a.k = k;
@@ -918,12 +925,31 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
         a.dt64 = static_cast<double*>(ln.o64);
         a.valid_len = ln.ov;
         launch_sample(a, ln.st);
+      };
+      auto copy_out = [&](int64_t i) {  // rows of sub-chunk i to the caller's buffers
+        Lane& ln = lanes[i % kStreams];
+        const int64_t c0 = i * sub, c = std::min(sub, q - c0);
+        const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
         const size_t r0 = static_cast<size_t>(c0) * static_cast<size_t>(l);
         d2h(node_index + r0, ln.on, sizeof(int32_t) * cl, ln.st);
         d2h(edge_index + r0, ln.oe, sizeof(int32_t) * cl, ln.st);
         if (dt32) d2h(dt32 + r0, ln.o32, sizeof(float) * cl, ln.st);
         if (dt64) d2h(dt64 + r0, ln.o64, sizeof(double) * cl, ln.st);
         d2h(valid_len + c0, ln.ov, sizeof(int32_t) * c, ln.st);
+      };
+      // the first sub-chunks sample while the host waits for the node check; nothing reaches
+      // the caller's buffers before it has passed
+      const int64_t pre = std::min<int64_t>(nsub, kStreams);
+      for (int64_t i = 0; i < pre; ++i) compute(i);
+      TGFX_CUDA(cudaStreamSynchronize(s));  // the node check -> bad
+      if (bad != none) {
+        release();
+        throw Error(TGFX_EVALIDATION,
+                    "query node " + std::to_string(nodes[bad]) + " out of range");
+      }
+      for (int64_t i = 0; i < nsub; ++i) {
+        if (i >= pre) compute(i);
+        copy_out(i);
       }
       for (Lane& ln : lanes) TGFX_CUDA(cudaStreamSynchronize(ln.st));
     } catch (...) {
@@ -931,11 +957,6 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
       throw;
     }
     release();
-    unsigned long long bad = none;
-    TGFX_CUDA(cudaMemcpy(&bad, first.p, sizeof(bad), cudaMemcpyDeviceToHost));
-    if (bad != none)
-      throw Error(TGFX_EVALIDATION,
-                  "query node " + std::to_string(nodes[bad]) + " out of range");
   });
 }
 
