@@ -344,7 +344,12 @@ def run_ours(args, cfg):
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": bytes_per_launch,
-                     "avg_launch_ms": avg_launch_ms},
+                     "avg_launch_ms": avg_launch_ms,
+                     # SURVEY 8(d) algorithmic bytes count every window read as HBM traffic;
+                     # most windows are L2 hits, so frac can exceed 1.  dram_frac is the ncu-
+                     # measured DRAM traffic per launch (traffic) over the same launch time.
+                     "dram_frac": (traffic / (avg_launch_ms * 1e-3) / 1e9 / peak
+                                   if traffic else None)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
