@@ -527,14 +527,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       // each lane fills slots s = lane + 32 it, it < l, in chunks of UNR: all of a chunk's
       // loads are issued (phase A) before any result is stored (phase B) -- the compiler will
       // not hoist a slot's loads above the previous slot's shared-memory stores by itself
-      for (int it0 = 0; it0 < l; it0 += UNR) {
+      for (int it0 = 0; it0 < QL * l; it0 += UNR) {
         uint32_t rn[UNR], re[UNR];
         double tv[UNR], tq[UNR];
         uint32_t sf[UNR];  // self-slot node id + 1, or 0
         bool tk[UNR];
 #pragma unroll
         for (int uu = 0; uu < UNR; ++uu) {
-          const bool valid = it0 + uu < l;
+          const bool valid = it0 + uu < QL * l;
           const int qr = valid ? qi : 0;  // padding slots run qi past the warp's 32 queries
           const int kbq = s_kb[warp][qr];
           const longlong2 st = s_st[warp][qr];
