@@ -63,9 +63,42 @@ const DeviceInfo& device_info() {
   return info;
 }
 
+// Large buffers (graph columns, gather records, upload staging) come from their own
+// stream-ordered pool: freed and re-requested in the same sizes every step, they never share
+// blocks with the small transient buffers, so the pool does not fragment and grow again
+// (which stalled a host-buffer build for 0.3-0.6 s on remapping).
+constexpr size_t kBigAlloc = size_t(256) << 20;
+
+cudaMemPool_t big_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      cudaGetLastError();
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+
 void* dmalloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
+  if (bytes >= kBigAlloc) {
+    if (cudaMemPool_t pool = big_pool(device_info().device)) {
+      check_cuda(cudaMallocFromPoolAsync(&p, bytes, pool, s), "cudaMallocFromPoolAsync");
+      return p;
+    }
+  }
   check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
   return p;
 }

@@ -33,6 +33,8 @@
 // num_nodes exceed the shared-memory cursor budget take the large-V path: global
 // degree histogram + scan, and a stable LSD radix sort of (node, emission index).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -1347,8 +1349,23 @@ void graph_release(tgfx_graph* g) {
   g->ws = g->ws_small = g->ws_rec = nullptr;
 }
 
+// TGFX_TRACE=1: host-side phase timers of build_graph on stderr (each phase synchronised)
+static bool build_trace() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static double trace_ms(cudaStream_t s) {
+  if (build_trace()) cudaStreamSynchronize(s);
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted) {
   g->cols_valid = true;  // every path writes the columns, except the tile scatter with records
+  const double t0 = trace_ms(s);
   (void)trusted;
   const int64_t n = g->n, V = g->V;
   const int R = g->reverse ? 2 : 1;
@@ -1375,6 +1392,7 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   }
   run_flags_pass(g, d_ev, C, chunk_ev, cnt, fast && V > 0, s);
   read_flags(g, s);
+  const double t1 = trace_ms(s);
   if (g->hflags->bad_index != ~0ull) throw_bad_endpoint(g, d_ev, s);
   g->max_eid = n ? g->hflags->max_eid : -1;
   g->min_eid = n ? g->hflags->min_eid : 0;
@@ -1395,7 +1413,11 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   else
     build_large(g, src, s);
   if (tmp) dfree(tmp, s);
+  const double t2 = trace_ms(s);
   build_node_dir(g, s);
+  if (build_trace())
+    fprintf(stderr, "[tgfx] build_graph: flags %.1f ms, scatter %.1f ms, node dir %.1f ms\n",
+            t1 - t0, t2 - t1, trace_ms(s) - t2);
 }
 
 __global__ void __launch_bounds__(256) k_widen(const uint4* __restrict__ rec, int64_t m,
