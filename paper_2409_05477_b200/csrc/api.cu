@@ -1,3 +1,4 @@
+#include <unordered_map>
 #include <chrono>
 #include <cstdio>
 // api.cu -- the extern "C" boundary (include/tgfx.h): argument checks with the reference's
@@ -63,48 +64,96 @@ const DeviceInfo& device_info() {
   return info;
 }
 
-// Large buffers (graph columns, gather records, upload staging) come from their own
-// stream-ordered pool: freed and re-requested in the same sizes every step, they never share
-// blocks with the small transient buffers, so the pool does not fragment and grow again
-// (which stalled a host-buffer build for 0.3-0.6 s on remapping).
+// Large buffers (graph columns, gather records, upload staging) are recycled by exact size:
+// freed blocks wait in a small cache (with an event marking the end of their last use) and
+// the next request of the same size takes one back.  A host-buffer build allocates and frees
+// the same ~16 GB every step; through the driver's pool that re-mapped physical memory now
+// and then, stalling single builds for 0.3-0.7 s.
 constexpr size_t kBigAlloc = size_t(256) << 20;
+constexpr size_t kBigCacheBytes = size_t(40) << 30;
 
-cudaMemPool_t big_pool(int dev) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!pools[dev]) {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
-      cudaGetLastError();
-      pools[dev] = nullptr;
-      return nullptr;
-    }
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  return pools[dev];
-}
+struct BigBlock {
+  void* p;
+  size_t bytes;
+  int dev;
+  cudaEvent_t done;
+};
+std::mutex g_big_mu;
+std::unordered_map<void*, std::pair<size_t, int>> g_big_live;  // ptr -> (bytes, device)
+std::vector<BigBlock> g_big_free;
+size_t g_big_free_bytes = 0;
 
 void* dmalloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
   if (bytes >= kBigAlloc) {
-    if (cudaMemPool_t pool = big_pool(device_info().device)) {
-      check_cuda(cudaMallocFromPoolAsync(&p, bytes, pool, s), "cudaMallocFromPoolAsync");
-      return p;
+    const int dev = device_info().device;
+    {
+      std::lock_guard<std::mutex> lk(g_big_mu);
+      for (size_t i = 0; i < g_big_free.size(); ++i) {
+        BigBlock& b = g_big_free[i];
+        if (b.bytes == bytes && b.dev == dev) {
+          check_cuda(cudaStreamWaitEvent(s, b.done, 0), "cudaStreamWaitEvent");
+          cudaEventDestroy(b.done);
+          p = b.p;
+          g_big_free_bytes -= b.bytes;
+          g_big_free.erase(g_big_free.begin() + static_cast<std::ptrdiff_t>(i));
+          g_big_live[p] = {bytes, dev};
+          return p;
+        }
+      }
     }
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {  // out of memory: drop the cache
+      cudaGetLastError();
+      {
+        std::lock_guard<std::mutex> lk(g_big_mu);
+        for (BigBlock& b : g_big_free) {
+          cudaEventSynchronize(b.done);
+          cudaEventDestroy(b.done);
+          cudaFreeAsync(b.p, 0);
+        }
+        g_big_free.clear();
+        g_big_free_bytes = 0;
+      }
+      cudaDeviceSynchronize();
+      check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    }
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    g_big_live[p] = {bytes, dev};
+    return p;
   }
   check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
   return p;
 }
 
 void dfree(void* p, cudaStream_t s) {
-  if (p) check_cuda(cudaFreeAsync(p, s), "cudaFreeAsync");
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    auto it = g_big_live.find(p);
+    if (it != g_big_live.end()) {
+      const size_t bytes = it->second.first;
+      const int dev = it->second.second;
+      g_big_live.erase(it);
+      cudaEvent_t done = nullptr;
+      if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(done, s) == cudaSuccess) {
+        g_big_free.push_back({p, bytes, dev, done});
+        g_big_free_bytes += bytes;
+        while (g_big_free_bytes > kBigCacheBytes && !g_big_free.empty()) {  // oldest first
+          BigBlock b = g_big_free.front();
+          g_big_free.erase(g_big_free.begin());
+          g_big_free_bytes -= b.bytes;
+          cudaEventSynchronize(b.done);
+          cudaEventDestroy(b.done);
+          cudaFreeAsync(b.p, 0);
+        }
+        return;
+      }
+      if (done) cudaEventDestroy(done);
+    }
+  }
+  check_cuda(cudaFreeAsync(p, s), "cudaFreeAsync");
 }
 
 namespace {

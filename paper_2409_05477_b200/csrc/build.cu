@@ -1146,6 +1146,20 @@ tgfx_event* sorted_copy(const tgfx_event* d_ev, int64_t n, cudaStream_t s) {
   return out;
 }
 
+// TGFX_TRACE=1: host-side phase timers of build_graph on stderr (each phase synchronised)
+static bool build_trace() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static double trace_ms(cudaStream_t s) {
+  if (build_trace()) cudaStreamSynchronize(s);
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, uint32_t* cnt,
                 cudaStream_t s) {
   const int32_t V = static_cast<int32_t>(g->V);
@@ -1175,14 +1189,17 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   int64_t ncold = 0;
   TGFX_CUDA(cudaMemcpyAsync(&ncold, ncold_d, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   TGFX_CUDA(cudaStreamSynchronize(s));
+  const double tf0 = trace_ms(s);
   ulonglong2* img = static_cast<ulonglong2*>(
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
+  const double tf1 = trace_ms(s);
   if (g->n == 0) return;
   if (use_tile_scatter(V)) {
     // with gather records the scatter writes {rec, ts} instead of {nbr, eid, ts}; the int64
     // columns are widened from the records when something asks for them (ensure_columns)
     uint4* rec = ensure_rec(g, s);
     g->cols_valid = rec == nullptr;
+    const double tf2 = trace_ms(s);
     const size_t tsm = tile_smem_for(V);
     int bits = 1;
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
@@ -1207,6 +1224,9 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
                                                                       g->eid, g->ts, rec);
       after_launch("k_cold_u");
     }
+    if (build_trace())
+      fprintf(stderr, "[tgfx] build_fast: cold image alloc %.1f ms, records alloc %.1f ms, "
+                      "scatter %.1f ms\n", tf1 - tf0, tf2 - tf1, trace_ms(s) - tf2);
     return;
   }
   const size_t smem = scatter_smem(V);
@@ -1347,20 +1367,6 @@ void graph_release(tgfx_graph* g) {
   g->dflags = nullptr;
   g->hflags = nullptr;
   g->ws = g->ws_small = g->ws_rec = nullptr;
-}
-
-// TGFX_TRACE=1: host-side phase timers of build_graph on stderr (each phase synchronised)
-static bool build_trace() {
-  static const bool on = [] {
-    const char* e = getenv("TGFX_TRACE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-static double trace_ms(cudaStream_t s) {
-  if (build_trace()) cudaStreamSynchronize(s);
-  return std::chrono::duration<double, std::milli>(
-             std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
 void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool trusted) {
