@@ -4,18 +4,23 @@
 // build_sequence_batch (proj/src/sequence.cpp:55-86):
 //
 //   * the strict-before-t prefix m(u, t) = #{ts < t} of a slice (lower_bound,
-//     sampler.cpp:16-20; NaN t -> 0) is found by search_lines: interpolated probes that each
-//     read and resolve a whole 8-entry ts line, bracketed by the node directory record
-//     (slice bounds + first/last ts).  Any search that keeps ts[lo-1] < t <= ts[hi] returns
-//     the unique lower_bound on a sorted, NaN-free slice; graphs not known to be sorted and
-//     NaN-free replay std::lower_bound's own bisection (search_interleaved) instead.
+//     sampler.cpp:16-20; NaN t -> 0) is found by search_lines: the slice's time bucket
+//     (build.cu, build_node_dir) narrows it to ~4 entries, then interpolated probes each read
+//     and resolve a whole kProbeW-entry ts line, bracketed by the node directory record
+//     (slice bounds + first/last ts + bucket grid).  Any search that keeps
+//     ts[lo-1] < t <= ts[hi] returns the unique lower_bound on a sorted, NaN-free slice;
+//     graphs not known to be sorted and NaN-free replay std::lower_bound's own bisection
+//     (search_interleaved) instead.
 //   * recent-k (k_recent_line): one query per lane for the search, then the warp assembles its
 //     32 rows "slot-parallel": lane s handles output slot s of the warp's [32 x l] block, so
-//     window gathers are near-contiguous and every store is a coalesced run.
+//     window gathers are near-contiguous and every store is a coalesced run; window entries
+//     come from the graph's 16-byte gather records, staged in shared memory and written out
+//     by bulk copies.
 //   * uniform-k: Floyd's algorithm with the reference's counter RNG (rng.hpp:23-38,
-//     sampler.cpp:66-80): draw d by O(1) skip-ahead (x_d = mix64(s0 + d*gamma)), collisions
-//     resolved in order d with one ballot each, offsets ranked by shuffles -- by 8-lane groups
-//     (k_random_g, k <= 32, four queries per warp at a time) or by the whole warp (k_random).
+//     sampler.cpp:66-80): draw d by O(1) skip-ahead (x_d = mix64(s0 + d*gamma)), a repeat
+//     resolved in order d -- one query per lane with draws and ranks in registers
+//     (k_random_lane, int32 rows, k <= 32), by 8-lane groups with ballots and shuffles
+//     (k_random_g, k <= 32) or by the whole warp (k_random, larger k / exact search).
 //   * suffix infilling epilogue: ids + 1, self-edge token at column kb, zero padding,
 //     dt = t_q - ts in fp64 then rounded to fp32 (and/or kept as fp64).
 #include <algorithm>
