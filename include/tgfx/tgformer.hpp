@@ -18,8 +18,7 @@
 //   synthetic.hpp:17   make_random_stream         same (device generator, bit-identical)
 //
 // Differences a caller can observe: none in values; num_threads is accepted and ignored (the
-// reference's results are thread-count independent too); uniform sampling is limited to
-// k <= 256 when the prefix is longer than k (std::runtime_error otherwise).
+// reference's results are thread-count independent too).
 #pragma once
 
 #include <cstddef>

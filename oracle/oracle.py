@@ -98,6 +98,8 @@ def ref():
         L.ref_graph_info.argtypes = [_P, _P]
         L.ref_graph_export.argtypes = [_P, _P, _P, _P, _P]
         L.ref_graph_validate.argtypes = [_P]
+        L.ref_graph_from_columns.restype = _P
+        L.ref_graph_from_columns.argtypes = [_I64, _I64, C.c_int, _I64, _P, _P, _P, _P]
         L.ref_sample_batch.argtypes = [_P, _P, _P, _I64, _I64, C.c_int, _U64, C.c_int, _P, _P, _P,
                                        _P, C.POINTER(C.c_double)]
         L.ref_sample_random.argtypes = [_P, _I64, C.c_double, _I64, _U64, _U64, _P, _P, _P, _P]
@@ -305,6 +307,17 @@ class RefGraph:
         ref().ref_graph_export(self.h, _ptr(indptr), _ptr(nbr), _ptr(eid), _ptr(ts))
         return dict(num_nodes=inf["num_nodes"], num_edges=inf["num_edges"],
                     reverse=inf["reverse"], indptr=indptr, nbr=nbr[:m], eid=eid[:m], ts=ts[:m])
+
+
+def ref_validate_columns(num_nodes, num_edges, reverse, indptr, nbr, eid, ts):
+    """TCsr::validate (tcsr.cpp:54-81) of the reference on the given columns -> message or ''."""
+    arrs = [np.ascontiguousarray(a, dtype=t) for a, t in
+            ((indptr, np.int64), (nbr, np.int64), (eid, np.int64), (ts, np.float64))]
+    h = ref().ref_graph_from_columns(num_nodes, num_edges, 1 if reverse else 0, len(arrs[1]),
+                                     *(_ptr(a) for a in arrs))
+    g = RefGraph(h)
+    rc = ref().ref_graph_validate(g.h)
+    return ref().ref_last_error().decode() if rc else ""
 
 
 def _ref_err(rc):

@@ -87,6 +87,21 @@ int ref_build_parallel_raw(void* stream, int reverse, int threads, void** graph_
 
 void ref_graph_free(void* g) { delete static_cast<tgf::TCsr*>(g); }
 
+// a tgf::TCsr assembled from caller columns (for TCsr::validate texts on corrupted graphs)
+void* ref_graph_from_columns(int64_t num_nodes, int64_t num_edges, int reverse, int64_t m,
+                             const int64_t* indptr, const int64_t* nbr, const int64_t* eid,
+                             const double* ts) {
+  auto* g = new tgf::TCsr();
+  g->num_nodes = num_nodes;
+  g->num_edges = num_edges;
+  g->reverse = reverse != 0;
+  g->indptr.assign(indptr, indptr + num_nodes + 1);
+  g->neighbor_ids.assign(nbr, nbr + m);
+  g->edge_ids.assign(eid, eid + m);
+  g->timestamps.assign(ts, ts + m);
+  return g;
+}
+
 void ref_graph_info(void* gp, int64_t* out4) {
   auto* g = static_cast<tgf::TCsr*>(gp);
   out4[0] = g->num_nodes;

@@ -183,8 +183,14 @@ struct DBuf {
   cudaStream_t s;
   DBuf(size_t bytes, cudaStream_t st) : s(st) { p = dmalloc(bytes, s); }
   ~DBuf() {
-    if (p) cudaFreeAsync(p, s);
+    // through dfree: buffers >= kBigAlloc are tracked in g_big_live and must be recycled there
+    try {
+      dfree(p, s);
+    } catch (...) {
+    }
   }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
   template <typename T>
   T* as() const {
     return static_cast<T*>(p);
@@ -398,10 +404,11 @@ int tgfx_graph_from_device(int64_t num_nodes, int64_t num_edges, int reverse, in
       if (flags & TGFX_TRUSTED) {
         g->search_exact = 0;  // caller vouches: slices sorted, NaN-free (e.g. built by tgfx)
       } else {
+        g->indptr_bad = indptr_in_range(g->indptr, num_nodes, m, s) ? 0 : 1;
         // interpolation search needs sorted, NaN-free slices; otherwise replay lower_bound
         g->search_exact = (!validate_graph(g, s).empty() || any_nan(g->ts, m, s)) ? 1 : 0;
       }
-      build_node_dir(g, s);
+      if (!g->indptr_bad) build_node_dir(g, s);
       TGFX_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
       free_graph(g);
@@ -485,15 +492,22 @@ int tgfx_graph_from_host(int64_t num_nodes, int64_t num_edges, int reverse, int6
       g->min_eid = mn;
       // interpolation search needs every slice sorted by ts and NaN-free; otherwise the
       // sampler replays std::lower_bound's bisection exactly (sampler.cpp:16-20)
-      bool ok = indptr[0] == 0 && indptr[num_nodes] == m;
+      bool mono = indptr[0] == 0 && indptr[num_nodes] == m;
+      for (int64_t u = 0; mono && u < num_nodes; ++u) {
+        const int64_t lo = indptr[u], hi = indptr[u + 1];
+        if (lo > hi || lo < 0 || hi > m) mono = false;
+      }
+      bool ok = mono;
       for (int64_t u = 0; ok && u < num_nodes; ++u) {
         const int64_t lo = indptr[u], hi = indptr[u + 1];
-        if (lo > hi || lo < 0 || hi > m) ok = false;
         for (int64_t i = lo; ok && i < hi; ++i)
           if (ts[i] != ts[i] || (i > lo && ts[i - 1] > ts[i])) ok = false;
       }
       g->search_exact = ok ? 0 : 1;
-      build_node_dir(g, s);
+      // a corrupt indptr (e.g. a CRC-valid but damaged container) must not reach the node
+      // directory kernels, which index ts through it
+      g->indptr_bad = mono ? 0 : 1;
+      if (mono) build_node_dir(g, s);
       TGFX_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
       free_graph(g);
@@ -964,8 +978,12 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
       for (Lane& ln : lanes) {
         if (!ln.st) continue;
         cudaStreamSynchronize(ln.st);
-        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov})
-          if (p) cudaFreeAsync(p, ln.st);
+        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov}) {
+          try {
+            dfree(p, ln.st);  // dmalloc'd: big blocks go back to the size cache
+          } catch (...) {
+          }
+        }
         cudaStreamSynchronize(ln.st);
         cudaStreamDestroy(ln.st);
         ln.st = nullptr;

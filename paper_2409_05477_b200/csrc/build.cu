@@ -907,35 +907,48 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
 }
 
 // ------------------------------------------------------------------ validate (tcsr.cpp:54-81)
+// The reference walks nodes in order (indptr monotone at u, then slice u sorted), then entries
+// in order (neighbour id, then edge id); the first failure is the one thrown.  Here every check
+// runs in parallel and reduces to the first failure in that same order:
+//   node_fail = min u whose slice is unsorted (only slices below the first non-monotone node
+//               u_mono, which the host finds in its copy of indptr, can be walked);
+//   entry_fail = min (2 i + which) over entries with an id out of range.
+// An entry pair (i-1, i) out of order lies in one slice unless a slice starts at i; the node
+// owning i (upper_bound over the monotone indptr prefix) is looked up only for such pairs, so
+// at most V + #failures searches run.
 __global__ void k_validate(const int64_t* __restrict__ indptr, const int64_t* __restrict__ nbr,
                            const int64_t* __restrict__ eid, const double* __restrict__ ts,
-                           int64_t V, int64_t Vn, int64_t E, int64_t m, int* err) {
-  // err codes: 1 indptr endpoints, 2 not monotone, 3 slice not sorted, 4 nbr range, 5 eid range
+                           int64_t u_mono, int64_t Vn, int64_t E, int64_t m,
+                           unsigned long long* __restrict__ node_fail,
+                           unsigned long long* __restrict__ entry_fail) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t0 == 0 && (indptr[0] != 0 || indptr[V] != m)) atomicMin(err, 1);
-  for (int64_t u = t0; u < V; u += stride)
-    if (indptr[u] > indptr[u + 1]) atomicMin(err, 2);
+  // entries walked by the node loop: [0, indptr[u_mono]) (indptr[0..u_mono] is monotone)
+  const int64_t top = __ldg(reinterpret_cast<const long long*>(indptr) + u_mono);
+  const int64_t walked = top < 0 ? 0 : (top < m ? top : m);
   for (int64_t i = t0; i < m; i += stride) {
-    if (nbr[i] < 0 || nbr[i] >= Vn) atomicMin(err, 4);
-    if (eid[i] < 0 || eid[i] >= E) atomicMin(err, 5);
+    const int64_t nb = nbr[i], e = eid[i];
+    if (nb < 0 || nb >= Vn) atomicMin(entry_fail, 2ull * static_cast<unsigned long long>(i));
+    else if (e < 0 || e >= E) atomicMin(entry_fail, 2ull * static_cast<unsigned long long>(i) + 1);
+    if (i >= 1 && i < walked) {
+      const double a = ts[i - 1], c = ts[i];
+      if (a > c || (a == c && eid[i - 1] > e)) {
+        int64_t lo = 0, n = u_mono + 1;  // upper_bound(indptr[0..u_mono], i) - 1
+        while (n > 0) {
+          const int64_t h = n >> 1;
+          if (__ldg(reinterpret_cast<const long long*>(indptr) + lo + h) <= i) {
+            lo += h + 1;
+            n -= h + 1;
+          } else {
+            n = h;
+          }
+        }
+        const int64_t u = lo - 1;
+        if (u >= 0 && u < u_mono && indptr[u] < i)  // i - 1 is in the same slice
+          atomicMin(node_fail, static_cast<unsigned long long>(u));
+      }
+    }
   }
-  // sortedness within slices: i and i+1 in the same slice <=> no indptr boundary between
-  for (int64_t u = t0; u < V; u += stride) {
-    const int64_t lo = indptr[u], hi = indptr[u + 1];
-    if (hi - lo > 4096) continue;  // long slices checked by the entry-parallel loop below
-    for (int64_t i = lo + 1; i < hi; ++i)
-      if (ts[i - 1] > ts[i] || (ts[i - 1] == ts[i] && eid[i - 1] > eid[i])) atomicMin(err, 3);
-  }
-}
-
-__global__ void k_validate_long(const int64_t* __restrict__ indptr,
-                                const int64_t* __restrict__ eid, const double* __restrict__ ts,
-                                int64_t u, int* err) {
-  const int64_t lo = indptr[u], hi = indptr[u + 1];
-  for (int64_t i = lo + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (ts[i - 1] > ts[i] || (ts[i - 1] == ts[i] && eid[i - 1] > eid[i])) atomicMin(err, 3);
 }
 
 int grid_for(int64_t work, int threads, int per_sm = 8) {
@@ -1439,10 +1452,13 @@ __global__ void __launch_bounds__(256) k_widen(const uint4* __restrict__ rec, in
 
 void ensure_columns(const tgfx_graph* cg, cudaStream_t s) {
   tgfx_graph* g = const_cast<tgfx_graph*>(cg);
+  std::lock_guard<std::mutex> lk(g->cols_mu);
   if (g->cols_valid) return;
   if (g->m > 0) {
     k_widen<<<grid_for(g->m, 256), 256, 0, s>>>(g->rec, g->m, g->nbr, g->eid);
     after_launch("k_widen");
+    // complete before another thread sees cols_valid and reads the columns on its own stream
+    TGFX_CUDA(cudaStreamSynchronize(s));
   }
   g->cols_valid = true;
 }
@@ -1506,37 +1522,39 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
 }
 
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {
-  ensure_columns(g, s);
-  int* err = static_cast<int*>(dmalloc(sizeof(int), s));
-  const int big = 1 << 30;
-  TGFX_CUDA(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-  k_validate<<<grid_for(std::max(g->V, g->m), 256), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
-                                                                 g->V, g->other_limit, g->eid_limit,
-                                                                 g->m, err);
-  after_launch("k_validate");
+  // tcsr.cpp:54-81 in the reference's order; the shape checks (sizes) are the caller's
   std::vector<int64_t> ip(static_cast<size_t>(g->V + 1));
   TGFX_CUDA(cudaMemcpyAsync(ip.data(), g->indptr, sizeof(int64_t) * (g->V + 1),
                             cudaMemcpyDeviceToHost, s));
   TGFX_CUDA(cudaStreamSynchronize(s));
-  for (int64_t u = 0; u < g->V; ++u) {
-    if (ip[u + 1] - ip[u] > 4096) {
-      k_validate_long<<<grid_for(ip[u + 1] - ip[u], 256), 256, 0, s>>>(g->indptr, g->eid, g->ts, u,
-                                                                       err);
-      after_launch("k_validate_long");
+  if (ip[0] != 0 || ip[static_cast<size_t>(g->V)] != g->m) return "indptr endpoints wrong";
+  int64_t u_mono = g->V;  // first node whose indptr pair decreases
+  for (int64_t u = 0; u < g->V; ++u)
+    if (ip[static_cast<size_t>(u)] > ip[static_cast<size_t>(u + 1)]) {
+      u_mono = u;
+      break;
     }
+  ensure_columns(g, s);
+  unsigned long long* fail = static_cast<unsigned long long*>(dmalloc(2 * sizeof(unsigned long long), s));
+  const unsigned long long none[2] = {~0ull, ~0ull};
+  TGFX_CUDA(cudaMemcpyAsync(fail, none, sizeof none, cudaMemcpyHostToDevice, s));
+  if (g->m > 0) {
+    k_validate<<<grid_for(g->m, 256), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts, u_mono,
+                                                  g->other_limit, g->eid_limit, g->m, fail,
+                                                  fail + 1);
+    after_launch("k_validate");
   }
-  int h = 0;
-  TGFX_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  unsigned long long h[2];
+  TGFX_CUDA(cudaMemcpyAsync(h, fail, sizeof h, cudaMemcpyDeviceToHost, s));
   TGFX_CUDA(cudaStreamSynchronize(s));
-  dfree(err, s);
-  switch (h) {  // messages of TCsr::validate (tcsr.cpp:54-81)
-    case 1: return "indptr endpoints wrong";
-    case 2: return "indptr not monotone";
-    case 3: return "slice not sorted";
-    case 4: return "neighbor id out of range";
-    case 5: return "edge id out of range";
-    default: return "";
-  }
+  dfree(fail, s);
+  // node loop: monotone check of u, then slice u (tcsr.cpp:64-72)
+  if (h[0] != ~0ull && static_cast<int64_t>(h[0]) < u_mono)
+    return "slice of node " + std::to_string(h[0]) + " not sorted";
+  if (u_mono < g->V) return "indptr not monotone";
+  // entry loop (tcsr.cpp:73-80)
+  if (h[1] != ~0ull) return (h[1] & 1) ? "edge id out of range" : "neighbor id out of range";
+  return "";
 }
 
 }  // namespace tgfx

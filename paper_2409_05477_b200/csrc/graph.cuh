@@ -1,6 +1,8 @@
 // graph.cuh -- the device-resident T-CSR handle and the builder / sampler entry points.
 #pragma once
 
+#include <mutex>
+
 #include "common.cuh"
 
 // Device-side build diagnostics, written by the histogram pass.
@@ -49,6 +51,9 @@ struct tgfx_graph {
   // the sampler replays std::lower_bound's exact bisection; 0: slices are sorted, any
   // bracketing search (interpolation) returns the same lower_bound.
   int search_exact = 0;
+  // 1: an imported indptr is not monotone within [0, m] (or has wrong endpoints); no node
+  // directory is built, samplers refuse the graph, validate() reports the reference's error
+  int indptr_bad = 0;
   int64_t* indptr = nullptr;
   int64_t* nbr = nullptr;
   int64_t* eid = nullptr;
@@ -66,6 +71,7 @@ struct tgfx_graph {
   // false: the last build wrote rec (+ ts) instead of the int64 nbr / eid columns; they are
   // widened from rec by ensure_columns before anything outside the sampler reads them
   bool cols_valid = true;
+  std::mutex cols_mu;  // serialises the lazy widening: a graph is shared by concurrent readers
   // bound on the other endpoint (nbr ids): V for an ordinary build; the global node count for
   // one node range of a partitioned build (reverse = 0, nbr ids stay global)
   int64_t other_limit = 0;
@@ -222,6 +228,7 @@ void launch_partition_scatter(const tgfx_event* ev, int64_t n, int reverse, cons
                               cudaStream_t s);
 // 1 if any ts is NaN
 bool any_nan(const double* ts, int64_t m, cudaStream_t s);
+bool indptr_in_range(const int64_t* indptr, int64_t V, int64_t m, cudaStream_t s);
 
 // ------------------------------------------------------------------ primitives
 // exclusive scan of n uint32 counts into int64 offsets (out has n+1 entries: out[n] = total)

@@ -134,6 +134,30 @@ __global__ void k_any_nan(const double* __restrict__ ts, int64_t m, int* flag) {
 
 }  // namespace
 
+__global__ void k_indptr_range(const int64_t* __restrict__ indptr, int64_t V, int64_t m,
+                               int* bad) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < V;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = indptr[u], hi = indptr[u + 1];
+    if (lo > hi || lo < 0 || hi > m || (u == 0 && lo != 0) || (u == V - 1 && hi != m)) *bad = 1;
+  }
+}
+
+// indptr[0] == 0, indptr[V] == m and monotone (so every slice lies inside [0, m])
+bool indptr_in_range(const int64_t* indptr, int64_t V, int64_t m, cudaStream_t s) {
+  if (V <= 0) return true;
+  int* d = static_cast<int*>(dmalloc(sizeof(int), s));
+  TGFX_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  k_indptr_range<<<static_cast<int>(std::min<int64_t>(ceil_div(V, 256), 4096)), 256, 0, s>>>(
+      indptr, V, m, d);
+  after_launch("k_indptr_range");
+  int h = 0;
+  TGFX_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaStreamSynchronize(s));
+  dfree(d, s);
+  return h == 0;
+}
+
 bool any_nan(const double* ts, int64_t m, cudaStream_t s) {
   if (m <= 0) return false;
   int* d = static_cast<int*>(dmalloc(sizeof(int), s));

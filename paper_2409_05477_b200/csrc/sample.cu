@@ -54,10 +54,12 @@ struct QueryIn {
 };
 
 // CounterRng(seed, stream) initial state of query qq (rng.hpp:23-24)
+// Dead lanes (qq >= Q) still evaluate it; their batch index is clamped to the last query's so
+// the seeds[] load stays inside the caller's array.
 __device__ __forceinline__ uint64_t query_rng(const QueryIn& in, uint64_t seed_mix,
-                                              uint64_t stream_base, int64_t qq) {
+                                              uint64_t stream_base, int64_t qq, int64_t Q) {
   if (in.seeds) {
-    const int64_t b = qq / in.batch_q;
+    const int64_t b = min(qq, Q - 1) / in.batch_q;
     return mix64(mix64(__ldg(reinterpret_cast<const unsigned long long*>(in.seeds) + b)) ^
                  (static_cast<uint64_t>(qq - b * in.batch_q) * kStreamMul));
   }
@@ -631,13 +633,76 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
 }
 
 // ------------------------------------------------------------------ uniform-k (Floyd)
-template <int P, bool ASSEMBLE, bool IDX64>
+// Floyd for any k (k > 256): the chosen offsets live in a per-warp open-addressing hash set
+// and list in global scratch (H + P2 u64 words, H = pow2 >= 2k, P2 = pow2 >= k).  Draws are
+// resolved 32 at a time: each lane looks its draw up in the set of earlier chunks, the chunk
+// itself is resolved in draw order by shuffles, then the chosen offsets are inserted.  The
+// list is bitonic-sorted in place, so out[r] is the r-th smallest offset (sampler.cpp:66-80).
+__device__ void floyd_big(uint64_t* __restrict__ hs, uint64_t* __restrict__ list, int64_t H,
+                          int64_t P2, uint64_t s0, int64_t qm, int kk, int lane) {
+  for (int64_t i = lane; i < H; i += 32) hs[i] = 0;
+  for (int64_t i = kk + lane; i < P2; i += 32) list[i] = ~0ull;
+  __syncwarp();
+  const int hbits = 63 - __clzll(static_cast<unsigned long long>(H));
+  auto slot = [&](uint64_t key) {
+    return static_cast<int64_t>((key * 0x9e3779b97f4a7c15ULL) >> (64 - hbits));
+  };
+  for (int d0 = 0; d0 < kk; d0 += 32) {
+    const int d = d0 + lane;
+    const bool live = d < kk;
+    const uint64_t top = static_cast<uint64_t>(qm - kk + d);
+    const uint64_t j = live ? mulhi64(rng_draw(s0, d), top + 1) : 0;
+    bool coll = false;
+    if (live) {  // chosen by an earlier chunk?
+      for (int64_t h = slot(j + 1);; h = (h + 1) & (H - 1)) {
+        const uint64_t v = hs[h];
+        if (v == 0) break;
+        if (v == j + 1) {
+          coll = true;
+          break;
+        }
+      }
+    }
+    const int nd = min(32, kk - d0);
+    for (int r = 0; r < nd; ++r) {  // lane r's choice is final once lanes < r are resolved
+      const uint64_t cr = __shfl_sync(kFull, coll ? top : j, r);
+      if (lane > r && j == cr) coll = true;
+    }
+    const uint64_t c = coll ? top : j;
+    if (live) {
+      list[d] = c;
+      for (int64_t h = slot(c + 1);; h = (h + 1) & (H - 1))
+        if (atomicCAS(reinterpret_cast<unsigned long long*>(hs + h), 0ull,
+                      static_cast<unsigned long long>(c + 1)) == 0ull)
+          break;
+    }
+    __syncwarp();
+  }
+  for (int64_t w = 2; w <= P2; w <<= 1) {  // bitonic sort, ascending
+    for (int64_t jj = w >> 1; jj > 0; jj >>= 1) {
+      for (int64_t i = lane; i < P2; i += 32) {
+        const int64_t x = i ^ jj;
+        if (x > i) {
+          const uint64_t a = list[i], b = list[x];
+          if (((i & w) == 0) ? (a > b) : (a < b)) {
+            list[i] = b;
+            list[x] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int P, bool ASSEMBLE, bool IDX64, bool BIG = false>
 __global__ void __launch_bounds__(kThreads) k_random(
     const int64_t* __restrict__ indptr, const NodeDir* __restrict__ dir,
     const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base, int exact,
-    Outs o, const uint4* __restrict__ rec) {
+    Outs o, const uint4* __restrict__ rec, uint64_t* __restrict__ scratch = nullptr,
+    int64_t H = 0, int64_t P2 = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ngroups = ceil_div(Q, 32);
   const int kk = static_cast<int>(k);
@@ -718,7 +783,42 @@ __global__ void __launch_bounds__(kThreads) k_random(
       }
       // Floyd: for d = 0..k-1, i_d = m-k+d, j_d = next_below(i_d+1); c_d = j_d unless already
       // chosen, then i_d.  Draws are independent of the resolution (one draw per iteration).
-      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq);
+      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq, Q);
+      if (BIG) {
+        const int64_t wid = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+        uint64_t* hs = scratch + wid * (H + P2);
+        uint64_t* list = hs + H;
+        floyd_big(hs, list, H, P2, s0, qm, kk, lane);
+        if (ASSEMBLE) {
+          const int kb = min(kk, l - 1);
+          const int drop = kk - kb;  // keep the most recent l-1 (sequence.cpp:70-71)
+          for (int j = lane; j < l; j += 32) {
+            if (j < kb) {
+              int64_t ni, ei;
+              double tv;
+              fetch_entry(rec, nbr, eid, ts, qlo + static_cast<int64_t>(list[drop + j]), ni, ei, tv);
+              write_slot<IDX64>(o, qq * l + j, ni + 1, ei + 1, qt - tv);
+            } else if (j == kb) {
+              write_slot<IDX64>(o, qq * l + j, qu + 1, self_idx, 0.0);
+            } else {
+              write_slot<IDX64>(o, qq * l + j, 0, 0, 0.0);
+            }
+          }
+          if (lane == 0) write_vlen<IDX64>(o, qq, kb + 1);
+        } else {
+          for (int r = lane; r < kk; r += 32) {
+            int64_t ni, ei;
+            double tv;
+            fetch_entry(rec, nbr, eid, ts, qlo + static_cast<int64_t>(list[r]), ni, ei, tv);
+            o.e_nbr[qq * k + r] = ni;
+            o.e_eid[qq * k + r] = ei;
+            o.e_ts[qq * k + r] = tv;
+          }
+          if (lane == 0) o.counts[qq] = kk;
+        }
+        __syncwarp();
+        continue;
+      }
       int64_t jd[P], c[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -926,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
       const double qt = live ? s_t[warp][qi] : 0.0;
       const bool floyd = pr && qm > k;
       // Floyd (all groups run the loop so the shuffles/ballots see every lane)
-      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq);
+      const uint64_t s0 = query_rng(in, seed_mix, stream_base, qq, Q);
       int64_t jd[P], c[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -1076,7 +1176,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_random_lane(
     const int kb = !pres[0] ? -1 : floyd ? min(k, l - 1) : min(static_cast<int>(qm), l - 1);
     // Floyd (sampler.cpp:66-80): draw d picks j in [0, qm - k + d]; a repeat takes qm - k + d
     uint32_t c[KM];
-    const uint64_t s0 = query_rng(in, seed_mix, stream_base, q);
+    const uint64_t s0 = query_rng(in, seed_mix, stream_base, q, Q);
 #pragma unroll
     for (int dd = 0; dd < KM; ++dd) {
       c[dd] = 0xffffffffu;
@@ -1200,7 +1300,31 @@ void launch_random_p(int P, const SampleArgs& a, const QueryIn& in, const Outs& 
     TGFX_RANDOM_CASE(2)
     TGFX_RANDOM_CASE(4)
     TGFX_RANDOM_CASE(8)
-    default: throw Error(TGFX_EUNSUPPORTED, "uniform sampling supports k <= 256");
+    default: {
+      // k > 256 (the reference has no limit, sampler.cpp:54-82): hash-set Floyd with per-warp
+      // global scratch; the grid is capped so the scratch stays within ~1 GB
+      if (a.k >= (int64_t(1) << 30)) throw Error(TGFX_EUNSUPPORTED, "k too large");
+      int64_t H = 1, P2 = 1;
+      while (H < 2 * a.k) H <<= 1;
+      while (P2 < a.k) P2 <<= 1;
+      const int64_t per_warp = (H + P2) * 8;
+      const int64_t max_warps = std::max<int64_t>(kWarps, (int64_t(1) << 30) / per_warp);
+      const int gb = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(grid, max_warps / kWarps)));
+      uint64_t* scratch = static_cast<uint64_t*>(
+          dmalloc(static_cast<size_t>(per_warp) * gb * kWarps, s));
+      k_random<1, ASM, I64, true><<<gb, kThreads, 0, s>>>(
+          g->indptr, g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l, a.self_edge_index, a.seed,
+          a.stream_base, g->search_exact, o, g->rec, scratch, H, P2);
+      try {
+        after_launch("k_random");
+      } catch (...) {
+        dfree(scratch, s);
+        throw;
+      }
+      dfree(scratch, s);
+      return;
+    }
   }
 #undef TGFX_RANDOM_CASE
   after_launch("k_random");
@@ -1232,6 +1356,8 @@ int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, c
 }
 
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
+  if (a.g->indptr_bad)  // an imported T-CSR whose indptr no slice walk can trust
+    throw Error(TGFX_EVALIDATION, "indptr not monotone");
   if (a.q <= 0) return;
   const tgfx_graph* g = a.g;
   QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q};
@@ -1366,6 +1492,7 @@ void launch_two_hop(const tgfx_graph* g, const int64_t* roots, const double* tim
                     int64_t l, int64_t self_edge_index, int32_t* h1n, int32_t* h1e, float* h1d,
                     int32_t* h1l, int32_t* h2n, int32_t* h2e, float* h2d, int32_t* h2l,
                     cudaStream_t s) {
+  if (g->indptr_bad) throw Error(TGFX_EVALIDATION, "indptr not monotone");
   if (q <= 0) return;
   // hop-1 rows
   SampleArgs a{};

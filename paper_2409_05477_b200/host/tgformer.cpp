@@ -19,14 +19,16 @@ namespace tgf {
 namespace detail {
 
 // Rethrow a libtgfx status as the reference's exception type (common.hpp:15-27).
-void check(int rc) {
-  if (rc == TGFX_OK) return;
-  const std::string msg = tgfx_last_error();
+[[noreturn]] void throw_status(int rc, const std::string& msg) {
   if (rc == TGFX_EVALIDATION) throw ValidationError(msg);
   if (rc == TGFX_EFORMAT) throw FormatError(msg);
   if (rc == TGFX_EPARSE) throw ParseError(msg);
   if (rc == TGFX_ENOMEM) throw std::bad_alloc();
   throw std::runtime_error(msg);
+}
+
+void check(int rc) {
+  if (rc != TGFX_OK) throw_status(rc, tgfx_last_error());
 }
 
 // Content fingerprint of the host columns: full FNV-1a over small graphs, a strided sample
@@ -56,7 +58,6 @@ std::uint64_t fingerprint(const TCsr& g) {
 }
 
 struct DeviceCopy {
-  std::mutex mu;
   tgfx_graph* handle = nullptr;
   std::uint64_t fp = 0;
   std::int64_t max_degree = 0;
@@ -71,11 +72,31 @@ std::int64_t max_degree(const TCsr& g) {
   return d;
 }
 
-void attach(const TCsr& g, tgfx_graph* h) {
+// A TCsr is shared by concurrent readers: every read or replacement of its
+// device_copy pointer, and every first upload, happens under this lock.  Callers hold the
+// returned shared_ptr while they use the handle, so a concurrent replacement cannot free it.
+std::mutex& copy_mu() {
+  static std::mutex mu;
+  return mu;
+}
+
+std::shared_ptr<DeviceCopy> make_copy(const TCsr& g, tgfx_graph* h) {
   auto dc = std::make_shared<DeviceCopy>();
   dc->handle = h;
   dc->fp = fingerprint(g);
   dc->max_degree = max_degree(g);
+  return dc;
+}
+
+void attach(const TCsr& g, tgfx_graph* h) {
+  std::shared_ptr<DeviceCopy> dc;
+  try {
+    dc = make_copy(g, h);
+  } catch (...) {
+    tgfx_graph_free(h);
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(copy_mu());
   g.device_copy = std::move(dc);
 }
 
@@ -103,13 +124,24 @@ tgfx_graph* upload(const TCsr& g) {
   return h;
 }
 
-DeviceCopy& device_of(const TCsr& g) {
+// The device copy to sample from.  The fingerprint samples large columns (see fingerprint),
+// so an in-place edit of a few entries after the copy exists can go unnoticed here: a TCsr
+// must not be edited once sampled (the reference treats it as immutable).  validate() always
+// checks freshly uploaded columns (TCsr::validate below).
+std::shared_ptr<DeviceCopy> device_of(const TCsr& g) {
+  std::lock_guard<std::mutex> lk(copy_mu());
   std::shared_ptr<DeviceCopy> dc = g.device_copy;
   if (!dc || dc->fp != fingerprint(g)) {
-    attach(g, upload(g));
-    dc = g.device_copy;
+    tgfx_graph* h = upload(g);
+    try {
+      dc = make_copy(g, h);
+    } catch (...) {
+      tgfx_graph_free(h);
+      throw;
+    }
+    g.device_copy = dc;
   }
-  return *dc;
+  return dc;
 }
 
 }  // namespace detail
@@ -153,7 +185,7 @@ EventStream load_csv(const std::string& path, bool has_features) {
 }
 
 // ------------------------------------------------------------------ T-CSR
-tgfx_graph* TCsr::device() const { return detail::device_of(*this).handle; }
+tgfx_graph* TCsr::device() const { return detail::device_of(*this)->handle; }
 
 void TCsr::validate() const {
   // tcsr.cpp:54-81: shape checks on the host, the O(m) scans on the device
@@ -163,7 +195,16 @@ void TCsr::validate() const {
     throw ValidationError("indptr endpoints wrong");
   if (edge_ids.size() != neighbor_ids.size() || timestamps.size() != neighbor_ids.size())
     throw ValidationError("column arrays disagree in length");
-  detail::check(tgfx_graph_validate(device()));
+  // the O(m) checks run on a fresh upload of the host columns, so an edit made after the
+  // device copy was attached is always seen (the reference validates the vectors themselves)
+  tgfx_graph* h = detail::upload(*this);
+  const int rc = tgfx_graph_validate(h);
+  if (rc != TGFX_OK) {
+    const std::string msg = tgfx_last_error();
+    tgfx_graph_free(h);
+    detail::throw_status(rc, msg);
+  }
+  detail::attach(*this, h);  // the validated copy replaces any older one
 }
 
 namespace {
@@ -346,7 +387,8 @@ namespace {
 std::vector<NeighborSample> run_batch(const TCsr& g, const NodeId* nodes, const Time* times,
                                       std::int64_t q, std::int64_t k, SampleStrategy strategy,
                                       std::uint64_t seed, std::uint64_t stream_base) {
-  detail::DeviceCopy& dc = detail::device_of(g);
+  const std::shared_ptr<detail::DeviceCopy> dcp = detail::device_of(g);
+  const detail::DeviceCopy& dc = *dcp;
   // padded output width: no query can return more than the longest slice, so a huge k
   // (sample_recent(g, u, t, 1 << 30)) does not size the buffers; results are unchanged
   const std::int64_t kpad = k < 1 ? k : std::max<std::int64_t>(1, std::min(k, dc.max_degree));
