@@ -116,49 +116,75 @@ def dist_setup():
 
 
 # ------------------------------------------------------------------------------ CPU reference
-def reference_sample(cfg, sample_events, ev_host, threads):
-    """Reference CPU path (oracle/_ref = /root/reference/proj/src compiled) on the first
-    `sample_events` events of the workload stream: build (faster of build_sequential and
-    build_parallel(threads)) + sample_batch/build_sequence_batch of all their queries in the
-    forward_concat layout, batch by batch as forward_concat calls it (seed 9 + batch index)."""
-    from oracle import oracle as O
-    ev = ev_host[:sample_events]
-    rs = O.RefStream(ev, cfg["V"])
-    _, t_seq = rs.build(True, 0)
-    rg, t_par = rs.build(True, threads)
-    t_build = min(t_seq, t_par)
-    nodes, times = O.make_queries(ev, 0, sample_events, cfg["B"], cfg["V"], NEG_SEED)
-    qb = 3 * cfg["B"]
-    # per forward_concat batch the reference is called with 3B queries; to keep the sample
-    # bounded and the per-call overhead faithful we time calls of qb queries
-    t_sample = 0.0
-    for b, s in enumerate(range(0, len(nodes), qb)):
-        _, ts = O.ref_sample_assemble(rg, nodes[s:s + qb], times[s:s + qb], cfg["k"],
-                                      cfg["strategy"], 9 + b, cfg["l"], cfg["E"] + 1,
-                                      threads=threads, want_outputs=False)
-        t_sample += ts
-    q = len(nodes)
-    return dict(build_s=t_build, build_seq_s=t_seq, build_par_s=t_par, sample_s=t_sample,
-                events=sample_events, queries=q,
-                value=sample_events / (t_build + t_sample),
-                build_edges_per_s=sample_events / t_build, sample_queries_per_s=q / t_sample)
+def reference_full(cfg, threads, steps, warmup, ev_host=None, builds=("sequential", "parallel"),
+                   batches_per_step=64):
+    """The reference's own CPU path (oracle/_ref: /root/reference/proj/src compiled, loaded in
+    the build for this host's CPU when it can run it) on the SAME workload as the GPU arm:
 
+      * stream: the full make_random_stream(E, V, 42) -- generated by the reference's own
+        generator unless ev_host is given;
+      * build: one full reverse=1 build of all E events, timed once per run (build_sequential,
+        and build_parallel(threads) -- the faster one counts);
+      * sampling: forward_concat batches (3B queries: [src | dst | neg], seed 9 + batch index,
+        sample_batch + build_sequence_batch as training.cpp:211-214 calls them) spread evenly
+        over the WHOLE stream, `batches_per_step` per step, `warmup` untimed + `steps` timed;
+        the per-query time of the timed steps is extrapolated to all 3E queries.
 
-def host_events(cfg, n):
-    """First n events of make_random_stream(E, V, 42) -- generated on the device (bit-identical
-    to the reference generator) and copied to the host."""
-    import torch
-    from paper_2409_05477_b200 import device as D
-    ev = D.random_stream(cfg["E"], cfg["V"], SEED)
-    out = ev[: n * 32].cpu().numpy().view(_event_dtype())
-    del ev
-    torch.cuda.empty_cache()
-    return out
-
-
-def _event_dtype():
+    value = E / (t_build + t_query * 3E): events through build + sampling per second."""
     import numpy as np
-    return np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
+    from oracle import oracle as O
+    O.ref(native=True)
+    E, V, B = cfg["E"], cfg["V"], cfg["B"]
+    t0 = time.perf_counter()
+    if ev_host is None:
+        ev_host = O.ref_make_random_stream(E, V, SEED)
+    t_gen = time.perf_counter() - t0
+    rs = O.RefStream(ev_host, V)
+    bt = {}
+    rg = None
+    for kind in builds:
+        g, secs = rs.build(True, 0 if kind == "sequential" else threads)
+        bt[kind] = secs
+        if rg is None:
+            rg = g  # both builders return the same T-CSR
+        del g
+    t_build = min(bt.values())
+    del rs
+    nbatch = -(-E // B)
+    per_step = []
+    for s in range(warmup + steps):
+        # batch indices spread over the stream; each step a different evenly spaced set
+        frac = (s + 0.5) / (warmup + steps)
+        bs = sorted({min(nbatch - 1, int((j + frac) * nbatch / batches_per_step))
+                     for j in range(batches_per_step)})
+        tq, nq = 0.0, 0
+        for b in bs:
+            e0, e1 = b * B, min(E, (b + 1) * B)
+            nodes, times = O.make_queries(ev_host, e0, e1, B, V, NEG_SEED)
+            _, secs = O.ref_sample_assemble(rg, nodes, times, cfg["k"], cfg["strategy"], 9 + b,
+                                            cfg["l"], E + 1, threads=threads, want_outputs=False)
+            tq += secs
+            nq += len(nodes)
+        if s >= warmup:
+            per_step.append((tq, nq))
+    tq = sum(t for t, _ in per_step)
+    nq = sum(n for _, n in per_step)
+    t_query = tq / max(nq, 1)
+    Q = 3 * E
+    total = t_build + t_query * Q
+    return dict(value=E / total, total_s=total, build_s=t_build, builds=bt, gen_s=t_gen,
+                t_query=t_query, queries_timed=nq, batches_timed=len(per_step) * batches_per_step,
+                build_edges_per_s=E / t_build, sample_queries_per_s=1.0 / t_query,
+                so=os.path.basename(O._ref_path or ""))
+
+
+def reference_sample_text(cfg, r, threads):
+    bt = ", ".join(f"{k} {v:.2f}s" for k, v in r["builds"].items())
+    return (f"full {cfg['name']} stream ({cfg['E']:,} events): one reference build of all events "
+            f"timed once ({bt}; the faster counts) + sample_batch+build_sequence_batch of "
+            f"{r['queries_timed']:,} forward_concat queries from {r['batches_timed']} batches "
+            f"spread over the whole stream ({threads} threads), per-query time extrapolated to "
+            f"all {3 * cfg['E']:,} queries; reference compiled {r['so']}")
 
 
 def run_reference(args, cfg):
@@ -166,31 +192,25 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     threads = len(os.sched_getaffinity(0))
-    import torch
-    torch.cuda.set_device(local)
-    n = args.cpu_events
-    ev_host = host_events(cfg, n)
-    for _ in range(args.warmup):
-        reference_sample(cfg, n, ev_host, threads)
-    runs = [reference_sample(cfg, n, ev_host, threads) for _ in range(args.steps)]
-    tot = sum(r["build_s"] + r["sample_s"] for r in runs)
-    value = n * len(runs) / tot
-    sample = (f"first {n:,} events of the {cfg['name']} stream: reference build (faster of "
-              f"build_sequential / build_parallel({threads})) + sample_batch+build_sequence_batch "
-              f"of their {runs[0]['queries']:,} queries, {threads} threads")
+    r = reference_full(cfg, threads, args.steps, args.warmup)
+    value = r["value"]
     line = {
         "impl": "reference", "metric": metric_name(cfg), "value": value, "unit": "edges/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * tot / len(runs), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
+        "ms_per_step": 1000 * r["total_s"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic (reference generator)",
         "config": dict(config_obj(cfg, ws), parallelism=(
-            f"reference CPU path (oracle/_ref, /root/reference/proj/src compiled), {threads} host "
-            f"threads on rank 0" + (f"; ranks 1..{ws - 1} idle" if ws > 1 else ""))),
+            f"reference CPU path (oracle/_ref, /root/reference/proj/src compiled -O3 "
+            f"-march for this host), {threads} host threads on rank 0"
+            + (f"; ranks 1..{ws - 1} idle" if ws > 1 else ""))),
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": reference_sample_text(cfg, r, threads)},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "build_edges_per_s": statistics.median(r["build_edges_per_s"] for r in runs),
-        "sample_queries_per_s": statistics.median(r["sample_queries_per_s"] for r in runs),
+        "same_config": True,
+        "extrapolation": "ms_per_step = build (timed once) + per-query sampling time x 3E",
+        "build_s": r["build_s"], "builds_s": r["builds"],
+        "build_edges_per_s": r["build_edges_per_s"],
+        "sample_queries_per_s": r["sample_queries_per_s"],
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -355,7 +375,7 @@ def run_ours(args, cfg):
     }
     ev_host = None
     if rank == 0 and not args.no_cpu:
-        ev_host = ev[: args.cpu_events * 32].cpu().numpy().view(_event_dtype())
+        ev_host = ev.cpu().numpy().view(_event_dtype())  # bit-identical to the reference's
     if not args.no_e2e:
         # the device-resident run's graph, rows and inputs are not part of the e2e path: the
         # e2e step starts from the device memory a fresh host-buffer caller would have
@@ -371,15 +391,14 @@ def run_ours(args, cfg):
             line["e2e"] = e2e
     if rank == 0 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        r = reference_sample(cfg, args.cpu_events, ev_host, threads)
+        r = reference_full(cfg, threads, steps=3, warmup=1, ev_host=ev_host,
+                           builds=("sequential",), batches_per_step=48)
         line["cpu_baseline"] = {
             "value": r["value"], "unit": "edges/s", "cores": threads, "kind": "reference",
-            "sample": (f"first {r['events']:,} events of the same stream: reference build "
-                       f"({r['build_s']:.3f}s, faster of sequential {r['build_seq_s']:.3f}s / "
-                       f"parallel({threads}) {r['build_par_s']:.3f}s) + sample_batch+"
-                       f"build_sequence_batch of {r['queries']:,} queries ({r['sample_s']:.3f}s)"),
+            "sample": reference_sample_text(cfg, r, threads),
             "build_edges_per_s": r["build_edges_per_s"],
             "sample_queries_per_s": r["sample_queries_per_s"]}
+        del ev_host
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -496,7 +515,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="G", choices=sorted(CONFIGS))
     ap.add_argument("--chunk", type=int, default=3 * 8_000_000)
-    ap.add_argument("--cpu-events", type=int, default=4_000_000)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

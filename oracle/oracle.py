@@ -19,6 +19,26 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libtgf_ref.so")
+# the same reference build for the GPU box's host CPU (Emerald Rapids): -march=native there
+REF_SO_NATIVE = os.path.join(HERE, "_ref", "libtgf_ref_emr.so")
+
+
+def host_has_native_isa():
+    """True when this CPU runs the -march=emeraldrapids build (AMX + AVX512-FP16 present)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((ln for ln in f if ln.startswith("flags")), "")
+    except OSError:
+        return False
+    need = ("avx512_fp16", "amx_tile", "avx512_bf16", "avx512_vbmi2", "avx_vnni", "movdir64b")
+    return all(n in flags.split() for n in need)
+
+
+def ref_so_path(native=False):
+    """native=True: the box-tuned build when it exists and this CPU can run it."""
+    if native and os.path.exists(REF_SO_NATIVE) and host_has_native_isa():
+        return REF_SO_NATIVE
+    return REF_SO
 
 EVENT_DTYPE = np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
 
@@ -80,13 +100,19 @@ def ref_available():
     return os.path.exists(REF_SO)
 
 
-def ref():
-    """The reference's own hot path (compiled from /root/reference by oracle/Makefile)."""
-    global _ref
+_ref_path = None
+
+
+def ref(native=False):
+    """The reference's own hot path (compiled from /root/reference by oracle/Makefile).
+    native=True (first call only) loads the build tuned for the GPU box's host CPU."""
+    global _ref, _ref_path
     if _ref is None:
-        if not os.path.exists(REF_SO):
-            raise RuntimeError(f"reference build {REF_SO} missing (run make -C oracle)")
-        L = C.CDLL(REF_SO)
+        path = ref_so_path(native)
+        if not os.path.exists(path):
+            raise RuntimeError(f"reference build {path} missing (run make -C oracle)")
+        L = C.CDLL(path)
+        _ref_path = path
         L.ref_last_error.restype = C.c_char_p
         L.ref_make_random_stream.argtypes = [_I64, _I64, _U64, C.c_double, _P]
         L.ref_stream_create.restype = _P
