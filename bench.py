@@ -281,6 +281,13 @@ def run_ours(args, cfg):
     g = D.build(ev, V, True)
     torch.cuda.synchronize()
 
+    # stratified row sample per chunk (64 rows) whose device-path result the e2e leg's host
+    # rows are checked against on every e2e step
+    rng = np.random.default_rng(1234)
+    probe = [np.sort(np.unique(((np.arange(64) + rng.random(64)) * (e - s) / 64).astype(np.int64)))
+             for s, e in chunks]
+    expect = []
+
     def one_step(record=None, taken=None):
         if record:
             record["b0"].record(stream)
@@ -297,6 +304,8 @@ def run_ours(args, cfg):
                 record["c"][i][1].record(stream)
             if taken is not None:
                 taken.append(int(sub["valid_len"].sum().item()) - (e - s))
+                ix = torch.from_numpy(probe[i]).to(sub["valid_len"].device)
+                expect.append({kk: vv[ix].cpu().numpy() for kk, vv in sub.items()})
 
     taken = []
     for w in range(args.warmup):
@@ -386,9 +395,11 @@ def run_ours(args, cfg):
         gc.collect()
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-        e2e = run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red)
+        e2e = run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red, probe, expect)
         if rank == 0:
             line["e2e"] = e2e
+    if rank == 0 and not args.no_e2e:
+        line["e2e_cpp"] = run_e2e_cpp(cfg)
     if rank == 0 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         r = reference_full(cfg, threads, steps=3, warmup=1, ev_host=ev_host,
@@ -421,7 +432,33 @@ def load_traffic(cfg, bytes_per_launch):
         return None
 
 
-def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda"):
+def run_e2e_cpp(cfg, batches=2000, warmup=50):
+    """The drop-in C++ route (tools/forward_concat_bench.cpp, linked against libtgformer.so):
+    tgf::build_parallel of the whole stream + forward_concat's per-batch pair
+    tgf::sample_batch -> tgf::build_sequence_batch ("exact"), and the one-call
+    tgf::sample_sequence_batch ("fused"), on forward_concat batches spread over the stream,
+    per-query time extrapolated to all 3E queries.  Wall clock, host vectors in and out."""
+    exe = os.path.join(ROOT, "paper_2409_05477_b200", "lib", "forward_concat_bench")
+    out = {}
+    for mode, name in ((0, "exact"), (1, "fused")):
+        try:
+            r = subprocess.run([exe, str(cfg["E"]), str(cfg["V"]), str(cfg["k"]), str(cfg["l"]),
+                                str(cfg["B"]), cfg["strategy"], str(batches), str(warmup),
+                                str(mode)], capture_output=True, text=True, timeout=600)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # report, do not fail the bench line
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+            continue
+        d["path"] = ("tgf::build_parallel + per batch tgf::sample_batch -> "
+                     "tgf::build_sequence_batch (training.cpp:211-214)" if mode == 0 else
+                     "tgf::build_parallel + per batch tgf::sample_sequence_batch")
+        d["extrapolation"] = (f"{batches} forward_concat batches of {3 * cfg['B']} queries spread "
+                              f"over the stream; per-query time x {3 * cfg['E']:,} queries")
+        out[name] = d
+    return out
+
+
+def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda", probe=None, expect=None):
     """Same step through the C ABI with HOST buffers (pinned): tgfx_build_parallel from host
     events, then tgfx_sample_assemble per chunk with host queries and host outputs.  At N > 1
     every rank runs it at once (PCIe and host memory are shared, as in a real job) when the
@@ -468,15 +505,36 @@ def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda"):
     strat = 0 if cfg["strategy"] == "recent" else 1
     P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 
+    # numpy views of the pinned outputs: the probe rows of each chunk are copied aside right
+    # after its call (a few KB) and checked against the device path after the step
+    v_n, v_e, v_d, v_v = (t.numpy() for t in (o_n, o_e, o_d, o_v))
+    got = [None] * len(chunks)
+    checked = [0, 0]  # rows, mismatching rows
+
     def step():
         h = C.c_void_p()
         _lib.check(L.tgfx_build_parallel(P(h_ev), E, V, 1, 1, C.byref(h)))
-        for s, e in chunks:
+        for i, (s, e) in enumerate(chunks):
             _lib.check(L.tgfx_sample_assemble(
                 h, C.c_void_p(h_nodes.data_ptr() + 8 * (s - lo)),
                 C.c_void_p(h_times.data_ptr() + 8 * (s - lo)), e - s, k, strat, 9, s, l, E + 1,
                 P(o_n), P(o_e), P(o_d), None, P(o_v)))
+            if probe is not None:
+                ix = probe[i]
+                got[i] = (v_n.reshape(-1, l)[ix].copy(), v_e.reshape(-1, l)[ix].copy(),
+                          v_d.reshape(-1, l)[ix].copy(), v_v[ix].copy())
         _lib.check(L.tgfx_graph_free(h))
+
+    def verify():
+        if probe is None or expect is None:
+            return
+        for i in range(len(chunks)):
+            n_, e_, d_, v_ = got[i]
+            want = expect[i]
+            bad = ~((n_ == want["node_index"]).all(1) & (e_ == want["edge_index"]).all(1) &
+                    (d_ == want["time_delta"]).all(1) & (v_ == want["valid_len"]))
+            checked[0] += len(v_)
+            checked[1] += int(bad.sum())
 
     step()  # warm-up
     n_steps = max(1, min(args.steps, args.e2e_steps))
@@ -490,6 +548,10 @@ def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda"):
         t0 = time.perf_counter()
         step()
         times_s.append(time.perf_counter() - t0)
+        verify()  # outside the timed region
+    if checked[1]:
+        raise RuntimeError(f"e2e host rows differ from the device path: {checked[1]} of "
+                           f"{checked[0]} probe rows")
     dt = statistics.median(times_s)
     from paper_2409_05477_b200 import shard as S
     dt = S.max_over_ranks([dt], device=red)[0]
@@ -504,7 +566,8 @@ def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda"):
             "h2d_bytes_per_step": nr * 32 * E + 16 * q_all,  # every rank uploads the stream
             "d2h_bytes_per_step": (12 * l + 4) * q_all,
             "path": "C ABI host-buffer calls tgfx_build_parallel + tgfx_sample_assemble "
-                    "(pinned host memory), wall clock, max over ranks"}
+                    "(pinned host memory), wall clock, max over ranks",
+            "checked_rows": checked[0], "mismatched_rows": checked[1]}
 
 
 def main():

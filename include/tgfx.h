@@ -171,6 +171,17 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
                          uint64_t stream_base, int64_t l, int64_t self_edge_index,
                          int32_t* node_index, int32_t* edge_index, float* dt32, double* dt64,
                          int32_t* valid_len);
+/* build_sequence_batch(sample_batch(g, nodes, times, k, strategy, seed), l, self_edge_index)
+ * in the reference's own SequenceBatch types (sequence.hpp:20-30): node_index / edge_index
+ * int64 [q, l], time_delta double [q, l], valid_len / target_row int64 [q].  Errors in the
+ * reference's order: every query node, then k (sampler.cpp:88-93), then l (sequence.cpp:57).
+ * Backs tgf::sample_sequence_batch, the one-call form of forward_concat's pair
+ * (training.cpp:211-214). */
+int tgfx_sample_sequence_batch(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                               int64_t q, int64_t k, int strategy, uint64_t seed,
+                               uint64_t stream_base, int64_t l, int64_t self_edge_index,
+                               int64_t* node_index, int64_t* edge_index, double* time_delta,
+                               int64_t* valid_len, int64_t* target_row);
 /* device variant; with TGFX_INDEX64 the node_index / edge_index / valid_len pointers are
  * int64_t* (the reference's SequenceBatch types). */
 int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,

@@ -208,6 +208,16 @@ SequenceBatch build_sequence_batch(const std::vector<NeighborSample>& samples, s
                                    std::int64_t self_edge_index);
 Matrix build_mask(const SequenceBatch& batch, MaskKind kind);
 
+// Extension (not in the reference): the one-call form of forward_concat's pair
+// (training.cpp:211-214),
+//   build_sequence_batch(sample_batch(g, nodes, times, k, strategy, seed), l, self_edge_index)
+// with identical results and errors, computed on the device without materialising
+// NeighborSamples on the host.  A caller swaps the two calls for this one.
+SequenceBatch sample_sequence_batch(const TCsr& g, const std::vector<NodeId>& nodes,
+                                    const std::vector<Time>& times, std::int64_t k,
+                                    SampleStrategy strategy, std::uint64_t seed, std::int64_t l,
+                                    std::int64_t self_edge_index, int num_threads = 0);
+
 // ------------------------------------------------------------------ synthetic.hpp
 EventStream make_random_stream(std::int64_t num_edges, NodeId num_nodes, std::uint64_t seed,
                                double zipf_exponent = 1.2);

@@ -1060,6 +1060,51 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
   });
 }
 
+int tgfx_sample_sequence_batch(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                               int64_t q, int64_t k, int strategy, uint64_t seed,
+                               uint64_t stream_base, int64_t l, int64_t self_edge_index,
+                               int64_t* node_index, int64_t* edge_index, double* time_delta,
+                               int64_t* valid_len, int64_t* target_row) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = 0;
+    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
+    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
+    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
+    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
+    check_queries(g, dn.as<int64_t>(), q, k, s);  // sampler.cpp:88-93 (k only if q > 0)
+    check_l(l);                                   // sequence.cpp:57, after sampling's checks
+    if (q <= 0) return;
+    const size_t ql = qb * static_cast<size_t>(l);
+    DBuf on(8 * ql, s), oe(8 * ql, s), od(8 * ql, s), ov(8 * qb, s);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = dn.as<int64_t>();
+    a.times = dt.as<double>();
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.l = l;
+    a.self_edge_index = self_edge_index;
+    a.node_index = on.p;
+    a.edge_index = oe.p;
+    a.dt32 = nullptr;
+    a.dt64 = od.as<double>();
+    a.valid_len = ov.p;
+    a.index64 = true;
+    launch_sample(a, s);
+    d2h(node_index, on.p, 8 * ql, s);
+    d2h(edge_index, oe.p, 8 * ql, s);
+    d2h(time_delta, od.p, 8 * ql, s);
+    d2h(valid_len, ov.p, 8 * qb, s);
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    if (target_row)
+      for (int64_t b = 0; b < q; ++b) target_row[b] = valid_len[b] - 1;  // sequence.cpp:83
+  });
+}
+
 int tgfx_sample_two_hop_device(const tgfx_graph* g, const int64_t* d_roots, const double* d_times,
                                int64_t q, int64_t k1, int64_t k2, int strategy, uint64_t seed,
                                uint64_t seed2, int64_t l, int64_t self_edge_index,

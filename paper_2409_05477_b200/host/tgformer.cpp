@@ -514,6 +514,33 @@ SequenceBatch build_sequence_batch(const std::vector<NeighborSample>& samples, s
   return out;
 }
 
+SequenceBatch sample_sequence_batch(const TCsr& g, const std::vector<NodeId>& nodes,
+                                    const std::vector<Time>& times, std::int64_t k,
+                                    SampleStrategy strategy, std::uint64_t seed, std::int64_t l,
+                                    std::int64_t self_edge_index, int num_threads) {
+  (void)num_threads;
+  if (nodes.size() != times.size())
+    throw ValidationError("node and time lists differ in length");  // sampler.cpp:88-90
+  const std::shared_ptr<detail::DeviceCopy> dc = detail::device_of(g);
+  const std::int64_t q = static_cast<std::int64_t>(nodes.size());
+  const std::size_t qs = nodes.size();
+  SequenceBatch out;
+  out.batch = q;
+  out.l = l;
+  const std::size_t ql = qs * static_cast<std::size_t>(l > 0 ? l : 0);
+  out.node_index.resize(ql);
+  out.edge_index.resize(ql);
+  out.time_delta = Matrix(qs, static_cast<std::size_t>(l > 0 ? l : 0));
+  out.valid_len.resize(qs);
+  out.target_row.resize(qs);
+  detail::check(tgfx_sample_sequence_batch(
+      dc->handle, nodes.data(), times.data(), q, k,
+      strategy == SampleStrategy::recent ? TGFX_RECENT : TGFX_RANDOM, seed, 0, l,
+      self_edge_index, out.node_index.data(), out.edge_index.data(), out.time_delta.data(),
+      out.valid_len.data(), out.target_row.data()));
+  return out;
+}
+
 SequenceBatch build_sequence(const NeighborSample& sample, std::int64_t l,
                              std::int64_t self_edge_index) {
   return build_sequence_batch(std::vector<NeighborSample>{sample}, l, self_edge_index);

@@ -148,3 +148,40 @@ TEST_CASE("hand-assembled and edited TCsr re-upload") {
   CHECK(s.neighbors[0].timestamp == 4.5);
   CHECK(tgf::sample_recent(g, 0, 4.55, 5).neighbors.size() == 1);  // original untouched: t=3
 }
+
+TEST_CASE("sample_sequence_batch equals build_sequence_batch(sample_batch(...))") {
+  const tgf::EventStream st = tgf::make_random_stream(20000, 120, 5);
+  const tgf::TCsr g = tgf::build_parallel(st, true, 4);
+  std::vector<tgf::NodeId> nodes;
+  std::vector<tgf::Time> times;
+  for (int i = 0; i < 3000; i += 3) {
+    nodes.push_back(st.events[i].src);
+    nodes.push_back(st.events[i].dst);
+    times.push_back(st.events[i].timestamp);
+    times.push_back(st.events[i].timestamp + 0.5);
+  }
+  for (auto strat : {tgf::SampleStrategy::recent, tgf::SampleStrategy::random}) {
+    for (std::int64_t k : {1, 10, 20, 300}) {
+      const auto two = tgf::build_sequence_batch(tgf::sample_batch(g, nodes, times, k, strat, 9),
+                                                 11, 20001);
+      const auto one = tgf::sample_sequence_batch(g, nodes, times, k, strat, 9, 11, 20001);
+      CHECK(one.node_index == two.node_index);
+      CHECK(one.edge_index == two.edge_index);
+      CHECK(one.time_delta == two.time_delta);
+      CHECK(one.valid_len == two.valid_len);
+      CHECK(one.target_row == two.target_row);
+      one.validate();
+    }
+  }
+  std::vector<tgf::NodeId> bad = nodes;
+  bad[5] = 999;
+  CHECK_THROWS_AS(tgf::sample_sequence_batch(g, bad, times, 5, tgf::SampleStrategy::recent, 0,
+                                             11, 1),
+                  tgf::ValidationError);
+  CHECK_THROWS_AS(tgf::sample_sequence_batch(g, nodes, times, 0, tgf::SampleStrategy::recent, 0,
+                                             11, 1),
+                  tgf::ValidationError);
+  CHECK_THROWS_AS(tgf::sample_sequence_batch(g, nodes, times, 5, tgf::SampleStrategy::recent, 0,
+                                             1, 1),
+                  tgf::ValidationError);
+}
