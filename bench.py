@@ -178,6 +178,11 @@ def reference_full(cfg, threads, steps, warmup, ev_host=None, builds=("sequentia
                 so=os.path.basename(O._ref_path or ""))
 
 
+def _event_dtype():
+    import numpy as np
+    return np.dtype([("edge_id", "<i8"), ("src", "<i8"), ("dst", "<i8"), ("timestamp", "<f8")])
+
+
 def reference_sample_text(cfg, r, threads):
     bt = ", ".join(f"{k} {v:.2f}s" for k, v in r["builds"].items())
     return (f"full {cfg['name']} stream ({cfg['E']:,} events): one reference build of all events "
