@@ -665,6 +665,111 @@ __global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ i
   }
 }
 
+// K3 "warp chunks" (TGFX_SCATTER_VARIANT=20): one warp per CTA, several CTAs per SM, each
+// owning a contiguous chunk of the stream and a PRIVATE cursor table for all V nodes in shared
+// memory (bit 31 = cold flag).  Because no other warp touches the table, a chunk is processed
+// strictly sequentially in emission order, 32 entries per step, with no block barriers and no
+// sort: lanes of one node are grouped by one MATCH.ANY, an entry's position is the node's
+// cursor + its rank among the group's lower lanes, and the group's highest lane advances the
+// cursor.  Events arrive through a private ring of bulk copies (cp.async.bulk + mbarrier).
+constexpr int kWStages = 2;
+constexpr int kWTE = 96;  // events per stage (3 KB): the cursor table leaves little room
+
+size_t warp_scatter_smem(int64_t V) {
+  const int64_t vpad = (V + 31) & ~31LL;
+  return static_cast<size_t>(kWStages) * kWTE * 32 + 64 + static_cast<size_t>(vpad) * 4;
+}
+
+template <int R>
+__global__ void __launch_bounds__(32) k_scatter_warp(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+    ulonglong2* __restrict__ cold_img, double* __restrict__ ts_out, uint4* __restrict__ rec_out,
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kWStages * kWTE * 32);
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(bars + 8);
+  const int lane = threadIdx.x;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  if (e0 >= e1) return;
+  const int64_t ntiles = ceil_div(e1 - e0, kWTE);
+  if (lane == 0) {
+    for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kWStages && s < ntiles; ++s) {
+      const int64_t b = e0 + static_cast<int64_t>(s) * kWTE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kWTE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[s], bytes);
+      bulk_g2s(stage + s * kWTE, ev + b, bytes, &bars[s]);
+    }
+  }
+  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
+  for (int i = lane; i < V; i += 32) {
+    const uint32_t cold = (__ldg(coldbits_g + (i >> 5)) >> (i & 31)) & 1u;
+    cursor[i] = __ldg(orow + i) | (cold << 31);
+  }
+  __syncwarp();
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int sidx = static_cast<int>(it % kWStages);
+    const uint32_t phase = static_cast<uint32_t>((it / kWStages) & 1);
+    const int64_t tb = e0 + it * kWTE;
+    const int ent = static_cast<int>(min(static_cast<int64_t>(kWTE), e1 - tb)) * R;
+    const tgfx_event* sev = stage + sidx * kWTE;
+    mbar_wait(&bars[sidx], phase);
+#pragma unroll 2
+    for (int j0 = 0; j0 < ent; j0 += 32) {
+      const int j = j0 + lane;
+      const bool valid = j < ent;
+      const int ei = R == 2 ? (j >> 1) : j;
+      const bool side = R == 2 && (j & 1);
+      longlong2 a = make_longlong2(0, 0), b = make_longlong2(0, 0);  // (eid, src), (dst, t)
+      if (valid) {
+        const longlong2* e = reinterpret_cast<const longlong2*>(sev + ei);
+        a = e[0];
+        b = e[1];
+      }
+      const uint32_t node = static_cast<uint32_t>(side ? b.x : a.y);
+      const long long other = side ? a.y : b.x;
+      const uint32_t key = valid ? node : (0x80000000u | static_cast<uint32_t>(lane));
+      const uint32_t c = valid ? cursor[node] : 0u;
+      const unsigned peers = __match_any_sync(kFull, key);
+      const uint32_t rank = static_cast<uint32_t>(__popc(peers & lanemask_lt()));
+      const uint32_t pos = (c & 0x7fffffffu) + rank;
+      if (valid && lane == 31 - __clz(peers)) cursor[node] = c + static_cast<uint32_t>(__popc(peers));
+      __syncwarp();
+      if (valid) {
+        if (c >> 31) {  // cold node: full 32-byte record in dense cold-index space
+          ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
+          rec[0] = make_ulonglong2(static_cast<unsigned long long>(other),
+                                   static_cast<unsigned long long>(a.x));
+          rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y),
+                                   static_cast<unsigned long long>(node));
+        } else {
+          ts_out[pos] = __longlong_as_double(b.y);
+          if (rec_out) {
+            rec_out[pos] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
+                                      static_cast<uint32_t>(b.y),
+                                      static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
+          } else {
+            nbr_out[pos] = other;
+            eid_out[pos] = a.x;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && it + kWStages < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t b = e0 + (it + kWStages) * kWTE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kWTE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[sidx], bytes);
+      bulk_g2s(stage + sidx * kWTE, ev + b, bytes, &bars[sidx]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ general path helpers
 __device__ __forceinline__ uint64_t time_key(double t) {
   // total order of doubles consistent with operator< for non-NaN; -0.0 keyed as +0.0
@@ -1028,7 +1133,15 @@ size_t tile_smem_for(int64_t V) {
   return 0;
 }
 
+// cursors carry the cold flag in bit 31, so positions must stay below 2^31
+thread_local int64_t t_build_m = 0;
+bool use_warp_scatter(int64_t V) {
+  return scatter_variant() == 20 && V <= 65535 && t_build_m < (int64_t(1) << 31) &&
+         warp_scatter_smem(V) <= static_cast<size_t>(device_info().smem_optin);
+}
+
 bool use_tile_scatter(int64_t V) {
+  if (use_warp_scatter(V)) return false;
   const size_t sm = tile_smem_for(V);
   return sm > 0 && V <= 65535 && sm <= static_cast<size_t>(device_info().smem_optin);
 }
@@ -1078,7 +1191,18 @@ int ticket_variant() {
   return v >= 0 && v <= 5 ? v : 0;
 }
 
+template <int R>
+int warp_bps_t(int64_t V) {
+  const size_t smem = warp_scatter_smem(V);
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_warp<R>, 32, smem));
+  return std::max(bps, 1);
+}
+
 int scatter_blocks_per_sm(int R, int64_t V) {
+  if (use_warp_scatter(V)) return R == 2 ? warp_bps_t<2>(V) : warp_bps_t<1>(V);
   if (use_tile_scatter(V)) return tile_bps(R, V);
   const int v = ticket_variant();
 #define X(ID, RO, W) \
@@ -1196,7 +1320,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   after_launch("k_indptr_scan");
   if (V > 0) {
     k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr, coldbits, cdelta,
-                               use_tile_scatter(V) ? 1 : 0);
+                               (use_tile_scatter(V) || use_warp_scatter(V)) ? 1 : 0);
     after_launch("k_coloff");
   }
   int64_t ncold = 0;
@@ -1207,6 +1331,24 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   const double tf1 = trace_ms(s);
   if (g->n == 0) return;
+  if (use_warp_scatter(V)) {
+    uint4* rec = ensure_rec(g, s);
+    g->cols_valid = rec == nullptr;
+    const size_t wsm = warp_scatter_smem(V);
+    if (g->reverse)
+      k_scatter_warp<2><<<C, 32, wsm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->ts,
+                                            rec, g->nbr, g->eid);
+    else
+      k_scatter_warp<1><<<C, 32, wsm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->ts,
+                                            rec, g->nbr, g->eid);
+    after_launch("k_scatter_warp");
+    if (ncold > 0) {
+      k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
+                                                                      g->eid, g->ts, rec);
+      after_launch("k_cold_u");
+    }
+    return;
+  }
   if (use_tile_scatter(V)) {
     // with gather records the scatter writes {rec, ts} instead of {nbr, eid, ts}; the int64
     // columns are widened from the records when something asks for them (ensure_columns)
@@ -1389,6 +1531,7 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   const int64_t n = g->n, V = g->V;
   const int R = g->reverse ? 2 : 1;
   const bool fast = V <= kFastMaxNodes && g->m < (int64_t(1) << 32);
+  t_build_m = g->m;
   int C = 1;
   int64_t chunk_ev = std::max<int64_t>(n, 1);
   uint32_t* cnt = nullptr;
