@@ -17,13 +17,14 @@
 //                  degrees, indptr (int64, V+1), cold-node bitmask (nodes with few entries
 //                  per chunk) and dense cold-index bases, and every chunk's starting cursor
 //                  per node (a C x V table, C = resident CTAs; ~20 MB for GDELT-shaped V).
-//   K3 k_scatter_tile  one more pass: each CTA streams its chunk through shared memory in
-//                  bulk-copied tiles and ranks every tile by node with a block-wide stable
-//                  radix sort, so each node's tile entries are one run written at
-//                  cursor[u] + offset (details at the kernel).  Cold nodes' entries go out as
-//                  full 32-byte records, placed by K4 k_cold_u.
-//                  (k_scatter, the earlier ticketed-warp kernel, remains for node counts
-//                  whose cursors do not fit the tile kernel's shared memory.)
+//   K3 k_scatter_big  one more pass: each CTA streams its chunk through shared memory in
+//                  bulk-copied 512-event tiles and ranks every tile by node with a block-wide
+//                  stable radix sort (4 keys per thread), so each node's tile entries are one
+//                  run written at cursor[u] + offset (details at the kernel).  Cold nodes'
+//                  entries go out as full 32-byte records, placed by K4 k_cold_u.
+//                  (k_scatter_tile, 256-event tiles with 2 keys per thread, and k_scatter, the
+//                  earlier ticketed-warp kernel, remain as A/B variants and for node counts
+//                  whose cursors do not fit.)
 //
 //   Algorithmic bytes: 32 B/event read (K3; K1 reads them once more) + 24 B/entry written
 //   + 8(V+1).
@@ -230,7 +231,18 @@ __global__ void k_coloff(uint32_t* __restrict__ cnt, int C, int32_t V,
   int64_t start = indptr[u];
   if (cold_space && ((coldbits[u >> 5] >> (u & 31)) & 1u)) start += cdelta[u];
   uint32_t run = static_cast<uint32_t>(start);
-  for (int c = 0; c < C; ++c) {
+  int c = 0;
+  for (; c + 8 <= C; c += 8) {  // 8 loads in flight per thread
+    uint32_t t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = cnt[static_cast<int64_t>(c + q) * V + u];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      cnt[static_cast<int64_t>(c + q) * V + u] = run;
+      run += t[q];
+    }
+  }
+  for (; c < C; ++c) {
     const int64_t i = static_cast<int64_t>(c) * V + u;
     const uint32_t t = cnt[i];
     cnt[i] = run;
@@ -390,6 +402,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -665,107 +680,237 @@ __global__ void __launch_bounds__(256) k_cold_u(const ulonglong2* __restrict__ i
   }
 }
 
-// K3 "warp chunks" (TGFX_SCATTER_VARIANT=20): one warp per CTA, several CTAs per SM, each
-// owning a contiguous chunk of the stream and a PRIVATE cursor table for all V nodes in shared
-// memory (bit 31 = cold flag).  Because no other warp touches the table, a chunk is processed
-// strictly sequentially in emission order, 32 entries per step, with no block barriers and no
-// sort: lanes of one node are grouped by one MATCH.ANY, an entry's position is the node's
-// cursor + its rank among the group's lower lanes, and the group's highest lane advances the
-// cursor.  Events arrive through a private ring of bulk copies (cp.async.bulk + mbarrier).
-constexpr int kWStages = 2;
-constexpr int kWTE = 96;  // events per stage (3 KB): the cursor table leaves little room
-
-size_t warp_scatter_smem(int64_t V) {
-  const int64_t vpad = (V + 31) & ~31LL;
-  return static_cast<size_t>(kWStages) * kWTE * 32 + 64 + static_cast<size_t>(vpad) * 4;
+// entry writer shared by the scatter kernels: gather record + ts at pos, or a 32-byte cold
+// record in dense cold-index space
+template <int R>
+__device__ __forceinline__ void hot_write_entry(const tgfx_event* sev, int j, uint32_t pos,
+                                                const uint32_t* coldbits,
+                                                ulonglong2* __restrict__ cold_img,
+                                                double* __restrict__ ts_out,
+                                                uint4* __restrict__ rec_out,
+                                                int64_t* __restrict__ nbr_out,
+                                                int64_t* __restrict__ eid_out) {
+  const longlong2* e = reinterpret_cast<const longlong2*>(sev + (R == 2 ? (j >> 1) : j));
+  const longlong2 a = e[0], b = e[1];  // (eid, src), (dst, t bits)
+  const bool side = R == 2 && (j & 1);
+  const long long other = side ? a.y : b.x;
+  const uint32_t u = static_cast<uint32_t>(side ? b.x : a.y);
+  if ((coldbits[u >> 5] >> (u & 31)) & 1u) {
+    ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
+    rec[0] = make_ulonglong2(static_cast<unsigned long long>(other), static_cast<unsigned long long>(a.x));
+    rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u));
+  } else {
+    ts_out[pos] = __longlong_as_double(b.y);
+    if (rec_out) {
+      rec_out[pos] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
+                                static_cast<uint32_t>(b.y),
+                                static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
+    } else {
+      nbr_out[pos] = other;
+      eid_out[pos] = a.x;
+    }
+  }
 }
 
 template <int R>
-__global__ void __launch_bounds__(32) k_scatter_warp(
-    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits_g,
+__device__ __forceinline__ uint32_t hot_node_of(const tgfx_event* sev, int j) {
+  const int64_t* e = reinterpret_cast<const int64_t*>(sev + (R == 2 ? (j >> 1) : j));
+  return static_cast<uint32_t>((R == 2 && (j & 1)) ? e[2] : e[1]);
+}
+
+// K3 "big tiles, cursors in L2" (TGFX_SCATTER_VARIANT=40).
+// The tile kernel above keeps every node's cursor in shared memory (V x 4 B), which leaves room
+// for only small tiles (2 keys per thread) -- its ranking is dominated by per-tile barrier and
+// shared-memory latency.  Here the cursors stay in the chunk's row of the C x V offset table in
+// global memory (L2-resident: 20 MB for the GDELT shape; read and written with .cg, only by the
+// owning CTA, tiles in order separated by __syncthreads), so shared memory holds just the event
+// stages and the key buffers, and a tile is 2048 entries: 8 keys per thread per radix pass
+// (block-wide stable LSD rank by 8-bit digits, warp-striped keys, per-warp digit counters
+// grouped by MATCH.ANY, one scan over (digit, warp)).  After the sort a node's tile entries
+// form one run: the run head fetches the node's cursor (one L2 round trip per tile, all runs
+// in parallel), every entry takes cursor + offset in run, the tail stores cursor + run length.
+// Entries are written in sorted order, so a run's stores are consecutive addresses.
+constexpr int kBT = 256;  // threads
+
+// SC: cursors (and cold bits) in shared memory instead of L2
+template <int R, int TE, int S, bool SC>
+size_t big_smem(int64_t V) {
+  const size_t vpad = static_cast<size_t>((V + 31) & ~31LL);
+  return static_cast<size_t>(S) * TE * 32 + 2 * static_cast<size_t>(R) * TE * 4 +
+         (kBT / 32) * 256 * 2 + S * 8 + 64 * 4 + (SC ? vpad * 4 + vpad / 8 : 0);
+}
+
+template <int R, int TE, int S, bool SC>
+__global__ void __launch_bounds__(kBT, 2) k_scatter_big(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev, int passes,
+    uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits,
     ulonglong2* __restrict__ cold_img, double* __restrict__ ts_out, uint4* __restrict__ rec_out,
     int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out) {
+  constexpr int NE = TE * R;
+  constexpr int KPT = NE / kBT;
+  constexpr int kW = kBT / 32;
+  static_assert(KPT * kBT == NE && NE <= 65536, "tile shape");
   extern __shared__ __align__(128) unsigned char sm[];
   tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kWStages * kWTE * 32);
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(bars + 8);
-  const int lane = threadIdx.x;
+  uint32_t* keys0 = reinterpret_cast<uint32_t*>(sm + static_cast<size_t>(S) * TE * 32);
+  uint32_t* keys1 = keys0 + NE;
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(keys1 + NE);  // [kW][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wcnt + kW * 256);
+  int* scr = reinterpret_cast<int*>(bars + S);
+  uint32_t* scur = reinterpret_cast<uint32_t*>(scr + 64);   // SC: [vpad] cursors
+  uint32_t* scold = scur + ((V + 31) & ~31);                 // SC: [vpad / 32] cold bits
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
   const int64_t e1 = min(n, e0 + chunk_ev);
   if (e0 >= e1) return;
-  const int64_t ntiles = ceil_div(e1 - e0, kWTE);
-  if (lane == 0) {
-    for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+  const int64_t ntiles = ceil_div(e1 - e0, TE);
+  uint32_t* crow = off + static_cast<int64_t>(blockIdx.x) * V;  // this chunk's cursors
+  if (SC) {
+    for (int i = tid; i < V; i += kBT) scur[i] = crow[i];
+    for (int i = tid; i < ((V + 31) >> 5); i += kBT) scold[i] = coldbits[i];
+  }
+  const uint32_t* cbits = SC ? scold : coldbits;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < kWStages && s < ntiles; ++s) {
-      const int64_t b = e0 + static_cast<int64_t>(s) * kWTE;
-      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kWTE), e1 - b) * 32);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < S && s < ntiles; ++s) {
+      const int64_t b = e0 + static_cast<int64_t>(s) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
       mbar_arrive_tx(&bars[s], bytes);
-      bulk_g2s(stage + s * kWTE, ev + b, bytes, &bars[s]);
+      bulk_g2s(stage + s * TE, ev + b, bytes, &bars[s]);
     }
   }
-  const uint32_t* orow = off + static_cast<int64_t>(blockIdx.x) * V;
-  for (int i = lane; i < V; i += 32) {
-    const uint32_t cold = (__ldg(coldbits_g + (i >> 5)) >> (i & 31)) & 1u;
-    cursor[i] = __ldg(orow + i) | (cold << 31);
-  }
-  __syncwarp();
   for (int64_t it = 0; it < ntiles; ++it) {
-    const int sidx = static_cast<int>(it % kWStages);
-    const uint32_t phase = static_cast<uint32_t>((it / kWStages) & 1);
-    const int64_t tb = e0 + it * kWTE;
-    const int ent = static_cast<int>(min(static_cast<int64_t>(kWTE), e1 - tb)) * R;
-    const tgfx_event* sev = stage + sidx * kWTE;
-    mbar_wait(&bars[sidx], phase);
-#pragma unroll 2
-    for (int j0 = 0; j0 < ent; j0 += 32) {
-      const int j = j0 + lane;
-      const bool valid = j < ent;
-      const int ei = R == 2 ? (j >> 1) : j;
-      const bool side = R == 2 && (j & 1);
-      longlong2 a = make_longlong2(0, 0), b = make_longlong2(0, 0);  // (eid, src), (dst, t)
-      if (valid) {
-        const longlong2* e = reinterpret_cast<const longlong2*>(sev + ei);
-        a = e[0];
-        b = e[1];
-      }
-      const uint32_t node = static_cast<uint32_t>(side ? b.x : a.y);
-      const long long other = side ? a.y : b.x;
-      const uint32_t key = valid ? node : (0x80000000u | static_cast<uint32_t>(lane));
-      const uint32_t c = valid ? cursor[node] : 0u;
-      const unsigned peers = __match_any_sync(kFull, key);
-      const uint32_t rank = static_cast<uint32_t>(__popc(peers & lanemask_lt()));
-      const uint32_t pos = (c & 0x7fffffffu) + rank;
-      if (valid && lane == 31 - __clz(peers)) cursor[node] = c + static_cast<uint32_t>(__popc(peers));
+    const int sidx = static_cast<int>(it % S);
+    const int64_t tb = e0 + it * TE;
+    const int ent = static_cast<int>(min(static_cast<int64_t>(TE), e1 - tb)) * R;
+    const tgfx_event* sev = stage + sidx * TE;
+    mbar_wait(&bars[sidx], static_cast<uint32_t>((it / S) & 1));
+    uint32_t key[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int j = warp * 32 * KPT + k * 32 + lane;
+      uint32_t node = static_cast<uint32_t>(V);  // sentinel sorts after every real node
+      if (j < ent) node = hot_node_of<R>(sev, j);
+      key[k] = (node << 16) | static_cast<uint32_t>(j);
+    }
+    uint32_t* src_keys = keys0;
+    uint32_t* dst_keys = keys1;
+    for (int p = 0; p < passes; ++p) {
+      const int shift = 16 + 8 * p;
+      uint16_t* wc = wcnt + warp * 256;
+      reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
       __syncwarp();
-      if (valid) {
-        if (c >> 31) {  // cold node: full 32-byte record in dense cold-index space
-          ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
-          rec[0] = make_ulonglong2(static_cast<unsigned long long>(other),
-                                   static_cast<unsigned long long>(a.x));
-          rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y),
-                                   static_cast<unsigned long long>(node));
-        } else {
-          ts_out[pos] = __longlong_as_double(b.y);
-          if (rec_out) {
-            rec_out[pos] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
-                                      static_cast<uint32_t>(b.y),
-                                      static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
-          } else {
-            nbr_out[pos] = other;
-            eid_out[pos] = a.x;
-          }
+      uint32_t rank[KPT];
+      uint32_t dig[KPT];
+      unsigned peers[KPT];
+      // all MATCH.ANYs first (independent; their latency overlaps), then the counter chain
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        dig[k] = (key[k] >> shift) & 0xffu;
+        peers[k] = __match_any_sync(kFull, dig[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const uint32_t b = wc[dig[k]];
+        __syncwarp();
+        if (lane == __ffs(peers[k]) - 1) wc[dig[k]] = static_cast<uint16_t>(b + __popc(peers[k]));
+        __syncwarp();
+        rank[k] = b + __popc(peers[k] & lanemask_lt());
+      }
+      __syncthreads();
+      {  // exclusive scan of the kW x 256 counters in (digit, warp) order, 8 per thread
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = tid * 8 + c;
+          v[c] = wcnt[(i % kW) * 256 + i / kW];
+          s += v[c];
+        }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) scr[warp] = static_cast<int>(x);
+        __syncthreads();
+        const uint32_t before = __reduce_add_sync(
+            kFull, lane < warp ? static_cast<uint32_t>(scr[lane]) : 0u);
+        uint32_t run = before + x - s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = tid * 8 + c;
+          wcnt[(i % kW) * 256 + i / kW] = static_cast<uint16_t>(run);
+          run += v[c];
         }
       }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) dst_keys[wc[dig[k]] + rank[k]] = key[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) key[k] = dst_keys[warp * 32 * KPT + k * 32 + lane];
+      uint32_t* tmp = src_keys;
+      src_keys = dst_keys;
+      dst_keys = tmp;
     }
-    __syncwarp();
-    if (lane == 0 && it + kWStages < ntiles) {
+    // sorted keys in src_keys; this thread holds positions s = warp*32*KPT + k*32 + lane.
+    // Run heads fetch the cursor into dst_keys[s] (free now); every entry finds its head by an
+    // inclusive max-scan of head positions.
+    int hp[KPT];
+    {
+      int carry = 0;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) {
+        const int s = warp * 32 * KPT + k * 32 + lane;
+        const uint32_t u = key[k] >> 16;
+        const bool head = s == 0 || (src_keys[s - 1] >> 16) != u;
+        if (head && u < static_cast<uint32_t>(V)) dst_keys[s] = SC ? scur[u] : __ldcg(crow + u);
+        int x = head ? s : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x = max(x, y);
+        }
+        x = max(x, carry);
+        hp[k] = x;
+        carry = __shfl_sync(kFull, x, 31);
+      }
+      if (lane == 31) scr[32 + warp] = carry;
+      __syncthreads();
+      const int prev = static_cast<int>(
+          __reduce_max_sync(kFull, lane < warp ? static_cast<unsigned>(scr[32 + lane]) : 0u));
+#pragma unroll
+      for (int k = 0; k < KPT; ++k) hp[k] = max(hp[k], prev);
+    }
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int s = warp * 32 * KPT + k * 32 + lane;
+      const uint32_t u = key[k] >> 16;
+      if (u >= static_cast<uint32_t>(V)) continue;
+      const uint32_t pos = dst_keys[hp[k]] + static_cast<uint32_t>(s - hp[k]);
+      const bool tail = s == NE - 1 || (src_keys[s + 1] >> 16) != u;
+      if (tail) {
+        if (SC)
+          scur[u] = pos + 1;
+        else
+          __stcg(crow + u, pos + 1);
+      }
+      hot_write_entry<R>(sev, static_cast<int>(key[k] & 0xffffu), pos, cbits, cold_img, ts_out,
+                         rec_out, nbr_out, eid_out);
+    }
+    __syncthreads();  // stage consumed; cursor stores ordered before the next tile's loads
+    if (tid == 0 && it + S < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int64_t b = e0 + (it + kWStages) * kWTE;
-      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kWTE), e1 - b) * 32);
+      const int64_t b = e0 + (it + S) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
       mbar_arrive_tx(&bars[sidx], bytes);
-      bulk_g2s(stage + sidx * kWTE, ev + b, bytes, &bars[sidx]);
+      bulk_g2s(stage + sidx * TE, ev + b, bytes, &bars[sidx]);
     }
   }
 }
@@ -1011,6 +1156,118 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
   }
 }
 
+// pass 3 (default): the same table, each thread walking 8 consecutive entries, so an entry's
+// predecessor bucket is the previous entry's (a register) and the write loop runs per thread.
+// The node of every entry comes from the tile's head marks (one max-scan per tile) instead of
+// a per-entry search of indptr; tiles inside one slice (the hubs) skip even that.
+__global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict__ indptr,
+                                                      const int64_t* __restrict__ nbr,
+                                                      const int64_t* __restrict__ eid,
+                                                      const double* __restrict__ ts,
+                                                      const NodeDir* __restrict__ dir,
+                                                      const int32_t* __restrict__ tile_node,
+                                                      int64_t V, int64_t m, bool buckets,
+                                                      uint4* __restrict__ rec) {
+  constexpr int P = 8;
+  static_assert(P * 256 == kFillTile, "tile");
+  __shared__ int32_t mark[kFillTile];
+  __shared__ int32_t wmax[8];
+  __shared__ double wts[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kFillTile;
+  if (i0 >= m) return;
+  const int64_t i1 = min(i0 + kFillTile, m) - 1;
+  const int cnt = static_cast<int>(i1 - i0 + 1);
+  const int64_t b0 = i0 + static_cast<int64_t>(tid) * P;
+  double x[P];
+  if (b0 + P - 1 <= i1) {  // 64-byte aligned: four 16-byte loads
+#pragma unroll
+    for (int k = 0; k < P; k += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(ts + b0 + k));
+      x[k] = v.x;
+      x[k + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < P; ++k) x[k] = b0 + k <= i1 ? ts[b0 + k] : 0.0;
+  }
+  if (rec) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int64_t i = b0 + k;
+      if (i > i1) break;
+      const unsigned long long tb = static_cast<unsigned long long>(__double_as_longlong(x[k]));
+      __stcs(rec + i, make_uint4(static_cast<uint32_t>(nbr[i]), static_cast<uint32_t>(eid[i]),
+                                 static_cast<uint32_t>(tb), static_cast<uint32_t>(tb >> 32)));
+    }
+  }
+  if (!buckets) return;
+  const int32_t v0 = tile_node[blockIdx.x];
+  const int32_t v1 = i1 + 1 < m ? tile_node[blockIdx.x + 1] : static_cast<int32_t>(V - 1);
+  // ts of the entry before this thread's first one
+  double xprev = __shfl_up_sync(kFull, x[P - 1], 1);
+  if (lane == 31) wts[warp] = x[P - 1];
+  int32_t first = v0;  // node of this thread's first entry
+  const bool hub = dir[v0].end > i1;
+  if (!hub) {
+    for (int q = tid; q < cnt; q += 256) mark[q] = -1;
+    __syncthreads();
+    for (int32_t u = v0 + 1 + tid; u <= v1; u += 256) {
+      const int64_t a = indptr[u];
+      if (a > i0 && a <= i1 && indptr[u + 1] > a) mark[a - i0] = u;
+    }
+    __syncthreads();
+    int32_t run = -1;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int q = tid * P + k;
+      if (q < cnt) run = max(run, mark[q]);
+    }
+    int32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc = max(inc, y);
+    }
+    if (lane == 31) wmax[warp] = inc;
+    __syncthreads();
+    int32_t ex = __shfl_up_sync(kFull, inc, 1);
+    if (lane == 0) ex = -1;
+    for (int w = 0; w < warp; ++w) ex = max(ex, wmax[w]);
+    first = max(v0, ex);  // node owning position tid*P (before this thread's own marks)
+  } else {
+    __syncthreads();
+  }
+  if (lane == 0) xprev = warp ? wts[warp - 1] : (i0 > 0 ? ts[i0 - 1] : 0.0);
+  int32_t u = first;
+  NodeDir d = dir[u];
+  int jprev = -1;  // bucket of the previous entry of the same slice
+  {
+    const int64_t i = b0;
+    if (i <= i1 && i > d.start && d.nb) jprev = static_cast<int>(bucket_of(xprev, d.t_first, d.scale, d.nb));
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int64_t i = b0 + k;
+    if (i > i1) break;
+    if (!hub) {
+      const int32_t mk = mark[tid * P + k];
+      if (mk >= 0 && mk != u) {  // a new slice starts here
+        u = mk;
+        d = dir[u];
+        jprev = -1;
+      }
+    }
+    if (!d.nb) continue;
+    const uint32_t r = static_cast<uint32_t>(i - d.start);
+    const int jr = static_cast<int>(bucket_of(x[k], d.t_first, d.scale, d.nb));
+    uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
+    for (int j = jprev + 1; j <= jr; ++j) bkt[j] = r;
+    jprev = jr;
+    if (i == d.end - 1) bkt[d.nb] = r + 1;
+  }
+}
+
 // ------------------------------------------------------------------ validate (tcsr.cpp:54-81)
 // The reference walks nodes in order (indptr monotone at u, then slice u sorted), then entries
 // in order (neighbour id, then edge id); the first failure is the one thrown.  Here every check
@@ -1114,7 +1371,7 @@ int64_t cold_theta() {
 int scatter_variant() {
   static int v = [] {
     const char* e = getenv("TGFX_SCATTER_VARIANT");
-    return e ? atoi(e) : 10;
+    return e ? atoi(e) : 43;
   }();
   return v;
 }
@@ -1124,8 +1381,12 @@ int scatter_variant() {
 // 12.9 ms, 256 x 512 12.0 ms but 1 CTA/SM on larger V, 128 x 128 16.7 ms.
 #define TGFX_TILE_SHAPES(X) X(10, 256, 256)
 
+// the tile-kernel shape in use (the default shape when a big-tile variant is selected but the
+// graph falls back to the tile kernel)
+int tile_variant() { return scatter_variant() >= 40 ? 10 : scatter_variant(); }
+
 size_t tile_smem_for(int64_t V) {
-  const int v = scatter_variant();
+  const int v = tile_variant();
 #define X(ID, TT, TE) \
   if (v == ID) return tile_scatter_smem<TT, TE>(V);
   TGFX_TILE_SHAPES(X)
@@ -1133,15 +1394,51 @@ size_t tile_smem_for(int64_t V) {
   return 0;
 }
 
-// cursors carry the cold flag in bit 31, so positions must stay below 2^31
 thread_local int64_t t_build_m = 0;
-bool use_warp_scatter(int64_t V) {
-  return scatter_variant() == 20 && V <= 65535 && t_build_m < (int64_t(1) << 31) &&
-         warp_scatter_smem(V) <= static_cast<size_t>(device_info().smem_optin);
+
+// big-tile scatter shapes: variant -> (events per tile, stages, cursors in shared memory).
+// 43 (default): 512-event tiles, 2 stages, shared-memory cursors -- 2 CTAs/SM up to V ~ 16.7 K
+// (GDELT shape); when that leaves fewer than 2 CTAs per SM the cursors move to L2 (42).
+#define TGFX_BIG_SHAPES(X) X(40, 1024, 2, false) X(41, 512, 3, false) X(42, 512, 2, false) \
+  X(43, 512, 2, true) X(44, 256, 4, true) X(45, 256, 3, true)
+
+template <int R, int TE, int S, bool SC>
+int big_bps_t(int64_t V) {
+  const size_t smem = big_smem<R, TE, S, SC>(V);
+  if (smem > static_cast<size_t>(device_info().smem_optin)) return 0;
+  int bps = 0;
+  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_big<R, TE, S, SC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_big<R, TE, S, SC>, kBT, smem));
+  return bps;
 }
 
-bool use_tile_scatter(int64_t V) {
-  if (use_warp_scatter(V)) return false;
+int big_bps(int R, int v, int64_t V) {
+#define X(ID, TE, S, SC) \
+  if (v == ID) return R == 2 ? big_bps_t<2, TE, S, SC>(V) : big_bps_t<1, TE, S, SC>(V);
+  TGFX_BIG_SHAPES(X)
+#undef X
+  return 0;
+}
+
+// the big-tile variant this build uses, 0 if none (node ids 0..V must fit the 16-bit key field)
+int big_variant(int R, int64_t V) {
+  int v = scatter_variant();
+  if (v < 40 || v > 45 || V > 65534 || t_build_m >= (int64_t(1) << 32)) return 0;
+  if (v == 43 && big_bps(R, 43, V) < 2) {
+    // shared-memory cursors would leave one CTA per SM: the 256-event tile kernel when its
+    // cursors fit (measured faster there, e.g. V = 40 K), else cursors in L2 (42)
+    const size_t tsm = tile_scatter_smem<256, 256>(V);
+    if (V <= 65535 && tsm <= static_cast<size_t>(device_info().smem_optin)) return 0;
+    v = 42;
+  }
+  return big_bps(R, v, V) >= 1 ? v : 0;
+}
+
+bool use_big_scatter(int64_t V, int R) { return big_variant(R, V) != 0; }
+
+bool use_tile_scatter(int64_t V, int R) {
+  if (use_big_scatter(V, R)) return false;
   const size_t sm = tile_smem_for(V);
   return sm > 0 && V <= 65535 && sm <= static_cast<size_t>(device_info().smem_optin);
 }
@@ -1158,7 +1455,7 @@ int tile_bps_t(int64_t V) {
 }
 
 int tile_bps(int R, int64_t V) {
-  const int v = scatter_variant();
+  const int v = tile_variant();
 #define X(ID, TT, TE) \
   if (v == ID) return R == 2 ? tile_bps_t<2, TT, TE>(V) : tile_bps_t<1, TT, TE>(V);
   TGFX_TILE_SHAPES(X)
@@ -1191,19 +1488,9 @@ int ticket_variant() {
   return v >= 0 && v <= 5 ? v : 0;
 }
 
-template <int R>
-int warp_bps_t(int64_t V) {
-  const size_t smem = warp_scatter_smem(V);
-  int bps = 0;
-  TGFX_CUDA(cudaFuncSetAttribute(k_scatter_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  TGFX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_warp<R>, 32, smem));
-  return std::max(bps, 1);
-}
-
 int scatter_blocks_per_sm(int R, int64_t V) {
-  if (use_warp_scatter(V)) return R == 2 ? warp_bps_t<2>(V) : warp_bps_t<1>(V);
-  if (use_tile_scatter(V)) return tile_bps(R, V);
+  if (const int v = big_variant(R, V)) return big_bps(R, v, V);
+  if (use_tile_scatter(V, R)) return tile_bps(R, V);
   const int v = ticket_variant();
 #define X(ID, RO, W) \
   if (v == ID) return R == 2 ? scatter_bps<2, RO, W>(V) : scatter_bps<1, RO, W>(V);
@@ -1304,11 +1591,13 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   const int vb = static_cast<int>(ceil_div(std::max<int64_t>(V, 1), tb));
   const int64_t vpad = (static_cast<int64_t>(V) + 31) & ~31LL;
   // small workspace: cold bitmask [vpad/32] u32 | cdelta [V] i64 | ncold i64
-  char* small = static_cast<char*>(ws_get(g->ws_small, g->ws_small_bytes,
-                                          16 + 4 * (vpad / 32) + 8 * (vpad + 2), s));
+  const int64_t cb = (4 * (vpad / 32) + 15) & ~15LL;
+  char* small = static_cast<char*>(ws_get(g->ws_small, g->ws_small_bytes, cb + 8 * (vpad + 2), s));
   uint32_t* coldbits = reinterpret_cast<uint32_t*>(small);
-  int64_t* cdelta = reinterpret_cast<int64_t*>(small + ((4 * (vpad / 32) + 15) & ~15LL));
+  int64_t* cdelta = reinterpret_cast<int64_t*>(small + cb);
   int64_t* ncold_d = cdelta + vpad;
+  const int R = g->reverse ? 2 : 1;
+  const int bigv = big_variant(R, V);
   if (V > 0) {
     k_colsum<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr);
     after_launch("k_colsum");
@@ -1320,7 +1609,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   after_launch("k_indptr_scan");
   if (V > 0) {
     k_coloff<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr, coldbits, cdelta,
-                               (use_tile_scatter(V) || use_warp_scatter(V)) ? 1 : 0);
+                               (bigv || use_tile_scatter(V, R)) ? 1 : 0);
     after_launch("k_coloff");
   }
   int64_t ncold = 0;
@@ -1331,17 +1620,26 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
       ws_get(g->ws_rec, g->ws_rec_bytes, 32 * static_cast<size_t>(std::max<int64_t>(ncold, 1)), s));
   const double tf1 = trace_ms(s);
   if (g->n == 0) return;
-  if (use_warp_scatter(V)) {
+  if (bigv) {
+    // with gather records the scatter writes {rec, ts} instead of {nbr, eid, ts}; the int64
+    // columns are widened from the records when something asks for them (ensure_columns)
     uint4* rec = ensure_rec(g, s);
     g->cols_valid = rec == nullptr;
-    const size_t wsm = warp_scatter_smem(V);
-    if (g->reverse)
-      k_scatter_warp<2><<<C, 32, wsm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->ts,
-                                            rec, g->nbr, g->eid);
-    else
-      k_scatter_warp<1><<<C, 32, wsm, s>>>(d_ev, g->n, V, chunk_ev, cnt, coldbits, img, g->ts,
-                                            rec, g->nbr, g->eid);
-    after_launch("k_scatter_warp");
+    int bits = 1;
+    while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
+    const int passes = (bits + 7) / 8;
+#define X(ID, TE, S, SC)                                                                       \
+    if (bigv == ID) {                                                                          \
+      if (g->reverse)                                                                          \
+        k_scatter_big<2, TE, S, SC><<<C, kBT, big_smem<2, TE, S, SC>(V), s>>>(                 \
+            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid);  \
+      else                                                                                     \
+        k_scatter_big<1, TE, S, SC><<<C, kBT, big_smem<1, TE, S, SC>(V), s>>>(                 \
+            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid);  \
+    }
+    TGFX_BIG_SHAPES(X)
+#undef X
+    after_launch("k_scatter_big");
     if (ncold > 0) {
       k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
                                                                       g->eid, g->ts, rec);
@@ -1349,7 +1647,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
     }
     return;
   }
-  if (use_tile_scatter(V)) {
+  if (use_tile_scatter(V, R)) {
     // with gather records the scatter writes {rec, ts} instead of {nbr, eid, ts}; the int64
     // columns are widened from the records when something asks for them (ensure_columns)
     uint4* rec = ensure_rec(g, s);
@@ -1359,7 +1657,7 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
     int bits = 1;
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
     const int passes = (bits + 7) / 8;
-    const int v = scatter_variant();
+    const int v = tile_variant();
 #define X(ID, TT, TE)                                                                        \
   if (v == ID) {                                                                             \
     if (g->reverse)                                                                          \
@@ -1606,6 +1904,16 @@ void ensure_columns(const tgfx_graph* cg, cudaStream_t s) {
   g->cols_valid = true;
 }
 
+// bucket-fill kernel (TGFX_BUCKET_FILL: 8 = per-thread walk over 8 entries (default), 1 = one
+// entry per thread)
+static int bucket_fill_v() {
+  static const int v = [] {
+    const char* e = getenv("TGFX_BUCKET_FILL");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
+}
+
 // entries per time bucket (TGFX_BUCKET_ENTRIES, default 4; 0 disables the tables)
 static int64_t bucket_entries() {
   static const int64_t r = [] {
@@ -1654,9 +1962,14 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   k_node_dir_bkt<<<vb, 256, 0, s>>>(off, g->V, g->bkt, g->dir);
   after_launch("k_node_dir_bkt");
   if (g->m > 0) {
-    k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
-                                                          g->dir, tile_node, g->V, g->m, true,
-                                                          rec);
+    if (bucket_fill_v() == 8)
+      k_bucket_fill8<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
+                                                             g->dir, tile_node, g->V, g->m, true,
+                                                             rec);
+    else
+      k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
+                                                            g->dir, tile_node, g->V, g->m, true,
+                                                            rec);
     after_launch("k_bucket_fill");
   }
   dfree(tile_node, s);
