@@ -44,6 +44,15 @@ CONFIGS = {
               name="Wikipedia-shaped synthetic (V=9,227, E=157,474)"),
     "L": dict(E=1_293_103, V=1980, strategy="random", k=20, l=21, B=4000,
               name="LastFM-shaped synthetic (V=1,980, E=1,293,103)"),
+    # MAG-shaped (BASELINE configs[4]): at N > 1 the T-CSR comes from the node-range-partitioned
+    # build (one NCCL all-to-all) + all-gather replication, then query-sharded sampling.  The
+    # full shape needs N >= 4 (41.6 GB stream + 63 GB T-CSR + records per replica); M16 is the
+    # 1/16 scale the parity tests use (fits one GPU).
+    "M": dict(E=1_300_000_000, V=121_000_000, strategy="recent", k=10, l=11, B=600,
+              partitioned=True, name="MAG-shaped synthetic (V=121,000,000, E=1,300,000,000, Zipf 1.2)"),
+    "M16": dict(E=81_250_000, V=7_562_500, strategy="recent", k=10, l=11, B=600,
+                partitioned=True,
+                name="1/16-scale MAG-shaped synthetic (V=7,562,500, E=81,250,000, Zipf 1.2)"),
 }
 SEED, NEG_SEED, ZIPF = 42, 7, 1.2
 
@@ -227,19 +236,25 @@ def metric_name(cfg):
 
 
 def config_obj(cfg, ws, weak=True):
+    E, V = cfg["E"], cfg["V"]
     if ws == 1:
         par = "1 GPU"
     elif weak:
         par = (f"dp{ws}: {ws} data-parallel workers, each a full pass (own T-CSR replica, "
                f"own negatives neg_seed+rank); no collective in the step")
+    elif cfg.get("partitioned"):
+        par = (f"node-range-partitioned build x{ws} (one all-to-all) + replication, then "
+               f"query-sharded sampling x{ws} (whole batches, stream_base)")
     else:
-        par = f"query-sharded x{ws} (whole batches, stream_base), T-CSR replicated"
+        par = (f"query-sharded x{ws} (whole batches, stream_base), T-CSR replicated (each rank "
+               f"builds it from the stream)")
     return {"workload": cfg["name"] + f"; reverse=1 T-CSR build + {cfg['strategy']}-{cfg['k']} "
                                       f"sampling, l={cfg['l']}, all 3E queries, batch {cfg['B']}",
-            "events": cfg["E"], "num_nodes": cfg["V"], "queries": 3 * cfg["E"], "k": cfg["k"],
+            "events": E, "num_nodes": V, "queries": 3 * E, "k": cfg["k"],
             "seq_len": cfg["l"], "batch": cfg["B"], "reverse": 1,
             "parallelism": par,
-            "l2_flush": "inputs larger than L2 (6.1 GB events, 9.2 GB queries vs 126 MB L2)"}
+            "l2_flush": (f"inputs larger than L2 ({32 * E / 1e9:.1f} GB events, "
+                         f"{48 * E / 1e9:.1f} GB queries vs 126 MB L2)")}
 
 
 # ------------------------------------------------------------------------------ our path
@@ -269,21 +284,35 @@ def run_ours(args, cfg):
     # strong: one pass, whole-batch query shards across ranks (shard.py)
     neg_seed = S.weak_neg_seed(NEG_SEED, rank) if weak else NEG_SEED
 
-    # resident inputs: event stream (generated on device) and all queries
+    # resident inputs: event stream (generated on device) and this rank's queries
     ev = D.random_stream(E, V, SEED)
-    nodes = torch.empty(Q, dtype=torch.int64, device="cuda")
-    times = torch.empty(Q, dtype=torch.float64, device="cuda")
-    # whole batches per generation call keep the [src|dst|neg] batch layout
-    step_ev = (8_000_000 // B) * B
-    for e0 in range(0, E, step_ev):
-        e1 = min(E, e0 + step_ev)
-        D.make_queries(ev, e0, e1, B, V, neg_seed, nodes=nodes[3 * e0:3 * e1],
-                       times=times[3 * e0:3 * e1])
     q_lo, q_hi = (0, Q) if weak else S.shard_range(Q, 3 * B, ws, rank)
+    nodes = torch.empty(max(q_hi - q_lo, 1), dtype=torch.int64, device="cuda")
+    times = torch.empty(max(q_hi - q_lo, 1), dtype=torch.float64, device="cuda")
+    # whole batches per generation call keep the [src|dst|neg] batch layout (shards are whole
+    # batches, so query q of the shard belongs to event (q_lo + q) // 3's batch)
+    step_ev = (8_000_000 // B) * B
+    for e0 in range(q_lo // 3, q_hi // 3, step_ev):
+        e1 = min(q_hi // 3, e0 + step_ev)
+        D.make_queries(ev, e0, e1, B, V, neg_seed, nodes=nodes[3 * e0 - q_lo:3 * e1 - q_lo],
+                       times=times[3 * e0 - q_lo:3 * e1 - q_lo])
     chunk = args.chunk
     chunks = S.chunks(q_lo, q_hi, chunk)
     out = D.alloc_rows(min(chunk, max(q_hi - q_lo, 1)), l)
-    g = D.build(ev, V, True)
+    # the T-CSR every rank samples: a local build of the whole stream (a replica), or for the
+    # partitioned configs at N > 1 the node-range-partitioned build + all-gather replication
+    part = bool(cfg.get("partitioned")) and ws > 1
+    ev_part = None
+    if part:
+        from paper_2409_05477_b200 import partition as PT
+        e_lo, e_hi = E * rank // ws, E * (rank + 1) // ws  # rank r holds the r-th stream chunk
+        ev_part = ev[e_lo * 32:e_hi * 32].clone()
+        del ev
+        ev = None
+        torch.cuda.empty_cache()
+        g = PT.build_partitioned(ev_part, V, True, E, replicate=True, exchange_on_host=share)["full"]
+    else:
+        g = D.build(ev, V, True)
     torch.cuda.synchronize()
 
     # stratified row sample per chunk (64 rows) whose device-path result the e2e leg's host
@@ -293,24 +322,42 @@ def run_ours(args, cfg):
              for s, e in chunks]
     expect = []
 
+    # check_query (sampler.cpp:22-27) runs inside the sampler kernel for every query (fused
+    # check): the kernels record the first failing global query index in `first_bad`, read
+    # once per step (one 8-byte copy + sync inside the timed region) and raised like the
+    # reference's ValidationError
+    first_bad = D.first_bad_word()
+
+    graph = [g]
+    del g
+
     def one_step(record=None, taken=None):
         if record:
             record["b0"].record(stream)
-        D.rebuild(g, ev, trusted=True)
+        if part:  # partitioned build + all-gather replication (collectives inside)
+            graph[0] = None
+            graph[0] = PT.build_partitioned(ev_part, V, True, E, replicate=True,
+                                            exchange_on_host=share)["full"]
+        else:
+            D.rebuild(graph[0], ev, trusted=True)
+        g = graph[0]
         if record:
             record["b1"].record(stream)
+        first_bad.fill_(-1)
         for i, (s, e) in enumerate(chunks):
             if record:
                 record["c"][i][0].record(stream)
             sub = {kk: vv[: e - s] for kk, vv in out.items()}
-            D.sample_assemble(g, nodes[s:e], times[s:e], k, strat, 9, l, E + 1, out=sub,
-                              stream_base=s, trusted=True)
+            D.sample_assemble(g, nodes[s - q_lo:e - q_lo], times[s - q_lo:e - q_lo], k, strat, 9,
+                              l, E + 1, out=sub,
+                              stream_base=s, first_bad=first_bad)
             if record:
                 record["c"][i][1].record(stream)
-            if taken is not None:
+            if taken is not None:  # warm-up only (the rows buffer is reused by every chunk)
                 taken.append(int(sub["valid_len"].sum().item()) - (e - s))
                 ix = torch.from_numpy(probe[i]).to(sub["valid_len"].device)
                 expect.append({kk: vv[ix].cpu().numpy() for kk, vv in sub.items()})
+        D.query_error(nodes, first_bad, stream_base=q_lo)
 
     taken = []
     for w in range(args.warmup):
@@ -338,6 +385,25 @@ def run_ours(args, cfg):
         dist.barrier()
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
+    # build + int64 columns (untimed in the step): the step's build writes the sampler's 16-byte
+    # gather records {u32 nbr, u32 eid, f64 ts} and ts; the reference's int64 neighbor_ids /
+    # edge_ids columns are widened from the records on demand (k_widen).  Timed here as
+    # rebuild + widening, the full reference-layout T-CSR.
+    w_ms = []
+    for _ in range(0 if part else 3):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        D.rebuild(graph[0], ev, trusted=True)
+        D.graph_tensors(graph[0])
+        a1.record(stream)
+        torch.cuda.synchronize()
+        w_ms.append(a0.elapsed_time(a1))
+    build_i64_ms = S.max_over_ranks([statistics.median(w_ms) if w_ms else 0.0], device=red)[0]
+    # N > 1: the node-range-partitioned build (degree all-reduce, one all-to-all
+    # of 32-byte records, local stable build of the owned range), timed on its own, and the
+    # all-gather that replicates it for query-sharded sampling
+    build_part = measure_partitioned(ev_part if part else ev, E, V, ws, rank, share, red, stream,
+                                     owned_chunk=part) if ws > 1 else None
     total_ms = start.elapsed_time(end)
     build_ms = [r["b0"].elapsed_time(r["b1"]) for r in ev_rec]
     samp_launch_ms = [a.elapsed_time(b) for r in ev_rec for (a, b) in r["c"]]
@@ -372,6 +438,11 @@ def run_ours(args, cfg):
                   "alg_bytes": build_bytes,
                   "achieved_gbs": build_bytes / (build_med * 1e-3) / 1e9,
                   "frac": build_bytes / (build_med * 1e-3) / 1e9 / peak},
+        "build_int64": None if part else {
+                        "ms": build_i64_ms, "edges_per_s": E / (build_i64_ms * 1e-3),
+                        "frac": build_bytes / (build_i64_ms * 1e-3) / 1e9 / peak,
+                        "what": "rebuild + k_widen of the int64 neighbor_ids/edge_ids columns "
+                                "(the reference TCsr layout); not part of the step"},
         "sample": {"ms": samp_med, "queries_per_s": q_all / (samp_med * 1e-3),
                    "launches_per_step": len(chunks), "mean_taken": taken_all / max(q_all, 1)},
         "roofline": {"kernel": "k_recent_line (fused recent-k line-probe sampler + sequence packing)",
@@ -387,13 +458,19 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if build_part is not None:
+        line["build_partitioned"] = build_part
+    if part:
+        line["build"]["what"] = ("partitioned build + all-gather replication per step "
+                                 "(partition.build_partitioned, NCCL)")
     ev_host = None
     if rank == 0 and not args.no_cpu:
         ev_host = ev.cpu().numpy().view(_event_dtype())  # bit-identical to the reference's
     if not args.no_e2e:
         # the device-resident run's graph, rows and inputs are not part of the e2e path: the
         # e2e step starts from the device memory a fresh host-buffer caller would have
-        del g, out
+        graph.clear()
+        del out
         dev_inputs = {"ev": ev, "nodes": nodes, "times": times}
         del ev, nodes, times
         import gc
@@ -420,6 +497,55 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def measure_partitioned(ev_any, E, V, ws, rank, share, red, stream, owned_chunk=False, reps=3):
+    """Device time (max over ranks) of partition.build_partitioned without replication, and of
+    one replication all-gather.  ev_any: the whole stream (a rank takes its chunk) or, with
+    owned_chunk, this rank's chunk already."""
+    import torch
+    import torch.distributed as dist
+    from paper_2409_05477_b200 import partition as PT, shard as S
+    if owned_chunk:
+        ev_loc = ev_any
+    else:
+        e_lo, e_hi = E * rank // ws, E * (rank + 1) // ws
+        ev_loc = ev_any[e_lo * 32:e_hi * 32]
+    ms = []
+    for i in range(reps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        r = PT.build_partitioned(ev_loc, V, True, E, replicate=False, exchange_on_host=share)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ms.append(a0.elapsed_time(a1))
+        del r
+    dist.barrier()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r = PT.build_partitioned(ev_loc, V, True, E, replicate=False, exchange_on_host=share)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0.record(stream)
+    full = PT.replicate(r, V, E, True, exchange_on_host=share)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    rep_ms = a0.elapsed_time(a1)
+    sent = int(r.get("sent_records", 0))
+    del full, r
+    med = sorted(ms)[len(ms) // 2]
+    med, rep_ms = S.max_over_ranks([med, rep_ms], device=red)
+    sent_all = int(S.sum_over_ranks([sent], device=red)[0])
+    return {"ms": med, "edges_per_s": E / (med * 1e-3), "ranks": ws,
+            "exchange_bytes": 32 * sent_all, "replicate_ms": rep_ms,
+            "what": "node-range-partitioned build: degree all-reduce, one all-to-all of 32-byte "
+                    "records, local stable build of each owned range (aggregate events/s); "
+                    "replicate_ms = the all-gather + import that gives every rank the full "
+                    "T-CSR for query-sharded sampling",
+            "collectives": "gloo, host-staged (1-GPU test mode)" if share else "NCCL"}
 
 
 def load_traffic(cfg, bytes_per_launch):
@@ -586,9 +712,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--plan", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = each rank a full data-parallel pass (default); "
-                         "strong = one pass, queries sharded across ranks")
+    ap.add_argument("--plan", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong = one pass, queries sharded across ranks (default); "
+                         "weak = each rank a full data-parallel pass with its own negatives")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: W >= 3 required by the timing rules; using 3", file=sys.stderr)

@@ -182,6 +182,26 @@ int tgfx_sample_sequence_batch(const tgfx_graph* g, const int64_t* nodes, const 
                                uint64_t stream_base, int64_t l, int64_t self_edge_index,
                                int64_t* node_index, int64_t* edge_index, double* time_delta,
                                int64_t* valid_len, int64_t* target_row);
+/* tgfx_sample_assemble_device with the query check fused into the sampler kernel
+ * (check_query, proj/src/sampler.cpp:22-27, called for every query by sample_batch :93):
+ * instead of a separate validation pass and a synchronisation, the kernel compares each
+ * query node with [0, num_nodes) as it loads it and atomically lowers *d_first_bad (a device
+ * word the caller sets to ~0 beforehand) to stream_base + the first failing query index.
+ * Asynchronous; rows of failing queries are written as absent ones (all zero, valid_len 0)
+ * and, unlike sample_batch, the other rows are written too -- the caller raises the error
+ * with tgfx_query_error before using them (any number of calls may share one word). */
+int tgfx_sample_assemble_checked_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                        const double* d_times, int64_t q, int64_t k,
+                                        int strategy, uint64_t seed, uint64_t stream_base,
+                                        int64_t l, int64_t self_edge_index, void* d_node_index,
+                                        void* d_edge_index, float* d_dt32, double* d_dt64,
+                                        void* d_valid_len, unsigned long long* d_first_bad,
+                                        void* stream, unsigned flags);
+/* Reads *d_first_bad (synchronising `stream`): TGFX_OK if no query failed, else
+ * TGFX_EVALIDATION with the reference's text "query node <u> out of range" (sampler.cpp:24),
+ * u read from d_nodes[first_bad - stream_base] (d_nodes = the failing call's query nodes). */
+int tgfx_query_error(const int64_t* d_nodes, uint64_t stream_base,
+                     const unsigned long long* d_first_bad, void* stream);
 /* device variant; with TGFX_INDEX64 the node_index / edge_index / valid_len pointers are
  * int64_t* (the reference's SequenceBatch types). */
 int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,

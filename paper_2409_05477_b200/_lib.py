@@ -94,6 +94,9 @@ SIGNATURES = {
                              _P],
     "tgfx_sample_sequence_batch": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P,
                                    _P, _P, _P],
+    "tgfx_sample_assemble_checked_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64,
+                                            _P, _P, _P, _P, _P, _P, _P, _U],
+    "tgfx_query_error": [_P, _U64, _P, _P],
     "tgfx_sample_assemble_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P,
                                     _P, _P, _P, _P, _U],
     "tgfx_sample_assemble_batched_device": [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I64, _I64,

@@ -671,6 +671,58 @@ int tgfx_sample_assemble_device(const tgfx_graph* g, const int64_t* d_nodes,
   });
 }
 
+int tgfx_sample_assemble_checked_device(const tgfx_graph* g, const int64_t* d_nodes,
+                                        const double* d_times, int64_t q, int64_t k,
+                                        int strategy, uint64_t seed, uint64_t stream_base,
+                                        int64_t l, int64_t self_edge_index, void* d_node_index,
+                                        void* d_edge_index, float* d_dt32, double* d_dt64,
+                                        void* d_valid_len, unsigned long long* d_first_bad,
+                                        void* stream, unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    if (!d_first_bad) throw Error(TGFX_EVALIDATION, "null first_bad word");
+    if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
+    check_k(k);
+    check_l(l);
+    const bool i64 = (flags & TGFX_INDEX64) != 0;
+    if (!i64) check_int32_outputs(g, self_edge_index);
+    SampleArgs a{};
+    a.g = g;
+    a.nodes = d_nodes;
+    a.times = d_times;
+    a.q = q;
+    a.k = k;
+    a.strategy = strategy;
+    a.seed = seed;
+    a.stream_base = stream_base;
+    a.l = l;
+    a.self_edge_index = self_edge_index;
+    a.node_index = d_node_index;
+    a.edge_index = d_edge_index;
+    a.dt32 = d_dt32;
+    a.dt64 = d_dt64;
+    a.valid_len = d_valid_len;
+    a.index64 = i64;
+    a.first_bad = d_first_bad;
+    launch_sample(a, as_stream(stream));
+  });
+}
+
+int tgfx_query_error(const int64_t* d_nodes, uint64_t stream_base,
+                     const unsigned long long* d_first_bad, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    unsigned long long h = ~0ull;
+    TGFX_CUDA(cudaMemcpyAsync(&h, d_first_bad, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    if (h == ~0ull) return;
+    int64_t u = 0;
+    TGFX_CUDA(cudaMemcpyAsync(&u, d_nodes + (h - stream_base), sizeof(u), cudaMemcpyDeviceToHost, s));
+    TGFX_CUDA(cudaStreamSynchronize(s));
+    throw Error(TGFX_EVALIDATION, "query node " + std::to_string(u) + " out of range");
+  });
+}
+
 namespace {
 
 std::string trimmed(const std::string& x) {

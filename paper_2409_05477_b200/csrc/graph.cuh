@@ -147,6 +147,8 @@ struct SampleArgs {
   // batched uniform sampling: batch b = query / batch_q uses seeds[b] (device array)
   const uint64_t* seeds = nullptr;
   int64_t batch_q = 0;
+  // fused query check: first failing stream_base + q (atomicMin), or nullptr
+  unsigned long long* first_bad = nullptr;
 };
 
 // first invalid query index (or -1); validates node range on device (sampler.cpp:22-27)

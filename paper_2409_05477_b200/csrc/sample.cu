@@ -51,6 +51,12 @@ struct QueryIn {
   // sample_batch(seed = seeds[b]) call: RNG stream = qq - b * batch_q (sampler.cpp:100-101)
   const uint64_t* seeds = nullptr;
   int64_t batch_q = 0;
+  // query node range check fused into the sampler (check_query, sampler.cpp:22-27): a node
+  // outside [0, V) is never looked up (its row is written as an absent one); with `bad` set
+  // the smallest failing bad_base + q is recorded there for the caller to raise
+  int64_t V = 0;
+  unsigned long long* bad = nullptr;
+  uint64_t bad_base = 0;
 };
 
 // CounterRng(seed, stream) initial state of query qq (rng.hpp:23-24)
@@ -73,6 +79,10 @@ __device__ __forceinline__ bool fetch_query(const QueryIn& in, int64_t q, int64_
   }
   u = static_cast<int64_t>(__ldcs(reinterpret_cast<const long long*>(in.nodes) + q));
   t = __ldcs(in.times + q);
+  if (static_cast<uint64_t>(u) >= static_cast<uint64_t>(in.V)) {
+    if (in.bad) atomicMin(in.bad, static_cast<unsigned long long>(in.bad_base + q));
+    return false;
+  }
   return true;
 }
 
@@ -1360,7 +1370,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     throw Error(TGFX_EVALIDATION, "indptr not monotone");
   if (a.q <= 0) return;
   const tgfx_graph* g = a.g;
-  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q};
+  QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q,
+             g->V,    a.first_bad, a.stream_base};
   Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
          a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
   const int grid = grid_groups(a.q);

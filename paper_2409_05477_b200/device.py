@@ -94,13 +94,34 @@ def alloc_rows(q, l, index64=False, dt32=True, dt64=False):
     return d
 
 
+def first_bad_word():
+    """Device word for sample_assemble(first_bad=...): ~0 = no failing query yet."""
+    return torch.full((1,), -1, dtype=torch.int64, device="cuda")
+
+
+def query_error(nodes, first_bad, stream_base=0, stream=None):
+    """Raise the reference's ValidationError if a fused-check call recorded a bad query."""
+    check(lib().tgfx_query_error(_p(nodes), stream_base & (2**64 - 1), _p(first_bad),
+                                 _stream(stream)))
+
+
 def sample_assemble(g, nodes, times, k, strategy, seed, l, self_edge_index, out=None,
-                    stream_base=0, trusted=False, index64=False, dt64=False, stream=None):
-    """Fused sample_batch + build_sequence_batch into device rows [Q, l]."""
+                    stream_base=0, trusted=False, index64=False, dt64=False, stream=None,
+                    first_bad=None):
+    """Fused sample_batch + build_sequence_batch into device rows [Q, l].  first_bad: a
+    first_bad_word() tensor -> the query node check runs inside the sampler kernel (no
+    separate pass, no sync); raise with query_error() before using the rows."""
     q = nodes.numel()
     if out is None:
         out = alloc_rows(q, l, index64=index64, dt64=dt64)
     flags = (TGFX_TRUSTED if trusted else 0) | (TGFX_INDEX64 if index64 else 0)
+    if first_bad is not None:
+        check(lib().tgfx_sample_assemble_checked_device(
+            g.handle, _p(nodes), _p(times), q, k, _strategy_code(strategy), seed & (2**64 - 1),
+            stream_base & (2**64 - 1), l, self_edge_index, _p(out["node_index"]),
+            _p(out["edge_index"]), _p(out.get("time_delta")), _p(out.get("time_delta64")),
+            _p(out["valid_len"]), _p(first_bad), _stream(stream), flags))
+        return out
     check(lib().tgfx_sample_assemble_device(
         g.handle, _p(nodes), _p(times), q, k, _strategy_code(strategy), seed & (2**64 - 1),
         stream_base & (2**64 - 1), l, self_edge_index, _p(out["node_index"]),

@@ -12,9 +12,9 @@ One process per GPU.  Rank r holds the r-th contiguous chunk of the event stream
                   in global stream order
   5. local build  tgfx_build_range_device: an ordinary stable build of the owned range
                   (reverse = 0 over the records; neighbour ids stay global)
-  6. replicate    (optional) all_gather of the owned columns -> the full T-CSR on every rank
-                  (what query-sharded sampling needs); global indptr = exclusive scan of the
-                  all-reduced degrees.
+  6. replicate    (optional) every owner broadcasts its columns into their slice of the full
+                  columns on every rank (what query-sharded sampling needs); global indptr =
+                  exclusive scan of the all-reduced degrees.
 
 The owned range of rank r is bit-identical to the slices [indptr[b_r], indptr[b_{r+1}]) of the
 single-GPU build (tests/test_gpu_partition.py), because every node's entries arrive in
@@ -109,35 +109,41 @@ def build_partitioned(ev_local: torch.Tensor, num_nodes: int, reverse: bool, num
     check(L.tgfx_build_range_device(_ptr(recv), n_recv, hi - lo, num_nodes, num_edges, s, 0,
                                     C.byref(h)))
     local = TCsr(h.value)
-    out = dict(local=local, bounds=bounds, degrees=deg, range=(lo, hi))
+    out = dict(local=local, bounds=bounds, degrees=deg, range=(lo, hi), sent_records=sent)
     if replicate:
         out["full"] = _replicate(local, deg, bounds, num_nodes, num_edges, reverse,
                                  exchange_on_host)
     return out
 
 
+def replicate(part: dict, num_nodes: int, num_edges: int, reverse: bool,
+              exchange_on_host: bool = False):
+    """The full T-CSR on every rank from a build_partitioned(replicate=False) result."""
+    return _replicate(part["local"], part["degrees"], part["bounds"], num_nodes, num_edges,
+                      reverse, exchange_on_host)
+
+
 def _replicate(local, deg, bounds, num_nodes, num_edges, reverse, on_host):
-    """all_gather of every rank's owned columns -> one full device T-CSR per rank."""
+    """Every rank's owned columns broadcast straight into their slice of the full columns
+    (one broadcast per owner and column: no padding to the largest part, no concatenation
+    copy), then imported as one device T-CSR per rank (node directory, bucket tables and gather
+    records built on the device)."""
     from .device import graph_tensors
     from .tgformer import TCsr
     L = lib()
-    world = dist.get_world_size()
+    world, rank = dist.get_world_size(), dist.get_rank()
     dev = deg.device
     indptr = torch.zeros(num_nodes + 1, dtype=torch.int64, device=dev)
     torch.cumsum(deg, 0, out=indptr[1:])
     m = int(indptr[-1].item())
-    part = [int(indptr[int(bounds[d + 1])].item() - indptr[int(bounds[d])].item())
-            for d in range(world)]
-    mx = max(max(part), 1)
+    starts = indptr[bounds].tolist()  # entry offset of each owner's range, [world + 1]
     _, nb, ed, ts = graph_tensors(local)
-    cols = []
-    for col, dt in ((nb, torch.int64), (ed, torch.int64), (ts.view(torch.int64), torch.int64)):
-        pad = torch.zeros(mx, dtype=dt, device=dev)
-        pad[:col.numel()] = col
-        gathered = torch.empty(world * mx, dtype=dt, device=dev)
-        _all_gather(gathered, pad, on_host)
-        cols.append(torch.cat([gathered[d * mx:d * mx + part[d]] for d in range(world)]))
-        del gathered, pad
+    cols = [torch.empty(max(m, 1), dtype=torch.int64, device=dev) for _ in range(3)]
+    for col, mine in zip(cols, (nb, ed, ts.view(torch.int64))):
+        col[starts[rank]:starts[rank + 1]].copy_(mine)
+        for d in range(world):
+            if starts[d + 1] > starts[d]:
+                _broadcast(col[starts[d]:starts[d + 1]], d, on_host)
     h = C.c_void_p()
     check(L.tgfx_graph_from_device(num_nodes, num_edges, 1 if reverse else 0, m, _ptr(indptr),
                                    _ptr(cols[0]), _ptr(cols[1]), _ptr(cols[2]), _stream(None),
@@ -165,10 +171,10 @@ def _all_to_all(out, inp, out_splits, in_splits, on_host):
         dist.all_to_all_single(out, inp, out_splits, in_splits)
 
 
-def _all_gather(out, inp, on_host):
+def _broadcast(t, src, on_host):
     if on_host:
-        parts = [torch.empty(inp.shape, dtype=inp.dtype) for _ in range(dist.get_world_size())]
-        dist.all_gather(parts, inp.cpu())
-        out.copy_(torch.cat(parts))
+        c = t.cpu()
+        dist.broadcast(c, src)
+        t.copy_(c)
     else:
-        dist.all_gather_into_tensor(out, inp)
+        dist.broadcast(t, src)

@@ -157,3 +157,46 @@ def test_batched_uniform_tail_lanes(T, oracle_mod):
             want = oracle_mod.sample_assemble(og, hn[sl], ht[sl], k, "random", 9 + b, l, E + 1)
             got = {kk: v[sl].cpu().numpy() for kk, v in out.items()}
             check_rows(got, want, (k, l, b))
+
+
+def test_fused_query_check():
+    """check_query (sampler.cpp:22-27) fused into the sampler kernel: rows equal the
+    validating path's, the first failing query over several calls sharing one word is
+    reported with the reference's text, failing rows come out absent, and a trusted call with
+    a bad node neither faults nor writes a bogus row."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    from paper_2409_05477_b200._lib import ValidationError
+    E, V = 60_000, 500
+    ev = D.random_stream(E, V, 5)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 0, 6000, 600, V)
+    for strat, k, l in (("recent", 10, 11), ("random", 20, 21)):
+        want = D.sample_assemble(g, nodes, times, k, strat, 9, l, E + 1)
+        w = D.first_bad_word()
+        got = D.sample_assemble(g, nodes, times, k, strat, 9, l, E + 1, first_bad=w)
+        D.query_error(nodes, w)  # no failure
+        for key in want:
+            assert torch.equal(want[key], got[key]), (strat, key)
+    # two calls (stream_base 0 and 9000) sharing a word; failures at global 9000+17 and 9000+40
+    bad = nodes.clone()
+    bad[17] = V
+    bad[40] = -2
+    w = D.first_bad_word()
+    D.sample_assemble(g, nodes[:9000], times[:9000], 10, "recent", 9, 11, E + 1, first_bad=w)
+    rows = D.sample_assemble(g, bad[:9000], times[:9000], 10, "recent", 9, 11, E + 1,
+                             stream_base=9000, first_bad=w)
+    with pytest.raises(ValidationError, match=f"query node {V} out of range"):
+        D.query_error(bad[:9000], w, stream_base=9000)
+    assert int(rows["valid_len"][17]) == 0 and int(rows["valid_len"][40]) == 0
+    assert int(rows["node_index"][17].abs().sum()) == 0
+    ref = D.sample_assemble(g, nodes[:9000], times[:9000], 10, "recent", 9, 11, E + 1)
+    keep = torch.ones(9000, dtype=torch.bool, device="cuda")
+    keep[[17, 40]] = False
+    assert torch.equal(rows["node_index"][keep], ref["node_index"][keep])
+    # the validating path raises the same error, and trusted sampling of a bad node is absent
+    with pytest.raises(ValidationError, match=f"query node {V} out of range"):
+        D.sample_assemble(g, bad[:9000], times[:9000], 10, "recent", 9, 11, E + 1)
+    tr = D.sample_assemble(g, bad[:9000], times[:9000], 10, "recent", 9, 11, E + 1, trusted=True)
+    torch.cuda.synchronize()
+    assert int(tr["valid_len"][40]) == 0
