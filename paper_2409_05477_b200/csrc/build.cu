@@ -403,9 +403,6 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -948,33 +945,15 @@ __global__ void k_gather_events(const tgfx_event* __restrict__ ev,
 }
 
 // ------------------------------------------------------------------ large-V path helpers
-template <int R>
-__global__ void k_global_deg(const tgfx_event* __restrict__ ev, int64_t n, int64_t V, int64_t Vd,
-                             uint32_t* deg) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = b + threadIdx.x;
-    Ev x{0, -1, -1, 0.0};
-    if (e < n) x = load_event(ev, e);
-    const bool ok = x.src >= 0 && x.src < V && x.dst >= 0 && x.dst < Vd;
-#pragma unroll
-    for (int side = 0; side < R; ++side) {
-      const unsigned long long key = ok ? (unsigned long long)(side ? x.dst : x.src) : ~0ull;
-      const unsigned peers = __match_any_sync(kFull, key);
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&deg[key], __popc(peers));
-    }
-  }
-}
-
-template <int R>
-__global__ void k_entry_keys(const tgfx_event* __restrict__ ev, int64_t m, uint64_t* key,
+template <int R, typename K>
+__global__ void k_entry_keys(const tgfx_event* __restrict__ ev, int64_t m, K* key,
                              uint32_t* val) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = R == 2 ? (j >> 1) : j;
     const bool side = R == 2 && (j & 1);
     const int64_t* p = reinterpret_cast<const int64_t*>(ev + e);
-    key[j] = static_cast<uint64_t>(side ? p[2] : p[1]);
+    key[j] = static_cast<K>(side ? p[2] : p[1]);
     val[j] = static_cast<uint32_t>(j);
   }
 }
@@ -1549,7 +1528,7 @@ tgfx_event* sorted_copy(const tgfx_event* d_ev, int64_t n, cudaStream_t s) {
   after_launch("k_sort_keys");
   uint64_t* k = ekey;
   uint32_t* v = idx;
-  radix_sort_pairs<uint32_t>(k, v, kalt, ialt, n, 64, s);
+  radix_sort_pairs<uint64_t, uint32_t>(k, v, kalt, ialt, n, 64, s);
   // now v = permutation sorted by eid; sort by time key stably
   uint64_t* k2 = (k == ekey) ? kalt : ekey;  // free buffer for gathered time keys
   k_gather_keys<<<grid, 256, 0, s>>>(tkey, v, n, k2);
@@ -1558,7 +1537,7 @@ tgfx_event* sorted_copy(const tgfx_event* d_ev, int64_t n, cudaStream_t s) {
   uint32_t* vv = v;
   uint64_t* kalt2 = tkey;
   uint32_t* valt2 = (v == idx) ? ialt : idx;
-  radix_sort_pairs<uint32_t>(kk, vv, kalt2, valt2, n, 64, s);
+  radix_sort_pairs<uint64_t, uint32_t>(kk, vv, kalt2, valt2, n, 64, s);
   tgfx_event* out = static_cast<tgfx_event*>(dmalloc(sizeof(tgfx_event) * n, s));
   k_gather_events<<<grid, 256, 0, s>>>(d_ev, vv, n, out);
   after_launch("k_gather_events");
@@ -1702,36 +1681,48 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   }
 }
 
-void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
-  const int64_t V = g->V, n = g->n, m = g->m;
-  if (m >= (int64_t(1) << 32)) throw Error(TGFX_EUNSUPPORTED, "more than 2^32 entries");
-  uint32_t* deg = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * std::max<int64_t>(V, 1), s));
-  TGFX_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * std::max<int64_t>(V, 1), s));
-  const int grid = grid_for(std::max(n, m), 256);
-  if (n > 0) {
-    if (g->reverse)
-      k_global_deg<2><<<grid, 256, 0, s>>>(d_ev, n, V, V, deg);
-    else
-      k_global_deg<1><<<grid, 256, 0, s>>>(d_ev, n, V, g->other_limit, deg);
-    after_launch("k_global_deg");
+// indptr[u] = lower_bound(sorted node keys, u) for u = 0..V (the degrees are the run lengths
+// of the sorted keys, so no degree-counting pass with atomics is needed)
+template <typename K>
+__global__ void k_indptr_lb(const K* __restrict__ keys, int64_t m, int64_t V,
+                            int64_t* __restrict__ indptr) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u > V) return;
+  int64_t lo = 0, len = m;
+  while (len > 0) {
+    const int64_t h = len >> 1;
+    if (static_cast<int64_t>(__ldg(keys + lo + h)) < u) {
+      lo += h + 1;
+      len -= h + 1;
+    } else {
+      len = h;
+    }
   }
-  scan_u32_to_i64(deg, V, g->indptr, s);
-  dfree(deg, s);
-  if (m == 0) return;
-  uint64_t* key = static_cast<uint64_t*>(dmalloc(sizeof(uint64_t) * m, s));
-  uint64_t* kalt = static_cast<uint64_t*>(dmalloc(sizeof(uint64_t) * m, s));
+  indptr[u] = lo;
+}
+
+// large V: (node, emission index) pairs sorted by node (stable LSD, 32-bit keys while node ids
+// fit), indptr from the sorted keys, then each output position gathers its event
+template <typename K>
+void build_large_k(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
+  const int64_t V = g->V, m = g->m;
+  const int grid = grid_for(m, 256);
+  K* key = static_cast<K*>(dmalloc(sizeof(K) * m, s));
+  K* kalt = static_cast<K*>(dmalloc(sizeof(K) * m, s));
   uint32_t* val = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
   uint32_t* valt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
   if (g->reverse)
-    k_entry_keys<2><<<grid, 256, 0, s>>>(d_ev, m, key, val);
+    k_entry_keys<2, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
   else
-    k_entry_keys<1><<<grid, 256, 0, s>>>(d_ev, m, key, val);
+    k_entry_keys<1, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
   after_launch("k_entry_keys");
   int bits = 1;
   while (bits < 63 && (int64_t(1) << bits) < V) ++bits;
-  uint64_t* k = key;
+  K* k = key;
   uint32_t* v = val;
-  radix_sort_pairs<uint32_t>(k, v, kalt, valt, m, bits, s);
+  radix_sort_pairs<K, uint32_t>(k, v, kalt, valt, m, bits, s);
+  k_indptr_lb<K><<<static_cast<unsigned>(ceil_div(V + 1, 256)), 256, 0, s>>>(k, m, V, g->indptr);
+  after_launch("k_indptr_lb");
   if (g->reverse)
     k_gather_entries<2><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts);
   else
@@ -1741,6 +1732,19 @@ void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
   dfree(kalt, s);
   dfree(val, s);
   dfree(valt, s);
+}
+
+void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
+  const int64_t V = g->V, m = g->m;
+  if (m >= (int64_t(1) << 32)) throw Error(TGFX_EUNSUPPORTED, "more than 2^32 entries");
+  if (m == 0) {
+    TGFX_CUDA(cudaMemsetAsync(g->indptr, 0, sizeof(int64_t) * (V + 1), s));
+    return;
+  }
+  if (V <= 0xffffffffLL)
+    build_large_k<uint32_t>(g, d_ev, s);
+  else
+    build_large_k<uint64_t>(g, d_ev, s);
 }
 
 }  // namespace

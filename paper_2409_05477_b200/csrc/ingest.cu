@@ -470,7 +470,7 @@ uint64_t parse_csv_device(const char* d_buf, int64_t nbytes, int d_e, CsvResult*
   }
   uint64_t* kk = key;
   uint32_t* vv = val;
-  if (n > 1) radix_sort_pairs<uint32_t>(kk, vv, kalt, valt, n, 64, s);  // stable, by time
+  if (n > 1) radix_sort_pairs<uint64_t, uint32_t>(kk, vv, kalt, valt, n, 64, s);  // stable, by time
   res->n = n;
   res->events = static_cast<tgfx_event*>(dmalloc(32 * nb, s));
   res->features = d_e > 0 ? static_cast<double*>(dmalloc(8 * nb * d_e, s)) : nullptr;

@@ -1,9 +1,18 @@
 // primitives.cu -- device-wide scan and stable LSD radix sort used by the builder's
-// general (unsorted-stream) and large-V paths.  Hand-written for sm_100a: warp-aggregated
-// digit ranking with __match_any_sync, warp-private shared-memory counters (deterministic,
-// stable), one scatter pass per 8-bit digit; digits constant across all keys are skipped.
+// general (unsorted-stream) and large-V paths.  Hand-written for sm_100a:
+//   * scan: single pass with decoupled look-back (each tile publishes its aggregate, then its
+//     inclusive prefix; a tile's exclusive prefix comes from walking back over its
+//     predecessors' published words -- no separate reduce / partials kernels);
+//   * sort: "onesweep" LSD -- one histogram pass computes every digit position's global
+//     histogram up front (digits constant across all keys are skipped), then ONE kernel per
+//     8-bit digit: tiles (taken in order from an atomic counter) rank their keys by digit with
+//     __match_any_sync and warp-private shared-memory counters (stable), publish per-digit
+//     tile counts, find their per-digit global offsets by decoupled look-back, and scatter.
 #include "graph.cuh"
 #include "primitives.cuh"
+
+#include <algorithm>
+#include <vector>
 
 namespace tgfx {
 
@@ -41,61 +50,74 @@ __device__ __forceinline__ int64_t block_exclusive_scan_i64(int64_t v, int64_t* 
   return before;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
-                                                              int64_t n, int64_t* partials) {
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
-  int64_t s = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t j = base + i * kScanThreads + threadIdx.x;
-    if (j < n) s += in[j];
-  }
-  int64_t tot;
-  block_exclusive_scan_i64(s, &tot);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+constexpr unsigned long long kFlagAgg = 1ull << 62;  // tile aggregate published
+constexpr unsigned long long kFlagInc = 2ull << 62;  // inclusive prefix published
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_partials(int64_t* partials, int64_t nb) {
-  // single block: exclusive scan in place, sequential chunks of blockDim values
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
+// exclusive prefix of tile `tile` for one value: walk back over published words until an
+// inclusive prefix (spins while a predecessor has published nothing yet -- predecessors took
+// their tile ids earlier from the same counter, so they are resident and make progress)
+__device__ __forceinline__ unsigned long long lookback(const unsigned long long* status,
+                                                       int64_t tile, int64_t stride) {
+  unsigned long long excl = 0;
+  for (int64_t t = tile - 1; t >= 0;) {
+    const unsigned long long w = ld_acquire(status + t * stride);
+    const unsigned long long f = w & ~kValMask;
+    if (f == 0) continue;
+    excl += w & kValMask;
+    if (f == kFlagInc) break;
+    --t;
+  }
+  return excl;
+}
+
+// single-pass exclusive scan u32 -> i64 (out[n] = total); thread owns kScanItems consecutive
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* __restrict__ in,
+                                                                int64_t n, int64_t* out,
+                                                                unsigned long long* status,
+                                                                unsigned int* counter) {
+  __shared__ int64_t s_tile, s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    const int64_t j = base + threadIdx.x;
-    const int64_t v = j < nb ? partials[j] : 0;
-    int64_t tot;
-    const int64_t ex = block_exclusive_scan_i64(v, &tot);
-    if (j < nb) partials[j] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __restrict__ in,
-                                                             int64_t n,
-                                                             const int64_t* __restrict__ partials,
-                                                             int64_t* out) {
-  // each thread owns kScanItems consecutive elements
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kScanTile + threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
-  int64_t s = 0;
+  int64_t sum = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     v[i] = base + i < n ? in[base + i] : 0u;
-    s += v[i];
+    sum += v[i];
   }
   int64_t tot;
-  int64_t run = partials[blockIdx.x] + block_exclusive_scan_i64(s, &tot);
+  const int64_t local = block_exclusive_scan_i64(sum, &tot);
+  if (threadIdx.x == 0) {
+    if (tile == 0) {
+      st_release(status, kFlagInc | static_cast<unsigned long long>(tot));
+      s_excl = 0;
+    } else {
+      st_release(status + tile, kFlagAgg | static_cast<unsigned long long>(tot));
+      const unsigned long long ex = lookback(status, tile, 1);
+      st_release(status + tile, kFlagInc | (ex + static_cast<unsigned long long>(tot)));
+      s_excl = static_cast<int64_t>(ex);
+    }
+  }
+  __syncthreads();
+  int64_t run = s_excl + local;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     if (base + i < n) out[base + i] = run;
     run += v[i];
   }
-  if (base + kScanItems >= n && base < n) {
-    // the thread owning the last element also writes out[n]
-    out[n] = run;
-  }
+  if (base + kScanItems >= n && base < n) out[n] = run;  // owner of the last element
 }
 }  // namespace
 
@@ -105,14 +127,14 @@ void scan_u32_to_i64(const uint32_t* in, int64_t n, int64_t* out, cudaStream_t s
     return;
   }
   const int64_t nb = ceil_div(n, kScanTile);
-  int64_t* partials = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * nb, s));
-  k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partials);
-  after_launch("k_scan_reduce");
-  k_scan_partials<<<1, 1024, 0, s>>>(partials, nb);
-  after_launch("k_scan_partials");
-  k_scan_final<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partials, out);
-  after_launch("k_scan_final");
-  dfree(partials, s);
+  // status words (one per tile) + the tile counter, zeroed together
+  char* ws = static_cast<char*>(dmalloc(sizeof(unsigned long long) * nb + 16, s));
+  TGFX_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * nb + 16, s));
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
+  unsigned int* counter = reinterpret_cast<unsigned int*>(ws + sizeof(unsigned long long) * nb);
+  k_scan_lookback<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, out, status, counter);
+  after_launch("k_scan_lookback");
+  dfree(ws, s);
 }
 
 // ------------------------------------------------------------------ radix sort
@@ -122,60 +144,42 @@ constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsRounds = 8;
 constexpr int kRsTile = kRsThreads * kRsRounds;  // 2048 keys per tile
 
-__global__ void __launch_bounds__(kRsThreads) k_or_and(const uint64_t* __restrict__ keys, int64_t n,
-                                                       unsigned long long* orand) {
-  uint64_t o = 0, a = ~0ull;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    o |= k;
-    a &= k;
+// all digit positions' global histograms in one pass: hist[pass * 256 + digit] (u64)
+template <typename K>
+__global__ void __launch_bounds__(kRsThreads) k_onesweep_hist(const K* __restrict__ keys,
+                                                              int64_t n, int passes,
+                                                              unsigned long long* hist) {
+  __shared__ uint32_t h[8][256];
+  for (int i = threadIdx.x; i < 8 * 256; i += kRsThreads) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)kRsThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kRsThreads) {
+    const K k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
   }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    o |= __shfl_xor_sync(kFull, o, off);
-    a &= __shfl_xor_sync(kFull, a, off);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicOr(&orand[0], (unsigned long long)o);
-    atomicAnd(&orand[1], (unsigned long long)a);
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kRsThreads) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, static_cast<unsigned long long>(c));
   }
 }
 
-// per-tile digit histograms, digit-major: hist[d * ntiles + tile]
-__global__ void __launch_bounds__(kRsThreads) k_digit_hist(const uint64_t* __restrict__ keys,
-                                                           int64_t n, int shift,
-                                                           uint32_t* __restrict__ hist,
-                                                           int64_t ntiles) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRsTile;
-#pragma unroll
-  for (int r = 0; r < kRsRounds; ++r) {
-    const int64_t j = base + r * kRsThreads + threadIdx.x;
-    const unsigned d = j < n ? static_cast<unsigned>((keys[j] >> shift) & 0xff) : 0x100u;
-    const unsigned peers = __match_any_sync(kFull, d);
-    if (d < 256 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
-  }
-  __syncthreads();
-  hist[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-// stable scatter: warp w owns keys [base + w*256, base + (w+1)*256) in 8 rounds of 32
-template <typename V>
-__global__ void __launch_bounds__(kRsThreads) k_digit_scatter(
-    const uint64_t* __restrict__ keys_in, const V* __restrict__ vals_in, int64_t n, int shift,
-    const int64_t* __restrict__ offsets, int64_t ntiles, uint64_t* __restrict__ keys_out,
-    V* __restrict__ vals_out) {
+// one onesweep pass: digit (key >> shift) & 0xff; digit_base[256] = the digit's global start
+template <typename K, typename V>
+__global__ void __launch_bounds__(kRsThreads) k_onesweep(
+    const K* __restrict__ keys_in, const V* __restrict__ vals_in, int64_t n, int shift,
+    const int64_t* __restrict__ digit_base, unsigned long long* status, unsigned int* counter,
+    K* __restrict__ keys_out, V* __restrict__ vals_out) {
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ int64_t goff[256];
+  __shared__ int64_t s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   for (int i = threadIdx.x; i < kRsWarps * 256; i += kRsThreads) (&wcnt[0][0])[i] = 0;
-  goff[threadIdx.x] = offsets[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x];
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRsTile + warp * (kRsRounds * 32);
-  uint64_t k[kRsRounds];
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kRsTile + warp * (kRsRounds * 32);
+  K k[kRsRounds];
   V v[kRsRounds];
   uint32_t rank[kRsRounds];
 #pragma unroll
@@ -184,6 +188,11 @@ __global__ void __launch_bounds__(kRsThreads) k_digit_scatter(
     const bool ok = j < n;
     k[r] = ok ? keys_in[j] : 0;
     v[r] = ok ? vals_in[j] : V(0);
+  }
+#pragma unroll
+  for (int r = 0; r < kRsRounds; ++r) {
+    const int64_t j = base + r * 32 + lane;
+    const bool ok = j < n;
     const unsigned d = ok ? static_cast<unsigned>((k[r] >> shift) & 0xff) : 0x100u;
     const unsigned peers = __match_any_sync(kFull, d);
     const int leader = __ffs(peers) - 1;
@@ -197,7 +206,9 @@ __global__ void __launch_bounds__(kRsThreads) k_digit_scatter(
     __syncwarp();
   }
   __syncthreads();
-  {  // exclusive prefix over warps per digit (thread = digit)
+  __shared__ uint32_t lbase[256];  // tile-local start of each digit (sorted tile order)
+  __shared__ uint32_t wtot[kRsWarps];
+  {  // thread = digit: exclusive prefix over warps, tile count, look-back for the global offset
     const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
@@ -206,58 +217,107 @@ __global__ void __launch_bounds__(kRsThreads) k_digit_scatter(
       wcnt[w][d] = run;
       run += c;
     }
+    unsigned long long* my = status + tile * 256 + d;
+    unsigned long long ex = 0;
+    if (tile == 0) {
+      st_release(my, kFlagInc | run);
+    } else {
+      st_release(my, kFlagAgg | run);
+      ex = lookback(status + d, tile, 256);
+      st_release(my, kFlagInc | (ex + run));
+    }
+    goff[d] = digit_base[d] + static_cast<int64_t>(ex);
+    // tile-local digit starts: exclusive block scan of the digit totals
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wtot[warp] = x;
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) before += w < warp ? wtot[w] : 0u;
+    lbase[d] = before + x - run;
   }
   __syncthreads();
+  // keys and values to their sorted tile positions in shared memory, then written out by
+  // consecutive threads to consecutive global positions (coalesced runs per digit)
+  __shared__ K sk[kRsTile];
+  __shared__ V sv[kRsTile];
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
     const int64_t j = base + r * 32 + lane;
     if (j < n) {
       const unsigned d = static_cast<unsigned>((k[r] >> shift) & 0xff);
-      const int64_t pos = goff[d] + wcnt[warp][d] + rank[r];
-      keys_out[pos] = k[r];
-      vals_out[pos] = v[r];
+      const uint32_t lp = lbase[d] + wcnt[warp][d] + rank[r];
+      sk[lp] = k[r];
+      sv[lp] = v[r];
     }
+  }
+  __syncthreads();
+  const int cnt = static_cast<int>(n - tile * kRsTile < kRsTile ? n - tile * kRsTile : kRsTile);
+  for (int p = threadIdx.x; p < cnt; p += kRsThreads) {
+    const K key = sk[p];
+    const unsigned d = static_cast<unsigned>((key >> shift) & 0xff);
+    const int64_t pos = goff[d] + (p - static_cast<int64_t>(lbase[d]));
+    keys_out[pos] = key;
+    vals_out[pos] = sv[p];
   }
 }
 }  // namespace
 
-template <typename V>
-void radix_sort_pairs(uint64_t*& keys, V*& vals, uint64_t* keys_alt, V* vals_alt, int64_t n,
+template <typename K, typename V>
+void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
                       int max_bits, cudaStream_t s) {
   if (n <= 1) return;
-  unsigned long long* orand = static_cast<unsigned long long*>(dmalloc(16, s));
-  const unsigned long long init[2] = {0ull, ~0ull};
-  TGFX_CUDA(cudaMemcpyAsync(orand, init, 16, cudaMemcpyHostToDevice, s));
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, kRsThreads), 4 * 148));
-  k_or_and<<<grid, kRsThreads, 0, s>>>(keys, n, orand);
-  after_launch("k_or_and");
-  unsigned long long h[2];
-  TGFX_CUDA(cudaMemcpyAsync(h, orand, 16, cudaMemcpyDeviceToHost, s));
-  TGFX_CUDA(cudaStreamSynchronize(s));
-  dfree(orand, s);
-  const uint64_t varying = h[0] ^ h[1];
+  const int passes = std::min(static_cast<int>(sizeof(K)), (max_bits + 7) / 8);
+  if (passes <= 0) return;
   const int64_t ntiles = ceil_div(n, kRsTile);
-  uint32_t* hist = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * 256 * ntiles, s));
-  int64_t* offs = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (256 * ntiles + 1), s));
-  for (int shift = 0; shift < max_bits; shift += 8) {
-    if (((varying >> shift) & 0xffull) == 0) continue;  // digit constant: pass is identity
-    k_digit_hist<<<static_cast<unsigned>(ntiles), kRsThreads, 0, s>>>(keys, n, shift, hist,
-                                                                      ntiles);
-    after_launch("k_digit_hist");
-    scan_u32_to_i64(hist, 256 * ntiles, offs, s);
-    k_digit_scatter<V><<<static_cast<unsigned>(ntiles), kRsThreads, 0, s>>>(
-        keys, vals, n, shift, offs, ntiles, keys_alt, vals_alt);
-    after_launch("k_digit_scatter");
+  // workspace: histograms [passes][256] u64 | digit bases [256] i64 | status [ntiles][256] u64
+  // | tile counter
+  const size_t hb = sizeof(unsigned long long) * 256 * passes;
+  const size_t sb = sizeof(unsigned long long) * 256 * static_cast<size_t>(ntiles);
+  char* ws = static_cast<char*>(dmalloc(hb + 2048 + sb + 16, s));
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(ws);
+  int64_t* dbase = reinterpret_cast<int64_t*>(ws + hb);
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + hb + 2048);
+  unsigned int* counter = reinterpret_cast<unsigned int*>(ws + hb + 2048 + sb);
+  TGFX_CUDA(cudaMemsetAsync(hist, 0, hb, s));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, kRsThreads), 8 * 148));
+  k_onesweep_hist<K><<<grid, kRsThreads, 0, s>>>(keys, n, passes, hist);
+  after_launch("k_onesweep_hist");
+  std::vector<unsigned long long> h(256 * passes);
+  TGFX_CUDA(cudaMemcpyAsync(h.data(), hist, hb, cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaStreamSynchronize(s));
+  for (int p = 0; p < passes; ++p) {
+    const unsigned long long* hp = h.data() + 256 * p;
+    int nonzero = 0;
+    for (int d = 0; d < 256; ++d) nonzero += hp[d] != 0;
+    if (nonzero <= 1) continue;  // digit constant across all keys: the pass is the identity
+    int64_t b[256], run = 0;
+    for (int d = 0; d < 256; ++d) {
+      b[d] = run;
+      run += static_cast<int64_t>(hp[d]);
+    }
+    TGFX_CUDA(cudaMemcpyAsync(dbase, b, sizeof b, cudaMemcpyHostToDevice, s));
+    TGFX_CUDA(cudaMemsetAsync(status, 0, sb + 16, s));
+    k_onesweep<K, V><<<static_cast<unsigned>(ntiles), kRsThreads, 0, s>>>(
+        keys, vals, n, 8 * p, dbase, status, counter, keys_alt, vals_alt);
+    after_launch("k_onesweep");
     std::swap(keys, keys_alt);
     std::swap(vals, vals_alt);
   }
-  dfree(offs, s);
-  dfree(hist, s);
+  TGFX_CUDA(cudaStreamSynchronize(s));  // b[] (host stack) copies done before return
+  dfree(ws, s);
 }
 
-template void radix_sort_pairs<uint32_t>(uint64_t*&, uint32_t*&, uint64_t*, uint32_t*, int64_t,
-                                         int, cudaStream_t);
-template void radix_sort_pairs<uint64_t>(uint64_t*&, uint64_t*&, uint64_t*, uint64_t*, int64_t,
-                                         int, cudaStream_t);
+template void radix_sort_pairs<uint64_t, uint32_t>(uint64_t*&, uint32_t*&, uint64_t*, uint32_t*,
+                                                   int64_t, int, cudaStream_t);
+template void radix_sort_pairs<uint64_t, uint64_t>(uint64_t*&, uint64_t*&, uint64_t*, uint64_t*,
+                                                   int64_t, int, cudaStream_t);
+template void radix_sort_pairs<uint32_t, uint32_t>(uint32_t*&, uint32_t*&, uint32_t*, uint32_t*,
+                                                   int64_t, int, cudaStream_t);
 
 }  // namespace tgfx

@@ -7,8 +7,8 @@ namespace tgfx {
 // Stable LSD radix sort of (key, value) pairs by the low max_bits of key, 8 bits per pass;
 // digits constant across all keys are skipped.  On return keys/vals point at the sorted
 // buffers (either the originals or the alternates).
-template <typename V>
-void radix_sort_pairs(uint64_t*& keys, V*& vals, uint64_t* keys_alt, V* vals_alt, int64_t n,
-                      int max_bits, cudaStream_t s);
+template <typename K, typename V>
+void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n, int max_bits,
+                      cudaStream_t s);
 
 }  // namespace tgfx
