@@ -307,6 +307,22 @@ int tgfx_make_random_stream_device(int64_t num_edges, int64_t num_nodes, uint64_
 int tgfx_make_queries_device(const tgfx_event* d_events, int64_t e0, int64_t e1,
                              int64_t batch, int64_t num_nodes, uint64_t neg_seed,
                              int64_t* d_nodes, double* d_times, void* stream);
+/* The sample_batch queries of one training epoch, on the device: make_batches
+ * (proj/src/training.cpp:157-182: batches of batch_size consecutive events of the training
+ * stream, negatives CounterRng(batch_seed, batch).next_below(num_nodes), neg_per_pos per
+ * event) split as train_epoch does (:425-440, min(workers, b) shards [h*b/m, (h+1)*b/m)), each
+ * shard in forward_concat's layout (:193-209) [src | dst | neg] -- one contiguous block per
+ * sample_batch call, calls in (batch, shard) order.  Batches [b0, b1) of the n-event stream;
+ * writes (min(n, b1*B) - b0*B) * (2 + neg_per_pos) queries.  batch_seed is make_batches'
+ * seed (train_epoch passes tgfx_mix_streams(cfg.seed, 0x6e67, epoch), :422-423). */
+int tgfx_make_train_queries_device(const tgfx_event* d_events, int64_t n, int64_t b0, int64_t b1,
+                                   int64_t batch_size, int64_t neg_per_pos, int64_t workers,
+                                   int64_t num_nodes, uint64_t batch_seed, int64_t* d_nodes,
+                                   double* d_times, void* stream);
+/* training.cpp:16-18 mix_streams: train_epoch's seeds -- make_batches seed
+ * (cfg.seed, 0x6e67, epoch) and the sample seed of step s, shard h
+ * (cfg.seed, epoch * 0x10001 + s, h), :445-446. */
+uint64_t tgfx_mix_streams(uint64_t a, uint64_t b, uint64_t c);
 
 #ifdef __cplusplus
 }

@@ -137,6 +137,7 @@ def ref(native=False):
         L.ref_load_csv.argtypes = [C.c_char_p, C.c_int, _P, _P, _P, _P, _P]
         L.ref_assemble_inputs.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P,
                                           _I64, _I64, _I64, C.c_int, _P]
+        L.ref_train_queries.argtypes = [_P, _I64, _I64, _I64, _I64, _U64, _P, _P, _P]
         _ref = L
     return _ref
 
@@ -159,6 +160,42 @@ def make_random_stream(num_edges, num_nodes, seed, zipf=1.2):
     if rc:
         raise OracleError(1, "bad stream dimensions")
     return ev
+
+
+_M64 = 2**64 - 1
+
+
+def mix_streams(a, b, c):
+    """proj/src/training.cpp:16-18 (train_epoch's seed derivation)."""
+    return mix64((mix64((a ^ 0x8f1bbcdcbfa53e0b) & _M64) ^ mix64(b & _M64) ^
+                  ((c * 0x2545f4914f6cdd1d) & _M64)) & _M64)
+
+
+def make_train_queries(events, batch_size, neg_per_pos, workers, num_nodes, batch_seed):
+    """The sample_batch queries of one train_epoch, concatenated in call order:
+    make_batches (proj/src/training.cpp:157-182; negatives CounterRng(batch_seed, batch index)
+    .next_below(num_nodes), rng.hpp:23-38), split into min(workers, b) shards
+    [h*b/m, (h+1)*b/m) (:425-440), each in forward_concat's layout [src | dst | neg]
+    (:193-209).  Pure restatement (small inputs)."""
+    events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    n = len(events)
+    nodes, times = [], []
+    for b, start in enumerate(range(0, n, batch_size)):
+        stop = min(start + batch_size, n)
+        s0 = mix64((mix64(batch_seed) ^ ((b * 0xd6e8feb86659fd93) & _M64)) & _M64)
+        bs = stop - start
+        neg = [lib().orc_mulhi64(mix64((s0 + d * 0x9e3779b97f4a7c15) & _M64), num_nodes)
+               for d in range(bs * neg_per_pos)]
+        ev = events[start:stop]
+        m = min(workers, bs)
+        for h in range(m):
+            lo, hi = h * bs // m, (h + 1) * bs // m
+            part = ev[lo:hi]
+            nodes += list(part["src"]) + list(part["dst"]) + neg[lo * neg_per_pos:hi * neg_per_pos]
+            times += (list(part["timestamp"]) * 2 +
+                      [float(ev["timestamp"][lo + j // neg_per_pos])
+                       for j in range((hi - lo) * neg_per_pos)])
+    return np.array(nodes, np.int64), np.array(times, np.float64)
 
 
 def zipf_cdf(num_nodes, zipf=1.2):
@@ -532,6 +569,26 @@ def ref_assemble_inputs(node_index, edge_index, time_delta, valid_len, node_tabl
 
 
 # ---------------------------------------------------------------------- CSV ingestion
+def ref_train_queries(events, num_nodes, batch_size, neg_per_pos, workers, batch_seed):
+    """The reference's own make_batches (training.cpp:157-182, compiled in oracle/_ref), split
+    and laid out per call as train_epoch + forward_concat do (ref_harness.cpp)."""
+    events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    n = len(events)
+    q = n * (2 + neg_per_pos)
+    nodes = np.zeros(max(q, 1), np.int64)
+    times = np.zeros(max(q, 1), np.float64)
+    tot = np.zeros(1, np.int64)
+    st = ref().ref_stream_create(_ptr(events), n, num_nodes)
+    try:
+        rc = ref().ref_train_queries(st, batch_size, neg_per_pos, workers, num_nodes,
+                                     batch_seed, _ptr(nodes), _ptr(times), _ptr(tot))
+    finally:
+        ref().ref_stream_free(st)
+    if rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    return nodes[:int(tot[0])], times[:int(tot[0])]
+
+
 def ref_load_csv(path, has_features=False):
     """The reference's own load_csv (event_stream.cpp:85-154, compiled in oracle/_ref) ->
     (events, num_nodes, features [n, d_e]).  Raises OracleError(code, message) with code 1

@@ -20,6 +20,7 @@
 #include "tgformer/sequence.hpp"
 #include "tgformer/synthetic.hpp"
 #include "tgformer/tcsr.hpp"
+#include "tgformer/training.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -318,6 +319,61 @@ int ref_load_csv(const char* path, int has_features, int64_t* n, int64_t* num_no
     return 0;
   } catch (const std::exception& ex) {
     cached_path.clear();
+    return fail(ex);
+  }
+}
+
+// tgf::make_batches (training.cpp:157-182), split into min(workers, b) shards as train_epoch
+// does (:425-440), each shard's queries laid out as forward_concat builds them (:193-209):
+// every sample_batch call of one epoch, concatenated in call order.
+int ref_train_queries(void* stream, int64_t batch_size, int64_t npp, int64_t workers,
+                      int64_t num_nodes, uint64_t seed, int64_t* nodes, double* times,
+                      int64_t* total) {
+  try {
+    const auto& st = *static_cast<const tgf::EventStream*>(stream);
+    const std::vector<tgf::LinkBatch> batches =
+        tgf::make_batches(st, batch_size, npp, num_nodes, seed);
+    int64_t o = 0;
+    for (const tgf::LinkBatch& batch : batches) {
+      const auto b = static_cast<int64_t>(batch.src.size());
+      const int64_t m = std::min<int64_t>(workers, b);
+      for (int64_t shard = 0; shard < m; ++shard) {
+        const int64_t lo = shard * b / m, hi = (shard + 1) * b / m;
+        for (int64_t i = lo; i < hi; ++i) {
+          nodes[o] = batch.src[i];
+          times[o++] = batch.times[i];
+        }
+        for (int64_t i = lo; i < hi; ++i) {
+          nodes[o] = batch.dst[i];
+          times[o++] = batch.times[i];
+        }
+        for (int64_t j = lo * npp; j < hi * npp; ++j) {
+          nodes[o] = batch.neg[j];
+          times[o++] = batch.times[j / npp];
+        }
+      }
+    }
+    *total = o;
+    return 0;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
+// tgf::save_tcsr / tgf::load_tcsr (tcsr.cpp:153-197) -- container interop checks
+int ref_save_tcsr(void* gp, const char* path) {
+  try {
+    tgf::save_tcsr(*static_cast<tgf::TCsr*>(gp), path);
+    return 0;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+int ref_load_tcsr(const char* path, void** out) {
+  try {
+    *out = new tgf::TCsr(tgf::load_tcsr(path));
+    return 0;
+  } catch (const std::exception& ex) {
     return fail(ex);
   }
 }

@@ -97,6 +97,9 @@ SIGNATURES = {
     "tgfx_sample_assemble_checked_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64,
                                             _P, _P, _P, _P, _P, _P, _P, _U],
     "tgfx_query_error": [_P, _U64, _P, _P],
+    "tgfx_make_train_queries_device": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _U64, _P,
+                                       _P, _P],
+    "tgfx_mix_streams": [_U64, _U64, _U64],
     "tgfx_sample_assemble_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P,
                                     _P, _P, _P, _P, _U],
     "tgfx_sample_assemble_batched_device": [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I64, _I64,
@@ -121,7 +124,8 @@ SIGNATURES = {
     "tgfx_make_queries_device": [_P, _I64, _I64, _I64, _I64, _U64, _P, _P, _P],
 }
 _RESTYPE = {"tgfx_last_error": C.c_char_p, "tgfx_launch_count": C.c_uint64,
-            "tgfx_device_bytes": C.c_int64, "tgfx_partition_warps": C.c_int64}
+            "tgfx_device_bytes": C.c_int64, "tgfx_partition_warps": C.c_int64,
+            "tgfx_mix_streams": C.c_uint64}
 
 _lib = None
 

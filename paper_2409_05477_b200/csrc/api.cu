@@ -1301,4 +1301,20 @@ int tgfx_make_queries_device(const tgfx_event* d_events, int64_t e0, int64_t e1,
   });
 }
 
+int tgfx_make_train_queries_device(const tgfx_event* d_events, int64_t n, int64_t b0, int64_t b1,
+                                   int64_t batch_size, int64_t neg_per_pos, int64_t workers,
+                                   int64_t num_nodes, uint64_t batch_seed, int64_t* d_nodes,
+                                   double* d_times, void* stream) {
+  return guarded([&] {
+    device_info();
+    launch_train_queries(d_events, n, b0, b1, batch_size, neg_per_pos, workers, num_nodes,
+                         batch_seed, d_nodes, d_times, as_stream(stream));
+  });
+}
+
+uint64_t tgfx_mix_streams(uint64_t a, uint64_t b, uint64_t c) {
+  // training.cpp:16-18
+  return mix64(mix64(a ^ 0x8f1bbcdcbfa53e0bULL) ^ mix64(b) ^ (c * 0x2545f4914f6cdd1dULL));
+}
+
 }  // extern "C"

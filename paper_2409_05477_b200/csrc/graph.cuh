@@ -218,6 +218,9 @@ void launch_random_stream(int64_t E, int64_t V, uint64_t seed, double zipf, tgfx
                           cudaStream_t s);
 void launch_make_queries(const tgfx_event* ev, int64_t e0, int64_t e1, int64_t batch, int64_t V,
                          uint64_t neg_seed, int64_t* nodes, double* times, cudaStream_t s);
+void launch_train_queries(const tgfx_event* ev, int64_t n, int64_t b0, int64_t b1, int64_t B,
+                          int64_t npp, int64_t workers, int64_t V, uint64_t batch_seed,
+                          int64_t* nodes, double* times, cudaStream_t s);
 
 // ------------------------------------------------------------------ partitioned build
 void launch_degree_hist(const tgfx_event* ev, int64_t n, int64_t V, int reverse,

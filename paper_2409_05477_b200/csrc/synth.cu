@@ -84,6 +84,45 @@ __global__ void k_queries(const tgfx_event* __restrict__ ev, int64_t e0, int64_t
   }
 }
 
+// train_epoch's sample_batch calls (training.cpp:419-473): batch b = events [b*B, b*B + bs) of
+// the training stream (make_batches, :157-182), split into `workers` shards [lo, hi) =
+// [h*bs/m, (h+1)*bs/m); each shard's call is forward_concat's layout (:193-209)
+// [src (pb) | dst (pb) | neg (pb*npp)], neg of batch-relative event r, draw j =
+// CounterRng(batch_seed, b).next_below(V) as the (r*npp + j)-th draw.  One thread per event of
+// batches [b0, b1); output offset of batch b = (b*B - b0*B) * (2 + npp).
+__global__ void k_train_queries(const tgfx_event* __restrict__ ev, int64_t n, int64_t b0,
+                                int64_t b1, int64_t B, int64_t npp, int64_t m, int64_t V,
+                                uint64_t batch_seed, int64_t* nodes, double* times) {
+  const int64_t e0 = b0 * B, e1 = min(n, b1 * B);
+  for (int64_t i = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / B;
+    const int64_t sb = b * B;
+    const int64_t bs = min(B, n - sb);
+    const int64_t r = i - sb;
+    const int64_t mm = min(m, bs);  // train_epoch: m = min(workers, b)
+    // shard h with lo = h*bs/mm <= r < hi: the largest h with h*bs/mm <= r
+    int64_t h = (r * mm) / bs;
+    while (h + 1 < mm && ((h + 1) * bs) / mm <= r) ++h;
+    while (h > 0 && (h * bs) / mm > r) --h;
+    const int64_t lo = (h * bs) / mm, hi = ((h + 1) * bs) / mm;
+    const int64_t pb = hi - lo, w = r - lo;
+    const int64_t o = (sb - e0) * (2 + npp) + lo * (2 + npp);
+    const Ev x = load_event(ev, i);
+    nodes[o + w] = x.src;
+    times[o + w] = x.t;
+    nodes[o + pb + w] = x.dst;
+    times[o + pb + w] = x.t;
+    const uint64_t s0 = rng_state(batch_seed, static_cast<uint64_t>(b));
+    for (int64_t j = 0; j < npp; ++j) {
+      const int64_t q = o + 2 * pb + w * npp + j;
+      nodes[q] = static_cast<int64_t>(
+          mulhi64(rng_draw(s0, static_cast<uint64_t>(r * npp + j)), static_cast<uint64_t>(V)));
+      times[q] = x.t;
+    }
+  }
+}
+
 int grid_for(int64_t work) {
   return static_cast<int>(
       std::min<int64_t>(ceil_div(std::max<int64_t>(work, 1), 256), device_info().sms * 16));
@@ -128,6 +167,20 @@ void launch_make_queries(const tgfx_event* ev, int64_t e0, int64_t e1, int64_t b
   if (batch < 1) throw Error(TGFX_EVALIDATION, "bad batch parameters");
   k_queries<<<grid_for(e1 - e0), 256, 0, s>>>(ev, e0, e1, batch, V, neg_seed, nodes, times);
   after_launch("k_queries");
+}
+
+void launch_train_queries(const tgfx_event* ev, int64_t n, int64_t b0, int64_t b1, int64_t B,
+                          int64_t npp, int64_t workers, int64_t V, uint64_t batch_seed,
+                          int64_t* nodes, double* times, cudaStream_t s) {
+  // make_batches (training.cpp:160-161) and train config checks
+  if (n == 0) throw Error(TGFX_EVALIDATION, "empty training stream");
+  if (B < 1 || npp < 1) throw Error(TGFX_EVALIDATION, "bad batch parameters");
+  if (workers < 1) throw Error(TGFX_EVALIDATION, "workers must be >= 1");
+  if (b0 < 0 || b1 < b0 || b1 > ceil_div(n, B)) throw Error(TGFX_EVALIDATION, "bad batch range");
+  if (b1 == b0) return;
+  k_train_queries<<<grid_for(std::min(n, b1 * B) - b0 * B), 256, 0, s>>>(
+      ev, n, b0, b1, B, npp, workers, V, batch_seed, nodes, times);
+  after_launch("k_train_queries");
 }
 
 }  // namespace tgfx

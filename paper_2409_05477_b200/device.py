@@ -82,6 +82,40 @@ def make_queries(ev, e0, e1, batch, num_nodes, neg_seed=7, nodes=None, times=Non
     return nodes[:q], times[:q]
 
 
+def mix_streams(a, b, c):
+    """training.cpp:16-18 (train_epoch's seed derivation), via libtgfx."""
+    return int(lib().tgfx_mix_streams(a & (2**64 - 1), b & (2**64 - 1), c & (2**64 - 1)))
+
+
+def make_train_queries(ev, n, b0, b1, batch_size, neg_per_pos, workers, num_nodes, batch_seed,
+                       nodes=None, times=None, stream=None):
+    """train_epoch's sample_batch queries for batches [b0, b1) of the n-event training stream
+    ev (make_batches negatives, workers shards, forward_concat layout per call), on device."""
+    q = (min(n, b1 * batch_size) - b0 * batch_size) * (2 + neg_per_pos)
+    nodes = torch.empty(max(q, 1), dtype=torch.int64, device="cuda") if nodes is None else nodes
+    times = torch.empty(max(q, 1), dtype=torch.float64, device="cuda") if times is None else times
+    check(lib().tgfx_make_train_queries_device(_p(ev), n, b0, b1, batch_size, neg_per_pos, workers,
+                                               num_nodes, batch_seed & (2**64 - 1), _p(nodes),
+                                               _p(times), _stream(stream)))
+    return nodes[:q], times[:q]
+
+
+def train_calls(n, batch_size, neg_per_pos, workers, cfg_seed, epoch):
+    """(offset, size, sample_seed) of every sample_batch call of train_epoch (training.cpp:
+    425-446) in the make_train_queries layout."""
+    out, off = [], 0
+    nb = -(-n // batch_size)
+    for step in range(nb):
+        bs = min(batch_size, n - step * batch_size)
+        m = min(workers, bs)
+        for h in range(m):
+            pb = (h + 1) * bs // m - h * bs // m
+            size = pb * (2 + neg_per_pos)
+            out.append((off, size, mix_streams(cfg_seed, epoch * 0x10001 + step, h)))
+            off += size
+    return out
+
+
 def alloc_rows(q, l, index64=False, dt32=True, dt64=False):
     it = torch.int64 if index64 else torch.int32
     d = dict(node_index=torch.empty((q, l), dtype=it, device="cuda"),

@@ -55,3 +55,34 @@ def test_reference_unit_tests_against_device_api():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "0 failed" in r.stdout
+
+
+def _ref_so():
+    p = os.path.join(ROOT, "oracle", "_ref", "libtgf_ref.so")
+    if not os.path.exists(p):
+        pytest.skip("oracle/_ref not built")
+    return p
+
+
+@pytest.mark.gpu
+def test_container_interop_with_reference(tmp_path):
+    """save_tcsr / load_tcsr (tcsr.cpp:153-197) both ways against the reference's own, and
+    byte-identical containers for the same graph (tests/cpp/tcsr_interop.cpp)."""
+    _ensure_built("ours")
+    r = subprocess.run([os.path.join(CPP, "tcsr_interop"), _ref_so(), str(tmp_path)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "interop ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_container_above_4gib_round_trip(tmp_path):
+    """A >= 4 GiB container round-trips through ours (the reference's load computes its CRC
+    over the length truncated to 32 bits, binary_io.hpp:95-96, and rejects it)."""
+    _ensure_built("ours")
+    import shutil
+    if shutil.disk_usage(str(tmp_path)).free < (6 << 30):
+        pytest.skip("needs 6 GiB of scratch disk")
+    r = subprocess.run([os.path.join(CPP, "tcsr_interop"), _ref_so(), str(tmp_path), "big"],
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0 and "big ok" in r.stdout, r.stdout + r.stderr
+    print(r.stdout)

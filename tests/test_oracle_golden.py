@@ -138,3 +138,22 @@ def test_assemble_inputs_restatement_vs_reference(oracle_mod):
     bad[0, 0] = 40
     with pytest.raises(oracle_mod.OracleError):
         oracle_mod.assemble_inputs(bad, ei, dt, vl, nt, et, om, ph, True)
+
+
+def test_train_queries_restatement_vs_reference(oracle_mod):
+    """make_batches + train_epoch's shard split + forward_concat layout (training.cpp:157-209,
+    425-440): the restatement against the reference's own make_batches (oracle/_ref)."""
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ev = oracle_mod.make_random_stream(7_000, 400, 5)
+    for npp, workers, B in ((1, 1, 200), (3, 1, 333), (2, 3, 250), (1, 8, 64)):
+        seed = oracle_mod.mix_streams(17, 0x6e67, 4)
+        got = oracle_mod.make_train_queries(ev, B, npp, workers, 400, seed)
+        want = oracle_mod.ref_train_queries(ev, 400, B, npp, workers, seed)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_mix_streams_device_library_matches_restatement(oracle_mod):
+    from paper_2409_05477_b200 import device as D
+    for a, b, c in ((0, 0x6e67, 0), (17, 3 * 0x10001 + 5, 2), (2**64 - 1, 2**63, 7)):
+        assert D.mix_streams(a, b, c) == oracle_mod.mix_streams(a, b, c)
