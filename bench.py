@@ -44,6 +44,10 @@ CONFIGS = {
               name="Wikipedia-shaped synthetic (V=9,227, E=157,474)"),
     "L": dict(E=1_293_103, V=1980, strategy="random", k=20, l=21, B=4000,
               name="LastFM-shaped synthetic (V=1,980, E=1,293,103)"),
+    # Reddit-shaped (BASELINE configs[1]): 2-hop recent 10x10 of every root;
+    # hop-2 rows [Q, k1, l] beside the hop-1 rows (device path only: no e2e / CPU legs)
+    "R": dict(E=672_447, V=10_984, strategy="recent", k=10, l=11, B=600, two_hop=True,
+              name="Reddit-shaped synthetic (V=10,984, E=672,447, Zipf 1.2), 2-hop recent 10x10"),
     # MAG-shaped (BASELINE configs[4]): at N > 1 the T-CSR comes from the node-range-partitioned
     # build (one NCCL all-to-all) + all-gather replication, then query-sharded sampling.  The
     # full shape needs N >= 4 (41.6 GB stream + 63 GB T-CSR + records per replica); M16 is the
@@ -298,7 +302,13 @@ def run_ours(args, cfg):
                        times=times[3 * e0 - q_lo:3 * e1 - q_lo])
     chunk = args.chunk
     chunks = S.chunks(q_lo, q_hi, chunk)
-    out = D.alloc_rows(min(chunk, max(q_hi - q_lo, 1)), l)
+    two = bool(cfg.get("two_hop"))
+    if two:  # hop-1 rows + hop-2 rows [q, k, l] per chunk
+        cq = min(chunk, max(q_hi - q_lo, 1))
+        out = dict(h1=D.alloc_rows(cq, l), h2=D.alloc_rows(cq * k, l))
+        args.no_e2e = args.no_cpu = True
+    else:
+        out = D.alloc_rows(min(chunk, max(q_hi - q_lo, 1)), l)
     # the T-CSR every rank samples: a local build of the whole stream (a replica), or for the
     # partitioned configs at N > 1 the node-range-partitioned build + all-gather replication
     part = bool(cfg.get("partitioned")) and ws > 1
@@ -347,6 +357,17 @@ def run_ours(args, cfg):
         for i, (s, e) in enumerate(chunks):
             if record:
                 record["c"][i][0].record(stream)
+            if two:
+                sub2 = dict(h1={kk: vv[: e - s] for kk, vv in out["h1"].items()},
+                            h2={kk: vv[: (e - s) * k] for kk, vv in out["h2"].items()})
+                D.two_hop(g, nodes[s - q_lo:e - q_lo], times[s - q_lo:e - q_lo], k, k, strat, 9,
+                          l, E + 1, out=sub2)
+                if record:
+                    record["c"][i][1].record(stream)
+                if taken is not None:
+                    taken.append(int(sub2["h1"]["valid_len"].sum().item()) - (e - s))
+                    taken2.append(int((sub2["h2"]["valid_len"].clamp(min=1) - 1).sum().item()))
+                continue
             sub = {kk: vv[: e - s] for kk, vv in out.items()}
             D.sample_assemble(g, nodes[s - q_lo:e - q_lo], times[s - q_lo:e - q_lo], k, strat, 9,
                               l, E + 1, out=sub,
@@ -359,7 +380,7 @@ def run_ours(args, cfg):
                 expect.append({kk: vv[ix].cpu().numpy() for kk, vv in sub.items()})
         D.query_error(nodes, first_bad, stream_base=q_lo)
 
-    taken = []
+    taken, taken2 = [], []
     for w in range(args.warmup):
         one_step(taken=taken if w == 0 else None)
     if not taken:
@@ -421,6 +442,8 @@ def run_ours(args, cfg):
     # algorithmic bytes, this rank's launches
     build_bytes = 32 * E + 24 * 2 * E + 8 * (V + 1)
     samp_bytes_local = 16 * q_local + 16 * q_local + 24 * local_taken + (12 * l + 4) * q_local
+    if two:  # + hop-2: every hop-1 entry is a query (indptr pair + its window), k rows per root
+        samp_bytes_local += 16 * local_taken + 24 * sum(taken2) + (12 * l + 4) * k * q_local
     avg_launch_ms = statistics.mean(samp_launch_ms)
     bytes_per_launch = samp_bytes_local / max(len(chunks), 1)
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
@@ -444,8 +467,12 @@ def run_ours(args, cfg):
                         "what": "rebuild + k_widen of the int64 neighbor_ids/edge_ids columns "
                                 "(the reference TCsr layout); not part of the step"},
         "sample": {"ms": samp_med, "queries_per_s": q_all / (samp_med * 1e-3),
+                   **({"hop2_rows_per_s": k * q_all / (samp_med * 1e-3),
+                       "mean_taken_hop2": sum(taken2) / max(local_taken, 1)} if two else {}),
                    "launches_per_step": len(chunks), "mean_taken": taken_all / max(q_all, 1)},
-        "roofline": {"kernel": "k_recent_line (fused recent-k line-probe sampler + sequence packing)",
+        "roofline": {"kernel": ("k_recent_line x3 (2-hop: hop-1 rows, hop-1 entries, hop-2 rows)"
+                                if two else
+                                "k_recent_line (fused recent-k line-probe sampler + sequence packing)"),
                      "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": bytes_per_launch,
@@ -551,6 +578,8 @@ def measure_partitioned(ev_any, E, V, ws, rank, share, red, stream, owned_chunk=
 def load_traffic(cfg, bytes_per_launch):
     """DRAM bytes per k_recent launch from the committed ncu --set full summary, scaled from
     the profiled launch's query count to this launch (null if absent)."""
+    if cfg is not CONFIGS["G"]:  # the committed capture is of the GDELT-shaped launch
+        return None
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
