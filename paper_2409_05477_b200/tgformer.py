@@ -60,7 +60,7 @@ class EventStream:
 
 
 def parse_strategy(name):
-    """proj/src/sampler.cpp:234-238"""
+    """tgf::parse_strategy (proj/src/sampler.cpp:35-39)"""
     if name == "recent":
         return "recent"
     if name == "random":
@@ -69,7 +69,7 @@ def parse_strategy(name):
 
 
 def parse_mask_kind(name):
-    """proj/src/sequence.cpp:353-358"""
+    """tgf::parse_mask_kind (proj/src/sequence.cpp:48-53)"""
     if name in ("causal", "tgat", "self_loop"):
         return name
     raise ValidationError(f"unknown mask kind '{name}'")
