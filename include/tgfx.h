@@ -272,6 +272,23 @@ int tgfx_assemble_inputs_device(int64_t q, int64_t l, const void* d_node_index,
                                 int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
                                 void* stream, unsigned flags);
 
+/* forward_concat's sampling, sequence assembly and model_forward's assemble_inputs
+ * (training.cpp:211-214, attention.cpp:414-451) in one call: z [q*l, d] of the sampled
+ * sequences (d = d_t for combine sum, d_v + d_e + d_t for concat), as
+ * tgfx_assemble_inputs_device(tgfx_sample_assemble_device(...)) with fp64 time deltas
+ * computes it.  Recent-k on line-probe graphs runs ONE kernel (the index / delta rows never
+ * reach HBM); other cases compose the two on the device.  d_valid_len (int32 [q]) optional.
+ * Validation as tgfx_sample_assemble_device, plus the reference's "sequence index outside
+ * embedding tables". */
+int tgfx_sample_inputs_device(const tgfx_graph* g, const int64_t* d_nodes, const double* d_times,
+                              int64_t q, int64_t k, int strategy, uint64_t seed,
+                              uint64_t stream_base, int64_t l, int64_t self_edge_index,
+                              const void* d_node_table, int64_t node_rows,
+                              const void* d_edge_table, int64_t edge_rows, int table_type,
+                              const double* d_omega, const double* d_phi, int64_t d_v,
+                              int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
+                              int32_t* d_valid_len, void* stream, unsigned flags);
+
 /* ---------------------------------------------------------------- CSV ingestion */
 /* replaces tgf::load_csv (event_stream.hpp:44, event_stream.cpp:85-154): reads the file,
  * parses it on the device (header required; rows "src,dst,timestamp[,features]"), stable

@@ -100,6 +100,9 @@ SIGNATURES = {
     "tgfx_make_train_queries_device": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _U64, _P,
                                        _P, _P],
     "tgfx_mix_streams": [_U64, _U64, _U64],
+    "tgfx_sample_inputs_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _I64,
+                                  _P, _I64, _I, _P, _P, _I64, _I64, _I64, _I, _P, _I, _P, _P,
+                                  _U],
     "tgfx_sample_assemble_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P,
                                     _P, _P, _P, _P, _U],
     "tgfx_sample_assemble_batched_device": [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I64, _I64,

@@ -941,6 +941,84 @@ int tgfx_assemble_inputs_device(int64_t q, int64_t l, const void* d_node_index,
   });
 }
 
+int tgfx_sample_inputs_device(const tgfx_graph* g, const int64_t* d_nodes, const double* d_times,
+                              int64_t q, int64_t k, int strategy, uint64_t seed,
+                              uint64_t stream_base, int64_t l, int64_t self_edge_index,
+                              const void* d_node_table, int64_t node_rows,
+                              const void* d_edge_table, int64_t edge_rows, int table_type,
+                              const double* d_omega, const double* d_phi, int64_t d_v,
+                              int64_t d_e, int64_t d_t, int concat, void* d_z, int z_type,
+                              int32_t* d_valid_len, void* stream, unsigned flags) {
+  return guarded([&] {
+    check_graph(g);
+    cudaStream_t s = as_stream(stream);
+    if (!(flags & TGFX_TRUSTED)) check_queries(g, d_nodes, q, k, s);
+    check_k(k);
+    check_l(l);
+    if (d_v < 0 || d_e < 0 || d_t < 0) throw Error(TGFX_EVALIDATION, "bad model dimensions");
+    if (!concat && !(d_v == d_t && d_e == d_t))  // ModelConfig::validate, attention.hpp:21-23
+      throw Error(TGFX_EVALIDATION, "combine sum requires d_v = d_e = d_t = d_model");
+    SampleInputsArgs a;
+    a.s.g = g;
+    a.s.nodes = d_nodes;
+    a.s.times = d_times;
+    a.s.q = q;
+    a.s.k = k;
+    a.s.strategy = strategy;
+    a.s.seed = seed;
+    a.s.stream_base = stream_base;
+    a.s.l = l;
+    a.s.self_edge_index = self_edge_index;
+    a.s.valid_len = d_valid_len;
+    a.in.q = q;
+    a.in.l = l;
+    a.in.node_table = d_node_table;
+    a.in.edge_table = d_edge_table;
+    a.in.node_rows = node_rows;
+    a.in.edge_rows = edge_rows;
+    a.in.table_type = table_type;
+    a.in.omega = d_omega;
+    a.in.phi = d_phi;
+    a.in.d_v = d_v;
+    a.in.d_e = d_e;
+    a.in.d_t = d_t;
+    a.in.concat = concat;
+    a.in.z = d_z;
+    a.in.z_type = z_type;
+    DBuf bad(sizeof(int), s);
+    TGFX_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    if (!launch_sample_inputs(a, bad.as<int>(), s)) {
+      // uniform-k or an exact-search graph: the composition, through device row buffers
+      check_int32_outputs(g, self_edge_index);
+      const size_t ql = static_cast<size_t>(std::max<int64_t>(q, 1)) * static_cast<size_t>(l);
+      DBuf ni(sizeof(int32_t) * ql, s), ei(sizeof(int32_t) * ql, s), dt(sizeof(double) * ql, s);
+      DBuf vl(sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(q, 1)), s);
+      SampleArgs sa = a.s;
+      sa.node_index = ni.p;
+      sa.edge_index = ei.p;
+      sa.dt64 = dt.as<double>();
+      sa.valid_len = d_valid_len ? static_cast<void*>(d_valid_len) : vl.p;
+      sa.index64 = false;
+      launch_sample(sa, s);
+      AssembleInputsArgs ia = a.in;
+      ia.node_index = ni.p;
+      ia.edge_index = ei.p;
+      ia.time_delta = dt.p;
+      ia.valid_len = sa.valid_len;
+      ia.index64 = 0;
+      ia.dt_type = TGFX_F64;
+      launch_assemble_inputs(ia, bad.as<int>(), s);
+      TGFX_CUDA(cudaStreamSynchronize(s));  // the row buffers are released below
+    }
+    if (!(flags & TGFX_TRUSTED)) {
+      int h = 0;
+      TGFX_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TGFX_CUDA(cudaStreamSynchronize(s));
+      if (h) throw Error(TGFX_EVALIDATION, "sequence index outside embedding tables");
+    }
+  });
+}
+
 int tgfx_sample_assemble_batched_device(const tgfx_graph* g, const int64_t* d_nodes,
                                         const double* d_times, int64_t q, int64_t batch_q,
                                         int64_t k, int strategy, const uint64_t* d_seeds,

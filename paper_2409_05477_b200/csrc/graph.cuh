@@ -194,6 +194,14 @@ struct AssembleInputsArgs {
 };
 void launch_assemble_inputs(const AssembleInputsArgs& a, int* bad, cudaStream_t s);
 
+// fused sampler + assemble_inputs (recent-k, line-probe graphs): s = the sampling arguments
+// (valid_len int32 or null), in = the tables / z (its row fields unused); false = not taken
+struct SampleInputsArgs {
+  SampleArgs s;
+  AssembleInputsArgs in;
+};
+bool launch_sample_inputs(const SampleInputsArgs& a, int* bad, cudaStream_t s);
+
 // ------------------------------------------------------------------ CSV ingestion
 struct CsvResult {
   int64_t n = 0, num_nodes = 0;

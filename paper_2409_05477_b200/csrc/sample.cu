@@ -25,6 +25,8 @@
 //     dt = t_q - ts in fp64 then rounded to fp32 (and/or kept as fp64).
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "graph.cuh"
 
 namespace tgfx {
@@ -639,6 +641,162 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       }
     }
     __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ sampler + assemble_inputs
+// forward_concat's sample_batch -> build_sequence_batch -> model_forward's assemble_inputs
+// (training.cpp:211-214, attention.cpp:414-451) in ONE kernel for recent-k: a warp searches
+// its 32 queries as k_recent_line does, keeps (window start, query time, node, kb) in shared
+// memory, then writes the Transformer input rows z [32 * l, d] directly -- lanes across the
+// columns, the slot's entry read once (broadcast) from the gather records -- so the int
+// index / delta rows never go through HBM.  Δt is the fp64 difference (the reference's
+// SequenceBatch::time_delta), the time encoding cos(omega * Δt + phi) is computed in fp64 and
+// rounded once to the output type, as k_assemble_inputs does.
+template <typename T>
+__device__ __forceinline__ double fin_f64(T v) {
+  return static_cast<double>(v);
+}
+template <typename T>
+__device__ __forceinline__ T fin_out(double v) {
+  return static_cast<T>(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 fin_out<__nv_bfloat16>(double v) {
+  return __double2bfloat16(v);
+}
+
+template <typename TabT, typename OutT, bool REC>
+__global__ void __launch_bounds__(kThreads, 4) k_recent_inputs(
+    const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
+    const int64_t* __restrict__ eid, const double* __restrict__ ts,
+    const uint4* __restrict__ rec, QueryIn in, int64_t Q, int64_t k, int l, int64_t self_idx,
+    const TabT* __restrict__ ntab, int64_t nrows, const TabT* __restrict__ etab, int64_t erows,
+    const double* __restrict__ omega, const double* __restrict__ phi, int d_v, int d_e, int d_t,
+    int concat, OutT* __restrict__ z, int32_t* __restrict__ vlen, int* __restrict__ bad) {
+  // a block per group: one warp searches the group's 32 queries, the block writes the rows
+  extern __shared__ double s_wp[];  // omega [d_t] | phi [d_t]
+  __shared__ int64_t s_st[32];
+  __shared__ double s_t[32];
+  __shared__ int64_t s_u[32];
+  __shared__ int s_kb[32];
+  for (int c = threadIdx.x; c < d_t; c += kThreads) {
+    s_wp[c] = omega[c];
+    s_wp[d_t + c] = phi[c];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = concat ? d_v + d_e + d_t : d_t;
+  const int64_t ngroups = ceil_div(Q, 32);
+  // one block per group of 32 queries: warp 0 searches them, all warps write the rows
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    if (warp == 0) {
+      const int64_t q = g * 32 + lane;
+      int64_t u = 0, m[1];
+      double t = 0.0;
+      bool pres[1];
+      pres[0] = q < Q && fetch_query(in, q, u, t);
+      NodeDir dd[1];
+      dd[0] = load_dir(dir, u, pres[0]);
+      double tt[1] = {t};
+      search_lines<kProbeW, 1>(ts, dd, pres, tt, m);
+      int kb = -1;
+      if (pres[0]) kb = static_cast<int>(min(min(k, m[0]), static_cast<int64_t>(l - 1)));
+      if (q < Q && vlen) vlen[q] = kb + 1;
+      s_st[lane] = dd[0].start + m[0] - kb;
+      s_t[lane] = t;
+      s_u[lane] = u;
+      s_kb[lane] = kb;
+    }
+    __syncthreads();
+    const int nq = static_cast<int>(min(static_cast<int64_t>(32), Q - g * 32));
+    for (int r = warp; r < nq * l; r += kWarps) {
+      const int qi = r / l, j = r - qi * l;
+      const int kbq = s_kb[qi];
+      OutT* zr = z + (g * 32 + qi) * static_cast<int64_t>(l) * d + static_cast<int64_t>(j) * d;
+      if (j > kbq) {  // padding row (and absent queries): zeros, as the reference's Matrix
+        for (int c = lane; c < d; c += 32) zr[c] = fin_out<OutT>(0.0);
+        continue;
+      }
+      int64_t ni, ei;
+      double dt;
+      if (j < kbq) {
+        const int64_t p = s_st[qi] + j;
+        int64_t nb, ed;
+        double tv;
+        if (REC) {
+          const uint4 e = __ldg(rec + p);
+          nb = e.x;
+          ed = e.y;
+          tv = __hiloint2double(static_cast<int>(e.w), static_cast<int>(e.z));
+        } else {
+          nb = __ldg(reinterpret_cast<const long long*>(nbr) + p);
+          ed = __ldg(reinterpret_cast<const long long*>(eid) + p);
+          tv = __ldg(ts + p);
+        }
+        ni = nb + 1;
+        ei = ed + 1;
+        dt = s_t[qi] - tv;
+      } else {  // the self-loop token (sequence.cpp:79-81)
+        ni = s_u[qi] + 1;
+        ei = self_idx;
+        dt = 0.0;
+      }
+      if (ni < 0 || ni >= nrows || ei < 0 || ei >= erows) {  // attention.cpp:427-431
+        if (lane == 0 && bad) atomicOr(bad, 1);
+        continue;
+      }
+      const TabT* nrow = ntab + ni * d_v;
+      const TabT* erow = etab + ei * d_e;
+      if (!concat) {
+        for (int c = lane; c < d; c += 32)
+          zr[c] = fin_out<OutT>(fin_f64(__ldg(nrow + c)) + fin_f64(__ldg(erow + c)) +
+                                cos(s_wp[c] * dt + s_wp[d_t + c]));
+      } else {
+        for (int c = lane; c < d_v; c += 32) zr[c] = fin_out<OutT>(fin_f64(__ldg(nrow + c)));
+        for (int c = lane; c < d_e; c += 32) zr[d_v + c] = fin_out<OutT>(fin_f64(__ldg(erow + c)));
+        for (int c = lane; c < d_t; c += 32)
+          zr[d_v + d_e + c] = fin_out<OutT>(cos(s_wp[c] * dt + s_wp[d_t + c]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename TabT, typename OutT>
+void launch_recent_inputs_t(const SampleInputsArgs& a, int* bad, cudaStream_t s) {
+  const tgfx_graph* g = a.s.g;
+  QueryIn in{a.s.nodes, a.s.times, nullptr, 0, nullptr, 0, g->V, a.s.first_bad, a.s.stream_base};
+  const int64_t groups = ceil_div(a.s.q, 32);
+  const int grid = static_cast<int>(std::min<int64_t>(groups, static_cast<int64_t>(device_info().sms) * 16));
+  const size_t smem = sizeof(double) * 2 * static_cast<size_t>(a.in.d_t);
+  const int l = static_cast<int>(a.s.l);
+  auto* z = static_cast<OutT*>(a.in.z);
+  auto* vl = static_cast<int32_t*>(a.s.valid_len);
+  if (g->rec)
+    k_recent_inputs<TabT, OutT, true><<<grid, kThreads, smem, s>>>(
+        g->dir, g->nbr, g->eid, g->ts, g->rec, in, a.s.q, a.s.k, l, a.s.self_edge_index,
+        static_cast<const TabT*>(a.in.node_table), a.in.node_rows,
+        static_cast<const TabT*>(a.in.edge_table), a.in.edge_rows, a.in.omega, a.in.phi,
+        static_cast<int>(a.in.d_v), static_cast<int>(a.in.d_e), static_cast<int>(a.in.d_t),
+        a.in.concat, z, vl, bad);
+  else
+    k_recent_inputs<TabT, OutT, false><<<grid, kThreads, smem, s>>>(
+        g->dir, g->nbr, g->eid, g->ts, nullptr, in, a.s.q, a.s.k, l, a.s.self_edge_index,
+        static_cast<const TabT*>(a.in.node_table), a.in.node_rows,
+        static_cast<const TabT*>(a.in.edge_table), a.in.edge_rows, a.in.omega, a.in.phi,
+        static_cast<int>(a.in.d_v), static_cast<int>(a.in.d_e), static_cast<int>(a.in.d_t),
+        a.in.concat, z, vl, bad);
+  after_launch("k_recent_inputs");
+}
+
+template <typename TabT>
+void launch_recent_inputs_tab(const SampleInputsArgs& a, int* bad, cudaStream_t s) {
+  switch (a.in.z_type) {
+    case TGFX_F32: launch_recent_inputs_t<TabT, float>(a, bad, s); break;
+    case TGFX_F64: launch_recent_inputs_t<TabT, double>(a, bad, s); break;
+    case TGFX_BF16: launch_recent_inputs_t<TabT, __nv_bfloat16>(a, bad, s); break;
+    default: throw Error(TGFX_EVALIDATION, "unknown output type");
   }
 }
 
@@ -1363,6 +1521,20 @@ int64_t find_bad_query(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, c
   TGFX_CUDA(cudaStreamSynchronize(s));
   dfree(first, s);
   return h == ~0ull ? -1 : static_cast<int64_t>(h);
+}
+
+// fused recent-k sampler + assemble_inputs when the graph takes the line-probe search;
+// returns false when the caller must compose sample + assemble_inputs instead
+bool launch_sample_inputs(const SampleInputsArgs& a, int* bad, cudaStream_t s) {
+  const tgfx_graph* g = a.s.g;
+  if (a.s.strategy != TGFX_RECENT || g->search_exact || g->indptr_bad) return false;
+  if (a.s.q <= 0) return true;
+  switch (a.in.table_type) {
+    case TGFX_F32: launch_recent_inputs_tab<float>(a, bad, s); break;
+    case TGFX_F64: launch_recent_inputs_tab<double>(a, bad, s); break;
+    default: throw Error(TGFX_EVALIDATION, "tables must be f32 or f64");
+  }
+  return true;
 }
 
 void launch_sample(const SampleArgs& a, cudaStream_t s) {

@@ -232,3 +232,24 @@ def assemble_inputs(rows, node_table, edge_table, omega, phi, concat=False, z_dt
         _DT[node_table.dtype], _p(om), _p(ph), d_v, d_e, d_t, 1 if concat else 0, _p(z),
         _DT[z_dtype], _stream(stream), TGFX_TRUSTED if trusted else 0))
     return z
+
+
+def sample_inputs(g, nodes, times, k, strategy, seed, l, self_edge_index, node_table, edge_table,
+                  omega, phi, concat=False, z_dtype=torch.float32, stream_base=0, trusted=False,
+                  stream=None):
+    """forward_concat's sample_batch + build_sequence_batch + assemble_inputs in one call
+    (tgfx_sample_inputs_device): -> (z [q*l, d], valid_len int32 [q])."""
+    q = nodes.numel()
+    d_v, d_e, d_t = node_table.shape[1], edge_table.shape[1], omega.numel()
+    d = d_v + d_e + d_t if concat else d_t
+    z = torch.empty((max(q * l, 1), d), dtype=z_dtype, device="cuda")
+    vl = torch.empty(max(q, 1), dtype=torch.int32, device="cuda")
+    om = omega.to(torch.float64).contiguous()
+    ph = phi.to(torch.float64).contiguous()
+    check(lib().tgfx_sample_inputs_device(
+        g.handle, _p(nodes), _p(times), q, k, _strategy_code(strategy), seed & (2**64 - 1),
+        stream_base & (2**64 - 1), l, self_edge_index, _p(node_table), node_table.shape[0],
+        _p(edge_table), edge_table.shape[0], _DT[node_table.dtype], _p(om), _p(ph), d_v, d_e,
+        d_t, 1 if concat else 0, _p(z), _DT[z_dtype], _p(vl), _stream(stream),
+        TGFX_TRUSTED if trusted else 0))
+    return z[:q * l], vl[:q]

@@ -66,3 +66,56 @@ def test_assemble_inputs_rejects_out_of_table_index():
     w = torch.zeros(4, dtype=torch.float64, device="cuda")
     with pytest.raises(ValidationError, match="outside embedding tables"):
         D.assemble_inputs(rows, t, t, w, w)
+
+
+@pytest.mark.parametrize("strategy,concat,dims,tab,out", [
+    ("recent", False, (32, 32, 32), torch.float64, torch.float64),
+    ("recent", True, (16, 24, 40), torch.float32, torch.float32),
+    ("recent", True, (8, 8, 48), torch.float32, torch.bfloat16),
+    ("random", False, (32, 32, 32), torch.float64, torch.float64),  # composed path
+])
+def test_fused_sample_inputs_equals_composition(oracle_mod, strategy, concat, dims, tab, out):
+    """tgfx_sample_inputs_device (sampler + assemble_inputs in one kernel for recent-k) equals
+    assemble_inputs of the sampler's rows bit for bit (same fp64 deltas, same cos), and the
+    reference's own assemble_inputs within the cos/fma tolerance."""
+    from paper_2409_05477_b200 import device as D
+    E, V, k, l = 120_000, 2500, 10, 11
+    d_v, d_e, d_t = dims
+    ev = D.random_stream(E, V, 23)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 1_000, 9_000, 600, V)
+    rng = np.random.default_rng(6)
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    nt, et = dev(rng.normal(size=(V + 1, d_v))).to(tab), dev(rng.normal(size=(E + 2, d_e))).to(tab)
+    om, ph = dev(rng.normal(size=d_t) * 1e-3), dev(rng.normal(size=d_t))
+    z, vl = D.sample_inputs(g, nodes, times, k, strategy, 3, l, E + 1, nt, et, om, ph, concat,
+                            out)
+    rows = D.sample_assemble(g, nodes, times, k, strategy, 3, l, E + 1, dt64=True)
+    want = D.assemble_inputs({kk: rows[kk] for kk in ("node_index", "edge_index", "valid_len",
+                                                      "time_delta64")},
+                             nt, et, om, ph, concat, out)
+    assert torch.equal(vl, rows["valid_len"])
+    assert torch.equal(z.view(torch.int16 if out == torch.bfloat16 else
+                              (torch.int32 if out == torch.float32 else torch.int64)),
+                       want.view(torch.int16 if out == torch.bfloat16 else
+                                 (torch.int32 if out == torch.float32 else torch.int64)))
+    if tab == torch.float64 and out == torch.float64:
+        h = {kk: vv.cpu().numpy() for kk, vv in rows.items()}
+        ref = oracle_mod.ref_assemble_inputs(h["node_index"], h["edge_index"], h["time_delta64"],
+                                             h["valid_len"], nt.cpu().numpy(), et.cpu().numpy(),
+                                             om.cpu().numpy(), ph.cpu().numpy(), concat)
+        assert np.abs(z.cpu().numpy() - ref).max() <= _tol(h["time_delta64"], om.cpu().numpy(),
+                                                           ph.cpu().numpy())
+
+
+def test_fused_sample_inputs_rejects_small_tables():
+    from paper_2409_05477_b200 import ValidationError, device as D
+    E, V = 20_000, 300
+    ev = D.random_stream(E, V, 2)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 0, 600, 600, V)
+    t = torch.zeros((V + 1, 4), dtype=torch.float64, device="cuda")
+    small_e = torch.zeros((10, 4), dtype=torch.float64, device="cuda")
+    w = torch.zeros(4, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValidationError, match="outside embedding tables"):
+        D.sample_inputs(g, nodes, times, 10, "recent", 0, 11, E + 1, t, small_e, w, w)
