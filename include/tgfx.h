@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TGFX_ABI_VERSION 1
+#define TGFX_ABI_VERSION 2
 
 /* status codes; the C++ shim (include/tgfx/tgformer.hpp) rethrows the reference types */
 #define TGFX_OK 0
@@ -123,16 +123,24 @@ int tgfx_degree_hist_device(const tgfx_event* d_events, int64_t n, int64_t num_n
                             uint64_t* d_deg, void* stream);
 /* warps the partition kernels use for n events (size of the count/offset tables / nparts) */
 int64_t tgfx_partition_warps(int64_t n);
-/* d_bounds[nparts+1]: rank d owns nodes [d_bounds[d], d_bounds[d+1]).  Count pass:
- * d_counts[w*nparts + d] = entries of warp w's event range destined to rank d. */
+/* Rank d owns the global entry positions [P[d], P[d+1]), P[d] = d*m/nparts: the nodes
+ * [d_bounds[d], d_bounds[d+1]) whole, except the at most nparts-1 "split" nodes whose slice
+ * contains a cut (the Zipf hubs), which are divided by entry position.  d_split (int64):
+ * [ns, node[7], gp[7], P[9]] -- gp[i] = indptr[node[i]] + node[i]'s entries in earlier ranks'
+ * chunks, i.e. the global position of this chunk's first entry of node[i].
+ * Count pass: d_counts[w*nparts + d] = entries of warp w's event range that are not split
+ * destined to rank d; d_split_counts[w*7 + i] = warp w's entries of split node i. */
 int tgfx_partition_count_device(const tgfx_event* d_events, int64_t n, int reverse,
                                 const int64_t* d_bounds, int nparts, int64_t nwarps,
-                                int64_t* d_counts, void* stream);
+                                const int64_t* d_split, int64_t* d_counts,
+                                int64_t* d_split_counts, void* stream);
 /* Stable scatter of the entries into per-destination records (32-byte tgfx_event: edge_id,
  * src = node - d_bounds[d] (owner-local id), dst = other endpoint (global id), timestamp) at
- * d_records[d_offsets[w*nparts + d] + rank in warp w], emission order preserved. */
+ * d_records[d_offsets[w*nparts + d] + rank in warp w], emission order preserved;
+ * d_split_occ[w*7 + i] = occurrences of split node i before warp w's range. */
 int tgfx_partition_scatter_device(const tgfx_event* d_events, int64_t n, int reverse,
                                   const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                  const int64_t* d_split, const int64_t* d_split_occ,
                                   const int64_t* d_offsets, tgfx_event* d_records, void* stream);
 /* Build one node range from received records (in global stream order): a reverse = 0 build
  * over num_local_nodes nodes whose neighbour ids stay global (< num_nodes_total). */

@@ -79,8 +79,8 @@ SIGNATURES = {
     "tgfx_build_range_device": [_P, _I64, _I64, _I64, _I64, _P, _U, C.POINTER(_P)],
     "tgfx_degree_hist_device": [_P, _I64, _I64, _I, _P, _P],
     "tgfx_partition_warps": [_I64],
-    "tgfx_partition_count_device": [_P, _I64, _I, _P, _I, _I64, _P, _P],
-    "tgfx_partition_scatter_device": [_P, _I64, _I, _P, _I, _I64, _P, _P, _P],
+    "tgfx_partition_count_device": [_P, _I64, _I, _P, _I, _I64, _P, _P, _P, _P],
+    "tgfx_partition_scatter_device": [_P, _I64, _I, _P, _I, _I64, _P, _P, _P, _P, _P],
     "tgfx_graph_info": [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I)],
     "tgfx_graph_export": [_P, _P, _P, _P, _P],
     "tgfx_graph_device_arrays": [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),

@@ -440,22 +440,24 @@ int64_t tgfx_partition_warps(int64_t n) {
 
 int tgfx_partition_count_device(const tgfx_event* d_events, int64_t n, int reverse,
                                 const int64_t* d_bounds, int nparts, int64_t nwarps,
-                                int64_t* d_counts, void* stream) {
+                                const int64_t* d_split, int64_t* d_counts,
+                                int64_t* d_split_counts, void* stream) {
   return guarded([&] {
     if (nparts < 1 || nparts > 8) throw Error(TGFX_EUNSUPPORTED, "1..8 partitions supported");
-    launch_partition_count(d_events, n, reverse, d_bounds, nparts, nwarps, d_counts,
-                           as_stream(stream));
+    launch_partition_count(d_events, n, reverse, d_bounds, nparts, nwarps, d_split, d_counts,
+                           d_split_counts, as_stream(stream));
   });
 }
 
 int tgfx_partition_scatter_device(const tgfx_event* d_events, int64_t n, int reverse,
                                   const int64_t* d_bounds, int nparts, int64_t nwarps,
+                                  const int64_t* d_split, const int64_t* d_split_occ,
                                   const int64_t* d_offsets, tgfx_event* d_records, void* stream) {
   return guarded([&] {
     if (nparts < 1 || nparts > 8) throw Error(TGFX_EUNSUPPORTED, "1..8 partitions supported");
     if (n > 0)
-      launch_partition_scatter(d_events, n, reverse, d_bounds, nparts, nwarps, d_offsets,
-                               d_records, as_stream(stream));
+      launch_partition_scatter(d_events, n, reverse, d_bounds, nparts, nwarps, d_split,
+                               d_split_occ, d_offsets, d_records, as_stream(stream));
   });
 }
 

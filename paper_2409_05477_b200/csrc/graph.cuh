@@ -235,10 +235,11 @@ void launch_degree_hist(const tgfx_event* ev, int64_t n, int64_t V, int reverse,
                         unsigned long long* deg, cudaStream_t s);
 int64_t partition_warps(int64_t n);
 void launch_partition_count(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
-                            int N, int64_t nw, int64_t* counts, cudaStream_t s);
+                            int N, int64_t nw, const int64_t* split, int64_t* counts,
+                            int64_t* scounts, cudaStream_t s);
 void launch_partition_scatter(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
-                              int N, int64_t nw, const int64_t* offs, tgfx_event* out,
-                              cudaStream_t s);
+                              int N, int64_t nw, const int64_t* split, const int64_t* occ,
+                              const int64_t* offs, tgfx_event* out, cudaStream_t s);
 // 1 if any ts is NaN
 bool any_nan(const double* ts, int64_t m, cudaStream_t s);
 bool indptr_in_range(const int64_t* indptr, int64_t V, int64_t m, cudaStream_t s);

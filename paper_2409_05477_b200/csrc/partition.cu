@@ -4,8 +4,10 @@
 // of BASELINE.json's north star.  Each rank holds a contiguous chunk of the
 // stream; the host (paper_2409_05477_b200/partition.py) drives:
 //   1. k_degree_hist   per-rank node degrees (src, and dst if reverse) -> all-reduce
-//   2. node ranges     split so every rank owns ~m/N entries (host, from the global degrees)
-//   3. k_part_count    per-warp entry counts per destination rank
+//   2. entry ranges    rank d owns global entry positions [d*m/N, (d+1)*m/N): contiguous node
+//                      ranges, plus the (at most N-1) nodes whose slice a cut falls into,
+//                      split by entry position (host, from the global degrees)
+//   3. k_part_count    per-warp entry counts per destination rank (and per split node)
 //   4. k_part_scatter  stable partition of the rank's entries into per-destination buckets of
 //                      32-byte records (eid, node - owner's first node, other endpoint, t): the
 //                      record is a TemporalEvent whose src is the owner-local node id, so the
@@ -48,26 +50,67 @@ __device__ __forceinline__ int owner_of(int64_t u, const int64_t* __restrict__ b
   return d;
 }
 
-// entries of warp w's contiguous event range [w*per, (w+1)*per): counts[w * N + d]
+// Split nodes (the Zipf hubs): rank d owns the GLOBAL entry positions [P[d], P[d+1]) with
+// P[d] = d*m/N, so a node whose slice contains a cut is split between ranks.  Its entry with
+// global position p goes to the largest d with P[d] <= p; p = gp + j for the j-th entry
+// (emission order) of that node in this rank's chunk, gp = indptr[node] + the node's entries
+// in earlier ranks' chunks.  Every other node goes to its node range [bounds[d], bounds[d+1]).
+// Split table d_split (int64): [ns, node[7], gp[7], P[9]].
+struct SplitTab {
+  int ns;
+  int64_t node[7], gp[7], P[9];
+};
+
+__device__ __forceinline__ void load_split(const int64_t* __restrict__ g, SplitTab& t) {
+  t.ns = static_cast<int>(g[0]);
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    t.node[i] = g[1 + i];
+    t.gp[i] = g[8 + i];
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) t.P[i] = g[15 + i];
+}
+
+__device__ __forceinline__ int split_index(const SplitTab& t, int64_t u) {
+  int si = -1;
+#pragma unroll
+  for (int i = 0; i < 7; ++i)
+    if (i < t.ns && t.node[i] == u) si = i;
+  return si;
+}
+
+// entries of warp w's contiguous event range [w*per, (w+1)*per): counts[w * N + d] of the
+// non-split nodes' entries per destination, scounts[w * 7 + i] of split node i's entries
 template <int R>
 __global__ void __launch_bounds__(kPT) k_part_count(const tgfx_event* __restrict__ ev, int64_t n,
                                                     int64_t per, const int64_t* __restrict__ bounds,
-                                                    int N, int64_t nw, int64_t* __restrict__ counts) {
+                                                    int N, int64_t nw,
+                                                    const int64_t* __restrict__ split,
+                                                    int64_t* __restrict__ counts,
+                                                    int64_t* __restrict__ scounts) {
   __shared__ int64_t sb[9];
+  __shared__ SplitTab st;
   if (threadIdx.x <= N) sb[threadIdx.x] = bounds[threadIdx.x];
+  if (threadIdx.x == 0) load_split(split, st);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)kPT + threadIdx.x) >> 5;
   if (w >= nw) return;
   const int64_t e0 = w * per, e1 = min(n, e0 + per);
   int64_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t cs[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int64_t e = e0 + lane; e < e1; e += 32) {
     const Ev x = load_event(ev, e);
 #pragma unroll
     for (int side = 0; side < R; ++side) {
-      const int d = owner_of(side ? x.dst : x.src, sb, N);
+      const int64_t u = side ? x.dst : x.src;
+      const int si = split_index(st, u);
+      const int d = si < 0 ? owner_of(u, sb, N) : -1;
 #pragma unroll
       for (int k = 0; k < 8; ++k) c[k] += (k == d);
+#pragma unroll
+      for (int k = 0; k < 7; ++k) cs[k] += (k == si);
     }
   }
 #pragma unroll
@@ -77,47 +120,89 @@ __global__ void __launch_bounds__(kPT) k_part_count(const tgfx_event* __restrict
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     if (lane == 0 && k < N) counts[w * N + k] = v;
   }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    int64_t v = cs[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) scounts[w * 7 + k] = v;
+  }
 }
 
-// stable scatter: offs[w * N + d] = first output slot of warp w's records for rank d
+// stable scatter: offs[w * N + d] = first output slot of warp w's records for rank d;
+// occ[w * 7 + i] = occurrences of split node i in this chunk before warp w's range
 template <int R>
 __global__ void __launch_bounds__(kPT) k_part_scatter(const tgfx_event* __restrict__ ev, int64_t n,
                                                       int64_t per, const int64_t* __restrict__ bounds,
                                                       int N, int64_t nw,
+                                                      const int64_t* __restrict__ split,
+                                                      const int64_t* __restrict__ occ,
                                                       const int64_t* __restrict__ offs,
                                                       tgfx_event* __restrict__ out) {
   __shared__ int64_t sb[9];
+  __shared__ SplitTab st;
   if (threadIdx.x <= N) sb[threadIdx.x] = bounds[threadIdx.x];
+  if (threadIdx.x == 0) load_split(split, st);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t w = (blockIdx.x * (int64_t)kPT + threadIdx.x) >> 5;
   if (w >= nw) return;
   const int64_t e0 = w * per, e1 = min(n, e0 + per);
-  int64_t cur[8];
+  int64_t cur[8], run[7];
 #pragma unroll
   for (int k = 0; k < 8; ++k) cur[k] = k < N ? offs[w * N + k] : 0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) run[k] = occ[w * 7 + k];
+  const unsigned le = lanemask_lt() | (1u << lane);
   for (int64_t b = e0; b < e1; b += 32) {
     const int64_t e = b + lane;
     const bool ok = e < e1;
     Ev x{0, 0, 0, 0.0};
     if (ok) x = load_event(ev, e);
-    // emission order: src entry of event e, then its dst entry (tcsr.cpp:99-102)
+    // the round's entries in emission order: event-major, src entry then dst entry
+    // (tcsr.cpp:99-102) -- an entry's rank in its bucket counts both sides of earlier events
+    int si[2] = {-1, -1}, d[2] = {-1, -1};
 #pragma unroll
     for (int side = 0; side < R; ++side) {
       const int64_t u = side ? x.dst : x.src;
-      const int64_t other = side ? x.src : x.dst;
-      const int d = ok ? owner_of(u, sb, N) : -1;
-      int64_t pos = 0;
+      si[side] = ok ? split_index(st, u) : -1;
+      d[side] = (ok && si[side] < 0) ? owner_of(u, sb, N) : -1;
+    }
+    // split nodes: the entry's global position gives its owner
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (k >= N) break;
-        const unsigned m = __ballot_sync(kFull, d == k);
-        if (d == k) pos = cur[k] + __popc(m & lanemask_lt());
-        cur[k] += __popc(m);
+    for (int k = 0; k < 7; ++k) {
+      if (k >= st.ns) break;
+      const unsigned ms = __ballot_sync(kFull, si[0] == k);
+      const unsigned md = R == 2 ? __ballot_sync(kFull, si[1] == k) : 0u;
+#pragma unroll
+      for (int side = 0; side < R; ++side) {
+        if (si[side] != k) continue;
+        const int64_t j = run[k] + __popc(ms & (side ? le : lanemask_lt())) +
+                          __popc(md & lanemask_lt());
+        const int64_t p = st.gp[k] + j;
+        int dd = 0;
+        while (dd + 1 < N && st.P[dd + 1] <= p) ++dd;
+        d[side] = dd;
       }
-      if (ok) {
-        longlong2* o = reinterpret_cast<longlong2*>(out + pos);
-        o[0] = make_longlong2(x.eid, u - sb[d]);
+      run[k] += __popc(ms) + __popc(md);
+    }
+    int64_t pos[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= N) break;
+      const unsigned ms = __ballot_sync(kFull, d[0] == k);
+      const unsigned md = R == 2 ? __ballot_sync(kFull, d[1] == k) : 0u;
+      if (d[0] == k) pos[0] = cur[k] + __popc(ms & lanemask_lt()) + __popc(md & lanemask_lt());
+      if (R == 2 && d[1] == k) pos[1] = cur[k] + __popc(ms & le) + __popc(md & lanemask_lt());
+      cur[k] += __popc(ms) + __popc(md);
+    }
+    if (ok) {
+#pragma unroll
+      for (int side = 0; side < R; ++side) {
+        const int64_t u = side ? x.dst : x.src;
+        const int64_t other = side ? x.src : x.dst;
+        longlong2* o = reinterpret_cast<longlong2*>(out + pos[side]);
+        o[0] = make_longlong2(x.eid, u - sb[d[side]]);
         o[1] = make_longlong2(other, __double_as_longlong(x.t));
       }
     }
@@ -189,25 +274,26 @@ int64_t partition_warps(int64_t n) {
 }
 
 void launch_partition_count(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
-                            int N, int64_t nw, int64_t* counts, cudaStream_t s) {
+                            int N, int64_t nw, const int64_t* split, int64_t* counts,
+                            int64_t* scounts, cudaStream_t s) {
   const int64_t per = ceil_div(std::max<int64_t>(n, 1), nw);
   const int grid = static_cast<int>(ceil_div(nw * 32, kPT));
   if (reverse)
-    k_part_count<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, counts);
+    k_part_count<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, split, counts, scounts);
   else
-    k_part_count<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, counts);
+    k_part_count<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, split, counts, scounts);
   after_launch("k_part_count");
 }
 
 void launch_partition_scatter(const tgfx_event* ev, int64_t n, int reverse, const int64_t* bounds,
-                              int N, int64_t nw, const int64_t* offs, tgfx_event* out,
-                              cudaStream_t s) {
+                              int N, int64_t nw, const int64_t* split, const int64_t* occ,
+                              const int64_t* offs, tgfx_event* out, cudaStream_t s) {
   const int64_t per = ceil_div(std::max<int64_t>(n, 1), nw);
   const int grid = static_cast<int>(ceil_div(nw * 32, kPT));
   if (reverse)
-    k_part_scatter<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, offs, out);
+    k_part_scatter<2><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, split, occ, offs, out);
   else
-    k_part_scatter<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, offs, out);
+    k_part_scatter<1><<<grid, kPT, 0, s>>>(ev, n, per, bounds, N, nw, split, occ, offs, out);
   after_launch("k_part_scatter");
 }
 

@@ -4,7 +4,11 @@ One process per GPU.  Rank r holds the r-th contiguous chunk of the event stream
 = stream order).  The build is one exchange step:
 
   1. degrees      tgfx_degree_hist_device on the local chunk, all_reduce(SUM)   [NCCL]
-  2. node ranges  contiguous, balanced by entry count (plan_bounds)
+  2. ownership    rank d owns the global entry positions [d*m/N, (d+1)*m/N) exactly
+                  (plan_entry_ranges): contiguous node ranges, plus the <= N-1 nodes a cut
+                  falls inside (the Zipf hubs), split by entry position -- the positions of a
+                  chunk's entries of such a node come from a tiny all-gather of their per-chunk
+                  counts (the node's entries in earlier chunks precede this chunk's)
   3. partition    tgfx_partition_count/scatter_device: the chunk's entries, stably split into
                   per-owner buckets of 32-byte records (eid, owner-local node, other, t)
   4. exchange     all_to_all of the bucket sizes, then one all_to_all_single of the records
@@ -16,9 +20,9 @@ One process per GPU.  Rank r holds the r-th contiguous chunk of the event stream
                   columns on every rank (what query-sharded sampling needs); global indptr =
                   exclusive scan of the all-reduced degrees.
 
-The owned range of rank r is bit-identical to the slices [indptr[b_r], indptr[b_{r+1}]) of the
-single-GPU build (tests/test_gpu_partition.py), because every node's entries arrive in
-emission order.  The compute is libtgfx's kernels; torch supplies device memory, small
+Rank r's columns are bit-identical to the entries [P_r, P_{r+1}) of the single-GPU build
+(tests/test_gpu_partition.py), because every node's entries arrive in emission order; every
+rank holds m/N entries (+-1) whatever the degree skew.  The compute is libtgfx's kernels; torch supplies device memory, small
 metadata arithmetic (cumsum / searchsorted on V counters) and torch.distributed.
 """
 from __future__ import annotations
@@ -31,20 +35,33 @@ import torch.distributed as dist
 from ._lib import TGFX_TRUSTED, check, lib
 
 
-def plan_bounds(deg: torch.Tensor, world: int) -> torch.Tensor:
-    """Node-range bounds [world+1] (int64): rank d owns nodes [b[d], b[d+1]).  Cuts where the
-    exclusive prefix of entries crosses d*m/world, so every rank owns ~m/world entries (a
-    single node's slice cannot be split: the Zipf hub bounds the balance)."""
+def plan_entry_ranges(deg: torch.Tensor, world: int):
+    """Balanced ownership by GLOBAL entry position: rank d owns [P[d], P[d+1]), P[d] = d*m/world.
+    Returns (P [world+1], bounds [world+1], split nodes [ns], indptr [V+1]): bounds[d] = the
+    node containing position P[d] (the first node rank d touches); a node whose slice has a
+    cut strictly inside is split between ranks (ns <= world-1), every other node belongs to
+    the rank whose node range [bounds[d], bounds[d+1]) holds it."""
     V = deg.numel()
-    csum = torch.cumsum(deg.to(torch.int64), 0)
-    m = int(csum[-1].item()) if V else 0
-    targets = torch.tensor([m * d // world for d in range(1, world)], dtype=torch.int64,
-                           device=deg.device)
-    cuts = torch.searchsorted(csum, targets, right=False) + 1 if V else targets * 0
-    b = torch.cat([torch.zeros(1, dtype=torch.int64, device=deg.device),
-                   torch.clamp(cuts, 0, V),
-                   torch.full((1,), V, dtype=torch.int64, device=deg.device)])
-    return torch.cummax(b, 0).values  # monotone
+    dev = deg.device
+    indptr = torch.zeros(V + 1, dtype=torch.int64, device=dev)
+    if V:
+        torch.cumsum(deg.to(torch.int64), 0, out=indptr[1:])
+    m = int(indptr[-1].item())
+    P = torch.tensor([m * d // world for d in range(world + 1)], dtype=torch.int64, device=dev)
+    # node containing position P[d]: the first node whose slice ends after P[d]
+    c = torch.searchsorted(indptr[1:], P, right=True) if V else P * 0
+    bounds = torch.clamp(c, 0, V)
+    bounds[0] = 0
+    bounds[world] = V
+    inner = bounds[1:world]
+    split = inner[(inner < V) & (indptr[torch.clamp(inner, max=V)] < P[1:world])] if world > 1 \
+        else inner
+    return P, bounds, torch.unique(split), indptr
+
+
+def plan_bounds(deg: torch.Tensor, world: int) -> torch.Tensor:
+    """Node-range bounds of plan_entry_ranges (kept for callers that only need them)."""
+    return plan_entry_ranges(deg, world)[1]
 
 
 def plan_offsets(counts: torch.Tensor, world: int):
@@ -55,6 +72,19 @@ def plan_offsets(counts: torch.Tensor, world: int):
     base = torch.cumsum(totals, 0) - totals
     offs = torch.cumsum(counts, 0) - counts + base[None, :]
     return offs.contiguous(), totals
+
+
+def split_counts_per_rank(scounts, gp, P, world):
+    """Per-warp entries of the split nodes per destination rank: split node i's entries of
+    warp w occupy global positions [gp[i] + occ[w, i], + scounts[w, i]); rank d takes their
+    overlap with [P[d], P[d+1]).  Returns (occ [nw, 7], per_rank [nw, world])."""
+    occ = torch.cumsum(scounts, 0) - scounts
+    start = gp[None, :] + occ
+    end = start + scounts
+    per_rank = torch.stack([(torch.clamp(torch.minimum(end, P[d + 1]) -
+                                         torch.maximum(start, P[d]), min=0)).sum(1)
+                            for d in range(world)], 1)
+    return occ.contiguous(), per_rank
 
 
 def _ptr(t):
@@ -80,22 +110,41 @@ def build_partitioned(ev_local: torch.Tensor, num_nodes: int, reverse: bool, num
     s = _stream(None)
     rev = 1 if reverse else 0
 
-    deg = torch.empty(max(num_nodes, 1), dtype=torch.int64, device=dev)
-    check(L.tgfx_degree_hist_device(_ptr(ev_local), n, num_nodes, rev, _ptr(deg), s))
-    deg = deg[:num_nodes]
+    deg_local = torch.empty(max(num_nodes, 1), dtype=torch.int64, device=dev)
+    check(L.tgfx_degree_hist_device(_ptr(ev_local), n, num_nodes, rev, _ptr(deg_local), s))
+    deg_local = deg_local[:num_nodes]
+    deg = deg_local.clone()
     _all_reduce(deg, exchange_on_host)
-    bounds = plan_bounds(deg, world)
+    P, bounds, split, indptr = plan_entry_ranges(deg, world)
+    ns = int(split.numel())
+    # this chunk's first entry of each split node: indptr + the node's entries in earlier chunks
+    sdeg = torch.zeros(8, dtype=torch.int64, device=dev)
+    if ns:
+        sdeg[:ns] = deg_local[split]
+    gathered = torch.empty(world * 8, dtype=torch.int64, device=dev)
+    _all_gather(gathered, sdeg, exchange_on_host)
+    before = gathered.view(world, 8)[:rank].sum(0)[:7]
+    gp = torch.zeros(7, dtype=torch.int64, device=dev)
+    if ns:
+        gp[:ns] = indptr[split] + before[:ns]
+    tab = torch.zeros(24, dtype=torch.int64, device=dev)
+    tab[0] = ns
+    tab[1:1 + ns] = split
+    tab[8:15] = gp
+    tab[15:15 + world + 1] = P
 
     nw = int(L.tgfx_partition_warps(max(n, 1)))
     counts = torch.zeros((nw, world), dtype=torch.int64, device=dev)
+    scounts = torch.zeros((nw, 7), dtype=torch.int64, device=dev)
     if n:
         check(L.tgfx_partition_count_device(_ptr(ev_local), n, rev, _ptr(bounds), world, nw,
-                                            _ptr(counts), s))
-    offs, send = plan_offsets(counts, world)
+                                            _ptr(tab), _ptr(counts), _ptr(scounts), s))
+    occ, per_rank = split_counts_per_rank(scounts, gp, P, world)
+    offs, send = plan_offsets(counts + per_rank, world)
     sent = int(send.sum().item())
     records = torch.empty(max(sent, 1) * 32, dtype=torch.uint8, device=dev)
     check(L.tgfx_partition_scatter_device(_ptr(ev_local), n, rev, _ptr(bounds), world, nw,
-                                          _ptr(offs), _ptr(records), s))
+                                          _ptr(tab), _ptr(occ), _ptr(offs), _ptr(records), s))
 
     recv_counts = torch.empty_like(send)
     _all_to_all(recv_counts, send, None, None, exchange_on_host)
@@ -104,26 +153,30 @@ def build_partitioned(ev_local: torch.Tensor, num_nodes: int, reverse: bool, num
                 exchange_on_host)
     n_recv = int(recv_counts.sum().item())
 
-    lo, hi = int(bounds[rank].item()), int(bounds[rank + 1].item())
+    Ph = P.tolist()
+    lo = int(bounds[rank].item())
+    # last node this rank touches: the one holding its last position P[rank+1] - 1
+    hi = int(torch.searchsorted(indptr[1:], P[rank + 1] - 1, right=True).item()) + 1 \
+        if Ph[rank + 1] > Ph[rank] else lo
     h = C.c_void_p()
-    check(L.tgfx_build_range_device(_ptr(recv), n_recv, hi - lo, num_nodes, num_edges, s, 0,
-                                    C.byref(h)))
+    check(L.tgfx_build_range_device(_ptr(recv), n_recv, max(hi - lo, 0), num_nodes, num_edges, s,
+                                    0, C.byref(h)))
     local = TCsr(h.value)
-    out = dict(local=local, bounds=bounds, degrees=deg, range=(lo, hi), sent_records=sent)
+    out = dict(local=local, bounds=bounds, degrees=deg, range=(lo, hi), positions=P,
+               split_nodes=split, sent_records=sent, received_records=n_recv)
     if replicate:
-        out["full"] = _replicate(local, deg, bounds, num_nodes, num_edges, reverse,
-                                 exchange_on_host)
+        out["full"] = _replicate(local, deg, P, num_nodes, num_edges, reverse, exchange_on_host)
     return out
 
 
 def replicate(part: dict, num_nodes: int, num_edges: int, reverse: bool,
               exchange_on_host: bool = False):
     """The full T-CSR on every rank from a build_partitioned(replicate=False) result."""
-    return _replicate(part["local"], part["degrees"], part["bounds"], num_nodes, num_edges,
+    return _replicate(part["local"], part["degrees"], part["positions"], num_nodes, num_edges,
                       reverse, exchange_on_host)
 
 
-def _replicate(local, deg, bounds, num_nodes, num_edges, reverse, on_host):
+def _replicate(local, deg, P, num_nodes, num_edges, reverse, on_host):
     """Every rank's owned columns broadcast straight into their slice of the full columns
     (one broadcast per owner and column: no padding to the largest part, no concatenation
     copy), then imported as one device T-CSR per rank (node directory, bucket tables and gather
@@ -136,7 +189,7 @@ def _replicate(local, deg, bounds, num_nodes, num_edges, reverse, on_host):
     indptr = torch.zeros(num_nodes + 1, dtype=torch.int64, device=dev)
     torch.cumsum(deg, 0, out=indptr[1:])
     m = int(indptr[-1].item())
-    starts = indptr[bounds].tolist()  # entry offset of each owner's range, [world + 1]
+    starts = P.tolist()  # each owner's global entry range [P[d], P[d+1])
     _, nb, ed, ts = graph_tensors(local)
     cols = [torch.empty(max(m, 1), dtype=torch.int64, device=dev) for _ in range(3)]
     for col, mine in zip(cols, (nb, ed, ts.view(torch.int64))):
@@ -169,6 +222,15 @@ def _all_to_all(out, inp, out_splits, in_splits, on_host):
         out.copy_(o)
     else:
         dist.all_to_all_single(out, inp, out_splits, in_splits)
+
+
+def _all_gather(out, inp, on_host):
+    if on_host:
+        parts = [torch.empty(inp.shape, dtype=inp.dtype) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, inp.cpu())
+        out.copy_(torch.cat(parts))
+    else:
+        dist.all_gather_into_tensor(out, inp)
 
 
 def _broadcast(t, src, on_host):

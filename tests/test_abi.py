@@ -61,7 +61,7 @@ def test_no_oracle_in_product(built):
 
 def test_abi_version_and_error_plumbing(built):
     L = built.lib()
-    assert L.tgfx_abi_version() == 1
+    assert L.tgfx_abi_version() == 2
     # num_threads validation happens before any device work (tcsr.cpp:108)
     import ctypes as C
     h = C.c_void_p()

@@ -166,7 +166,8 @@ def _mag_worker(rank, world, port, out_dir):
         ip, nb, ed, ts = D.graph_tensors(res["local"])
         fip, fnb, fed, fts = D.graph_tensors(res["full"])
         np.savez(os.path.join(out_dir, f"mag_r{rank}.npz"), bounds=res["bounds"].cpu().numpy(),
-                 ip=ip.cpu().numpy(), nb=nb.cpu().numpy(), ed=ed.cpu().numpy(),
+                 P=res["positions"].cpu().numpy(), rng=np.array(res["range"]),
+                 nrecv=res["received_records"], ip=ip.cpu().numpy(), nb=nb.cpu().numpy(), ed=ed.cpu().numpy(),
                  ts=ts.cpu().numpy(), fip=fip.cpu().numpy(), fnb=fnb.cpu().numpy(),
                  fed=fed.cpu().numpy(), fts=fts.cpu().numpy())
         del res
@@ -185,10 +186,12 @@ def test_mag_sixteenth_partitioned_two_ranks(tmp_path, oracle_mod):
     del ev
     for r in range(world):
         got = np.load(os.path.join(tmp_path, f"mag_r{r}.npz"))
-        b = got["bounds"]
-        lo, hi = int(b[r]), int(b[r + 1])
-        a0, a1 = want["indptr"][lo], want["indptr"][hi]
-        assert np.array_equal(got["ip"], want["indptr"][lo:hi + 1] - a0), r
+        lo, hi = (int(x) for x in got["rng"])
+        a0, a1 = int(got["P"][r]), int(got["P"][r + 1])
+        m = int(want["indptr"][-1])
+        assert a0 == m * r // world and a1 == m * (r + 1) // world  # balanced by entries
+        assert int(got["nrecv"]) == a1 - a0
+        assert np.array_equal(got["ip"], np.clip(want["indptr"][lo:hi + 1], a0, a1) - a0), r
         for k, w in (("nb", "nbr"), ("ed", "eid"), ("ts", "ts")):
             assert np.array_equal(got[k], want[w][a0:a1]), (r, k)
         assert np.array_equal(got["fip"], want["indptr"]), r

@@ -12,7 +12,10 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-CASES = [(400_000, 5000, True, 5), (200_000, 300, False, 6), (150_000, 16682, True, 42)]
+# the third and fourth shapes have a Zipf hub holding ~20 % of the entries; with 3 ranks the
+# cuts at 1/3 and 2/3 fall inside hub slices of the smaller shapes, so nodes are split
+CASES = [(400_000, 5000, True, 5), (200_000, 300, False, 6), (150_000, 16682, True, 42),
+         (300_000, 40, True, 9)]
 
 
 def _port():
@@ -36,7 +39,9 @@ def _worker(rank, world, port, out_dir):
             ip, nb, ed, ts = D.graph_tensors(res["local"])
             fip, fnb, fed, fts = D.graph_tensors(res["full"])
             np.savez(os.path.join(out_dir, f"r{rank}_c{ci}.npz"),
-                     bounds=res["bounds"].cpu().numpy(), ip=ip.cpu().numpy(),
+                     bounds=res["bounds"].cpu().numpy(), P=res["positions"].cpu().numpy(),
+                     rng=np.array(res["range"]), nsplit=res["split_nodes"].numel(),
+                     nrecv=res["received_records"], ip=ip.cpu().numpy(),
                      nb=nb.cpu().numpy(), ed=ed.cpu().numpy(), ts=ts.cpu().numpy(),
                      fip=fip.cpu().numpy(), fnb=fnb.cpu().numpy(), fed=fed.cpu().numpy(),
                      fts=fts.cpu().numpy())
@@ -47,21 +52,27 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def test_partitioned_build_matches_single_gpu(tmp_path, oracle_mod):
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_build_matches_single_gpu(tmp_path, oracle_mod, world):
     from paper_2409_05477_b200 import device as D
-    world = 2
     mp.spawn(_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    nsplit = 0
     for ci, (E, V, rev, seed) in enumerate(CASES):
         ev = D.random_stream(E, V, seed)
         want = oracle_mod.build(ev.cpu().numpy().view(oracle_mod.EVENT_DTYPE), V, rev)
         for r in range(world):
             got = np.load(os.path.join(tmp_path, f"r{r}_c{ci}.npz"))
-            b = got["bounds"]
-            lo, hi = int(b[r]), int(b[r + 1])
-            a0, a1 = want["indptr"][lo], want["indptr"][hi]
-            assert np.array_equal(got["ip"], want["indptr"][lo:hi + 1] - a0), (ci, r)
+            lo, hi = (int(x) for x in got["rng"])
+            a0, a1 = int(got["P"][r]), int(got["P"][r + 1])
+            m = int(want["indptr"][-1])
+            assert a0 == m * r // world and a1 == m * (r + 1) // world  # balanced by entries
+            assert int(got["nrecv"]) == a1 - a0
+            assert np.array_equal(got["ip"], np.clip(want["indptr"][lo:hi + 1], a0, a1) - a0), \
+                (ci, r)
             for k, w in (("nb", "nbr"), ("ed", "eid"), ("ts", "ts")):
                 assert np.array_equal(got[k], want[w][a0:a1]), (ci, r, k)
+            nsplit += int(got["nsplit"])
             assert np.array_equal(got["fip"], want["indptr"]), (ci, r)
             for k, w in (("fnb", "nbr"), ("fed", "eid"), ("fts", "ts")):
                 assert np.array_equal(got[k], want[w]), (ci, r, k)
+    assert nsplit > 0  # some cut fell inside a slice: the split-node path ran
