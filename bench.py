@@ -423,8 +423,13 @@ def run_ours(args, cfg):
     # N > 1: the node-range-partitioned build (degree all-reduce, one all-to-all
     # of 32-byte records, local stable build of the owned range), timed on its own, and the
     # all-gather that replicates it for query-sharded sampling
-    build_part = measure_partitioned(ev_part if part else ev, E, V, ws, rank, share, red, stream,
-                                     owned_chunk=part) if ws > 1 else None
+    build_part = None
+    if ws > 1:  # an auxiliary measurement: a failure here is reported, not fatal to the line
+        try:
+            build_part = measure_partitioned(ev_part if part else ev, E, V, ws, rank, share, red,
+                                             stream, owned_chunk=part)
+        except Exception as e:  # noqa: BLE001
+            build_part = {"error": f"{type(e).__name__}: {e}"[:300]}
     total_ms = start.elapsed_time(end)
     build_ms = [r["b0"].elapsed_time(r["b1"]) for r in ev_rec]
     samp_launch_ms = [a.elapsed_time(b) for r in ev_rec for (a, b) in r["c"]]
