@@ -17,12 +17,14 @@ by barrier + synchronize, max over ranks.  Inputs (6.1 GB events, 9.2 GB queries
 `cpu_baseline` / --impl reference time the reference's own CPU code (oracle/_ref, compiled
 from /root/reference) on a bounded prefix sample of the same workload.
 
-Multi-GPU (torchrun, one process per GPU): the T-CSR is replicated (each rank rebuilds it from
-its own copy of the stream) and sampling shards by query (paper_2409_05477_b200/shard.py).
-Default plan "weak": every rank is a data-parallel worker running a full pass with its own
-negatives (neg_seed + rank), per-rank work fixed, value = N x events / max-over-ranks step
-time.  --plan strong: one pass, whole-batch query shards with stream_base (rows identical
-to 1 GPU).  No collective touches the data path; only the timing max over ranks.
+Multi-GPU (torchrun, one process per GPU): default plan "strong": one pass, whole-batch query
+shards (each rank generates only its shard's queries; stream_base keeps rows identical to 1 GPU),
+every rank rebuilding its T-CSR replica from the stream; value = E / max-over-ranks step time.
+The line adds `build_partitioned`: the node-range / entry-position partitioned build (one
+all-to-all) and its replication, timed separately.  --config M / M16 make that partitioned build
++ replication the step's build.  --plan weak: every rank a full data-parallel pass with its own
+negatives (neg_seed + rank).  No collective touches the sampling path; only the timing max over
+ranks and the partitioned build's exchange.
 """
 import argparse
 import ctypes as C
@@ -656,8 +658,9 @@ def run_e2e(args, cfg, dev_inputs, chunks, ws, rank, weak, red="cuda", probe=Non
     lo, hi = chunks[0][0], chunks[-1][1]
     h_nodes = torch.empty(hi - lo, dtype=torch.int64, pin_memory=True)
     h_times = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True)
-    h_nodes.copy_(nodes[lo:hi])
-    h_times.copy_(times[lo:hi])
+    # the resident query arrays hold this rank's shard [q_lo, q_hi) = [lo, hi)
+    h_nodes.copy_(nodes[:hi - lo])
+    h_times.copy_(times[:hi - lo])
     del ev, nodes, times
     dev_inputs.clear()  # inputs now live in pinned host memory only
     torch.cuda.synchronize()
