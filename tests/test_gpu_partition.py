@@ -12,10 +12,10 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-# the third and fourth shapes have a Zipf hub holding ~20 % of the entries; with 3 ranks the
-# cuts at 1/3 and 2/3 fall inside hub slices of the smaller shapes, so nodes are split
+# Zipf hubs: with 3 or 4 ranks the cuts fall inside hub slices, so nodes are split; in the
+# last shape (6 nodes, reverse = 0) one hub holds ~40 % of the entries and spans two cuts
 CASES = [(400_000, 5000, True, 5), (200_000, 300, False, 6), (150_000, 16682, True, 42),
-         (300_000, 40, True, 9)]
+         (300_000, 40, True, 9), (100_000, 6, False, 3)]
 
 
 def _port():
@@ -52,7 +52,7 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_partitioned_build_matches_single_gpu(tmp_path, oracle_mod, world):
     from paper_2409_05477_b200 import device as D
     mp.spawn(_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
