@@ -1174,7 +1174,7 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       const int64_t i = b0 + k;
-      if (i > i1) break;
+      if (i > i1) continue;  // (no break: it keeps the loop, and x[], from being unrolled)
       const unsigned long long tb = static_cast<unsigned long long>(__double_as_longlong(x[k]));
       __stcs(rec + i, make_uint4(static_cast<uint32_t>(nbr[i]), static_cast<uint32_t>(eid[i]),
                                  static_cast<uint32_t>(tb), static_cast<uint32_t>(tb >> 32)));
@@ -1228,7 +1228,7 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const int64_t i = b0 + k;
-    if (i > i1) break;
+    if (i > i1) continue;
     if (!hub) {
       const int32_t mk = mark[tid * P + k];
       if (mk >= 0 && mk != u) {  // a new slice starts here
@@ -1241,7 +1241,10 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
     const uint32_t r = static_cast<uint32_t>(i - d.start);
     const int jr = static_cast<int>(bucket_of(x[k], d.t_first, d.scale, d.nb));
     uint32_t* bkt = const_cast<uint32_t*>(d.bkt);
-    for (int j = jprev + 1; j <= jr; ++j) bkt[j] = r;
+    // usually at most one bucket starts at an entry: one predicated store, the loop only for
+    // the rest of a run of empty buckets
+    if (jr > jprev) bkt[jprev + 1] = r;
+    for (int j = jprev + 2; j <= jr; ++j) bkt[j] = r;
     jprev = jr;
     if (i == d.end - 1) bkt[d.nb] = r + 1;
   }
