@@ -820,30 +820,46 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
         rank[k] = b + __popc(peers[k] & lanemask_lt());
       }
       __syncthreads();
-      {  // exclusive scan of the kW x 256 counters in (digit, warp) order, 8 per thread
-        uint32_t v[8], s = 0;
+      {  // exclusive scan of the kW x 256 counters in (digit, warp) order: 64 threads, each
+         // 4 digits x kW warps read as kW 8-byte loads (a quarter of the shared-memory
+         // instructions of one 2-byte load per counter)
+        static_assert(kW == 8, "scan layout");
+        constexpr int kDT = 4;           // digits per thread
+        constexpr int kNT = 256 / kDT;   // active threads (2 warps)
+        uint2 v[kW];
+        uint32_t tot = 0;
+        if (tid < kNT) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = tid * 8 + c;
-          v[c] = wcnt[(i % kW) * 256 + i / kW];
-          s += v[c];
+          for (int w = 0; w < kW; ++w) {
+            v[w] = *reinterpret_cast<const uint2*>(wcnt + w * 256 + kDT * tid);
+            tot += (v[w].x & 0xffffu) + (v[w].x >> 16) + (v[w].y & 0xffffu) + (v[w].y >> 16);
+          }
         }
-        uint32_t x = s;
+        uint32_t x = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(kFull, x, o);
           if (lane >= o) x += y;
         }
-        if (lane == 31) scr[warp] = static_cast<int>(x);
+        if (lane == 31 && warp == 0) scr[0] = static_cast<int>(x);
         __syncthreads();
-        const uint32_t before = __reduce_add_sync(
-            kFull, lane < warp ? static_cast<uint32_t>(scr[lane]) : 0u);
-        uint32_t run = before + x - s;
+        if (tid < kNT) {
+          uint32_t run = (warp == 1 ? static_cast<uint32_t>(scr[0]) : 0u) + x - tot;
+          uint32_t o[kW][kDT];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = tid * 8 + c;
-          wcnt[(i % kW) * 256 + i / kW] = static_cast<uint16_t>(run);
-          run += v[c];
+          for (int dd = 0; dd < kDT; ++dd) {
+#pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const uint32_t word = dd < 2 ? v[w].x : v[w].y;
+              const uint32_t c = (word >> (16 * (dd & 1))) & 0xffffu;
+              o[w][dd] = run;
+              run += c;
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < kW; ++w)
+            *reinterpret_cast<uint2*>(wcnt + w * 256 + kDT * tid) =
+                make_uint2(o[w][0] | (o[w][1] << 16), o[w][2] | (o[w][3] << 16));
         }
       }
       __syncthreads();
