@@ -709,6 +709,36 @@ __device__ __forceinline__ void hot_write_entry(const tgfx_event* sev, int j, ui
   }
 }
 
+// as hot_write_entry, with the entry's node and cold flag already known
+template <int R>
+__device__ __forceinline__ void write_entry_known(const tgfx_event* sev, int j, uint32_t pos,
+                                                  uint32_t u, bool cold,
+                                                  ulonglong2* __restrict__ cold_img,
+                                                  double* __restrict__ ts_out,
+                                                  uint4* __restrict__ rec_out,
+                                                  int64_t* __restrict__ nbr_out,
+                                                  int64_t* __restrict__ eid_out) {
+  const longlong2* e = reinterpret_cast<const longlong2*>(sev + (R == 2 ? (j >> 1) : j));
+  const longlong2 a = e[0], b = e[1];  // (eid, src), (dst, t bits)
+  const bool side = R == 2 && (j & 1);
+  const long long other = side ? a.y : b.x;
+  if (cold) {
+    ulonglong2* rec = cold_img + 2 * static_cast<int64_t>(pos);
+    rec[0] = make_ulonglong2(static_cast<unsigned long long>(other), static_cast<unsigned long long>(a.x));
+    rec[1] = make_ulonglong2(static_cast<unsigned long long>(b.y), static_cast<unsigned long long>(u));
+  } else {
+    ts_out[pos] = __longlong_as_double(b.y);
+    if (rec_out) {
+      rec_out[pos] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(a.x),
+                                static_cast<uint32_t>(b.y),
+                                static_cast<uint32_t>(static_cast<unsigned long long>(b.y) >> 32));
+    } else {
+      nbr_out[pos] = other;
+      eid_out[pos] = a.x;
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ uint32_t hot_node_of(const tgfx_event* sev, int j) {
   const int64_t* e = reinterpret_cast<const int64_t*>(sev + (R == 2 ? (j >> 1) : j));
@@ -742,7 +772,7 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
     const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev, int passes,
     uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits,
     ulonglong2* __restrict__ cold_img, double* __restrict__ ts_out, uint4* __restrict__ rec_out,
-    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out) {
+    int64_t* __restrict__ nbr_out, int64_t* __restrict__ eid_out, int cflag) {
   constexpr int NE = TE * R;
   constexpr int KPT = NE / kBT;
   constexpr int kW = kBT / 32;
@@ -883,7 +913,12 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
         const int s = warp * 32 * KPT + k * 32 + lane;
         const uint32_t u = key[k] >> 16;
         const bool head = s == 0 || (src_keys[s - 1] >> 16) != u;
-        if (head && u < static_cast<uint32_t>(V)) dst_keys[s] = SC ? scur[u] : __ldcg(crow + u);
+        // run heads fetch the cursor -- with the node's cold flag in bit 31 while positions
+        // fit 31 bits (cflag), so the run's entries need no cold-bit lookup of their own
+        if (head && u < static_cast<uint32_t>(V)) {
+          const uint32_t c = SC ? scur[u] : __ldcg(crow + u);
+          dst_keys[s] = cflag ? c | (((cbits[u >> 5] >> (u & 31)) & 1u) << 31) : c;
+        }
         int x = head ? s : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -906,7 +941,8 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
       const int s = warp * 32 * KPT + k * 32 + lane;
       const uint32_t u = key[k] >> 16;
       if (u >= static_cast<uint32_t>(V)) continue;
-      const uint32_t pos = dst_keys[hp[k]] + static_cast<uint32_t>(s - hp[k]);
+      const uint32_t h = dst_keys[hp[k]];
+      const uint32_t pos = (cflag ? h & 0x7fffffffu : h) + static_cast<uint32_t>(s - hp[k]);
       const bool tail = s == NE - 1 || (src_keys[s + 1] >> 16) != u;
       if (tail) {
         if (SC)
@@ -914,8 +950,12 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
         else
           __stcg(crow + u, pos + 1);
       }
-      hot_write_entry<R>(sev, static_cast<int>(key[k] & 0xffffu), pos, cbits, cold_img, ts_out,
-                         rec_out, nbr_out, eid_out);
+      if (cflag)
+        write_entry_known<R>(sev, static_cast<int>(key[k] & 0xffffu), pos, u, (h >> 31) != 0,
+                             cold_img, ts_out, rec_out, nbr_out, eid_out);
+      else
+        hot_write_entry<R>(sev, static_cast<int>(key[k] & 0xffffu), pos, cbits, cold_img, ts_out,
+                           rec_out, nbr_out, eid_out);
     }
     __syncthreads();  // stage consumed; cursor stores ordered before the next tile's loads
     if (tid == 0 && it + S < ntiles) {
@@ -1626,14 +1666,17 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
     int bits = 1;
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
     const int passes = (bits + 7) / 8;
+    const int cflag = std::max(g->m, ncold) < (int64_t(1) << 31) ? 1 : 0;
 #define X(ID, TE, S, SC)                                                                       \
     if (bigv == ID) {                                                                          \
       if (g->reverse)                                                                          \
         k_scatter_big<2, TE, S, SC><<<C, kBT, big_smem<2, TE, S, SC>(V), s>>>(                 \
-            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid);  \
+            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid,   \
+            cflag);                                                                             \
       else                                                                                     \
         k_scatter_big<1, TE, S, SC><<<C, kBT, big_smem<1, TE, S, SC>(V), s>>>(                 \
-            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid);  \
+            d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid,   \
+            cflag);                                                                             \
     }
     TGFX_BIG_SHAPES(X)
 #undef X
