@@ -119,3 +119,30 @@ def test_fused_sample_inputs_rejects_small_tables():
     w = torch.zeros(4, dtype=torch.float64, device="cuda")
     with pytest.raises(ValidationError, match="outside embedding tables"):
         D.sample_inputs(g, nodes, times, 10, "recent", 0, 11, E + 1, t, small_e, w, w)
+
+
+def test_fused_sample_inputs_edge_shapes():
+    """l = 2 (only the self-loop token and one neighbour), k larger than l - 1, an empty query
+    list, and queries before any event (empty prefixes: self token only)."""
+    from paper_2409_05477_b200 import device as D
+    E, V = 30_000, 400
+    ev = D.random_stream(E, V, 12)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 0, 1200, 600, V)
+    times = times.clone()
+    times[:50] = -1.0  # before every event
+    nt = torch.randn((V + 1, 16), device="cuda", dtype=torch.float64)
+    et = torch.randn((E + 2, 16), device="cuda", dtype=torch.float64)
+    om = torch.randn(16, device="cuda", dtype=torch.float64) * 1e-3
+    ph = torch.randn(16, device="cuda", dtype=torch.float64)
+    for k, l in ((10, 2), (3, 11), (30, 5)):
+        z, vl = D.sample_inputs(g, nodes, times, k, "recent", 0, l, E + 1, nt, et, om, ph, False,
+                                torch.float64)
+        rows = D.sample_assemble(g, nodes, times, k, "recent", 0, l, E + 1, dt64=True)
+        want = D.assemble_inputs({kk: rows[kk] for kk in ("node_index", "edge_index",
+                                                          "valid_len", "time_delta64")},
+                                 nt, et, om, ph, False, torch.float64)
+        assert torch.equal(z, want) and torch.equal(vl, rows["valid_len"]), (k, l)
+        assert int(vl[:50].max()) == 1  # self token only
+    z0, v0 = D.sample_inputs(g, nodes[:0], times[:0], 10, "recent", 0, 11, E + 1, nt, et, om, ph)
+    assert z0.numel() == 0 and v0.numel() == 0

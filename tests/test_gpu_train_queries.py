@@ -18,7 +18,7 @@ def O():
 
 
 @pytest.mark.parametrize("B,npp,workers", [(200, 1, 1), (333, 3, 1), (250, 2, 3), (64, 1, 8),
-                                           (1000, 5, 4)])
+                                           (1000, 5, 4), (5, 2, 8), (7, 1, 3)])
 def test_train_queries_match_reference_make_batches(O, B, npp, workers):
     import torch
     from paper_2409_05477_b200 import device as D
