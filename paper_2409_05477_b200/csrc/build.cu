@@ -1054,9 +1054,10 @@ __device__ __forceinline__ int64_t bucket_count(int64_t n, double t_first, doubl
 constexpr int kFillPer = 8;
 constexpr int64_t kFillTile = 256 * kFillPer;
 
+// directory records; a slice's bucket table at bkt + start / R + 2u (see DirC)
 __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __restrict__ ts,
                            int64_t V, int64_t R, NodeDir* __restrict__ dir,
-                           uint32_t* __restrict__ cnt) {
+                           DirC* __restrict__ dirc, uint32_t* __restrict__ bkt) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= V) return;
   const int64_t a = indptr[u], b = indptr[u + 1];
@@ -1067,10 +1068,17 @@ __global__ void k_node_dir(const int64_t* __restrict__ indptr, const double* __r
   d.t_last = b > a ? ts[b - 1] : 0.0;
   d.bkt = nullptr;
   d.scale = 0.0;
-  d.nb = cnt ? bucket_count(b - a, d.t_first, d.t_last, R, &d.scale) : 0;
+  d.nb = bkt ? bucket_count(b - a, d.t_first, d.t_last, R, &d.scale) : 0;
   d.width = d.nb ? (d.t_last - d.t_first) / static_cast<double>(d.nb) : 0.0;
+  if (d.nb) d.bkt = bkt + a / R + 2 * u;
   dir[u] = d;
-  if (cnt) cnt[u] = d.nb ? static_cast<uint32_t>(d.nb + 1) : 0u;
+  DirC c;
+  c.start = a;
+  c.n = static_cast<uint32_t>(b - a < 0xffffffffLL ? b - a : 0xffffffffLL);
+  c.nb = static_cast<uint32_t>(d.nb);
+  c.t_first = d.t_first;
+  c.st = d.nb ? d.scale : d.t_last;
+  dirc[u] = c;
 }
 
 // the node holding the first entry of each k_bucket_fill tile: last u with indptr[u] <= t * tile
@@ -1090,14 +1098,6 @@ __global__ void k_tile_node(const int64_t* __restrict__ indptr, int64_t V, int64
     }
   }
   tile_node[t] = static_cast<int32_t>(lo - 1);
-}
-
-// pass 2: bucket table offsets (exclusive scan of the sizes) -> pointers
-__global__ void k_node_dir_bkt(const int64_t* __restrict__ off, int64_t V, uint32_t* bkt,
-                               NodeDir* __restrict__ dir) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= V) return;
-  if (dir[u].nb) dir[u].bkt = bkt + off[u];
 }
 
 // pass 3: one thread per slice entry writes the table entries of the buckets that start at
@@ -1858,6 +1858,7 @@ void graph_alloc(tgfx_graph* g, cudaStream_t s) {
   g->ts = static_cast<double*>(dmalloc(sizeof(double) * (mm + kTsPad), s));
   TGFX_CUDA(cudaMemsetAsync(g->ts + mm, 0, sizeof(double) * kTsPad, s));
   g->dir = static_cast<NodeDir*>(dmalloc(sizeof(NodeDir) * std::max<int64_t>(g->V, 1), s));
+  g->dirc = static_cast<DirC*>(dmalloc(sizeof(DirC) * std::max<int64_t>(g->V, 1), s));
   g->dflags = static_cast<BuildFlags*>(dmalloc(sizeof(BuildFlags), s));
   g->hflags = flags_alloc();
 }
@@ -1870,6 +1871,7 @@ void graph_release(tgfx_graph* g) {
   if (g->ts) dfree(g->ts, s);
   if (g->dflags) dfree(g->dflags, s);
   if (g->dir) dfree(g->dir, s);
+  if (g->dirc) dfree(g->dirc, s);
   if (g->bkt) dfree(g->bkt, s);
   if (g->rec) dfree(g->rec, s);
   if (g->ws) dfree(g->ws, s);
@@ -1879,6 +1881,7 @@ void graph_release(tgfx_graph* g) {
   g->indptr = g->nbr = g->eid = nullptr;
   g->ts = nullptr;
   g->dir = nullptr;
+  g->dirc = nullptr;
   g->bkt = nullptr;
   g->bkt_cap = 0;
   g->rec = nullptr;
@@ -1996,8 +1999,10 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
   // gather records from the columns, unless the build's scatter already wrote them
   uint4* rec = g->cols_valid ? ensure_rec(g, s) : nullptr;
   const int64_t tiles = ceil_div(g->m, kFillTile);
-  if (R <= 0) {
-    k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, nullptr);
+  // the compact directory holds slice lengths as u32
+  g->bkt_r = R > 0 && g->m < (int64_t(1) << 32) ? R : 0;
+  if (g->bkt_r <= 0) {
+    k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, 0, g->dir, g->dirc, nullptr);
     after_launch("k_node_dir");
     if (rec) {
       k_bucket_fill<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
@@ -2007,26 +2012,21 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
     }
     return;
   }
-  // table size <= sum over slices of (n / R + 2) = m / R + 2V: allocated without a sync
-  const int64_t cap = g->m / R + 2 * g->V + 1;
+  // node u's table at start_u / R + 2u, nb_u + 1 <= n_u / R + 2 entries: size m / R + 2V + 2
+  const int64_t cap = g->m / R + 2 * g->V + 2;
   if (g->bkt_cap < cap) {
     if (g->bkt) dfree(g->bkt, s);
     g->bkt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * cap, s));
     g->bkt_cap = cap;
   }
-  uint32_t* cnt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->V, s));
-  int64_t* off = static_cast<int64_t*>(dmalloc(sizeof(int64_t) * (g->V + 1), s));
   int32_t* tile_node = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * std::max<int64_t>(tiles, 1), s));
-  k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, cnt);
+  k_node_dir<<<vb, 256, 0, s>>>(g->indptr, g->ts, g->V, R, g->dir, g->dirc, g->bkt);
   after_launch("k_node_dir");
   if (tiles > 0) {
     k_tile_node<<<static_cast<int>(ceil_div(tiles, 256)), 256, 0, s>>>(g->indptr, g->V, tiles,
                                                                         tile_node);
     after_launch("k_tile_node");
   }
-  scan_u32_to_i64(cnt, g->V, off, s);
-  k_node_dir_bkt<<<vb, 256, 0, s>>>(off, g->V, g->bkt, g->dir);
-  after_launch("k_node_dir_bkt");
   if (g->m > 0) {
     if (bucket_fill_v() == 8)
       k_bucket_fill8<<<static_cast<int>(tiles), 256, 0, s>>>(g->indptr, g->nbr, g->eid, g->ts,
@@ -2039,8 +2039,6 @@ void build_node_dir(tgfx_graph* g, cudaStream_t s) {
     after_launch("k_bucket_fill");
   }
   dfree(tile_node, s);
-  dfree(cnt, s);
-  dfree(off, s);
 }
 
 std::string validate_graph(const tgfx_graph* g, cudaStream_t s) {

@@ -26,6 +26,17 @@ struct __align__(32) NodeDir {
   double width;  // (t_last - t_first) / nb: bucket edges for the interpolation hints
 };
 
+// The recent-k sampler's compact copy of a NodeDir: 32 B per node, ONE 256-bit load.  A
+// slice's bucket table sits at bkt_base + start / R + 2u (tables never overlap: nb + 1 <=
+// n / R + 2), so no pointer is stored; st = scale when nb > 0 (t_last is then not needed: the
+// last bucket's table entry brackets a query past the slice), else t_last.
+struct __align__(32) DirC {
+  int64_t start;
+  uint32_t n, nb;
+  double t_first;
+  double st;
+};
+
 // bucket of time t in a slice with a bucket table: floor((t - t_first) * scale) clamped to
 // nb - 1 (nb < 2^32).  Monotone non-decreasing in t; the builder and the sampler evaluate this
 // same expression (explicitly rounded, never contracted), which is all exactness needs.
@@ -61,6 +72,8 @@ struct tgfx_graph {
   // node directory, 32 B per node: {slice start, slice end, ts[start], ts[end-1]} -- one
   // record gives the sampler both the slice bounds and the interpolation bracket
   NodeDir* dir = nullptr;
+  DirC* dirc = nullptr;  // compact copy for the recent-k sampler (entries_per_bucket below)
+  int64_t bkt_r = 0;     // entries per time bucket the tables were built with (0: none)
   // time bucket tables of the slices (uint32, ~m / bucket_entries + 2V), see NodeDir
   uint32_t* bkt = nullptr;
   int64_t bkt_cap = 0;

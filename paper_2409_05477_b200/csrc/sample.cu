@@ -366,6 +366,45 @@ __device__ __forceinline__ NodeDir load_dir(const NodeDir* __restrict__ dir, int
   return d;
 }
 
+// the compact directory record (graph.cuh DirC): ONE 256-bit load.  t_last is only known for
+// slices without buckets (+inf otherwise: the bracket then starts at n and the last bucket's
+// table entries close it); the bucket edges' width, an interpolation hint, from 1 / scale
+__device__ __forceinline__ NodeDir load_dirc(const DirC* __restrict__ dirc,
+                                             const uint32_t* __restrict__ bkt, int rshift,
+                                             int64_t u, bool pres) {
+  NodeDir d;
+  if (pres) {
+    unsigned long long x0, x1, x2, x3;
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(dirc + u));
+    const uint32_t n = static_cast<uint32_t>(x1), nb = static_cast<uint32_t>(x1 >> 32);
+    const double st = __longlong_as_double(static_cast<long long>(x3));
+    d.start = static_cast<int64_t>(x0);
+    d.end = d.start + n;
+    d.t_first = __longlong_as_double(static_cast<long long>(x2));
+    d.nb = nb;
+    if (nb) {
+      d.t_last = __longlong_as_double(0x7ff0000000000000LL);  // unknown: +inf
+      d.bkt = bkt + (d.start >> rshift) + 2 * u;
+      d.scale = st;
+      d.width = static_cast<double>(__frcp_rn(static_cast<float>(st)));
+    } else {
+      d.t_last = st;
+      d.bkt = nullptr;
+      d.scale = 0.0;
+      d.width = 0.0;
+    }
+  } else {
+    d.start = d.end = 0;
+    d.t_first = d.t_last = 0.0;
+    d.bkt = nullptr;
+    d.scale = 0.0;
+    d.nb = 0;
+    d.width = 0.0;
+  }
+  return d;
+}
+
 template <int W, int QL>
 __device__ __forceinline__ void search_lines(const double* __restrict__ ts, const NodeDir (&d)[QL],
                                              const bool (&pres)[QL], const double (&t)[QL],
@@ -385,7 +424,8 @@ __device__ __forceinline__ void search_lines(const double* __restrict__ ts, cons
       lo[j] = hi[j] = n;
     } else {
       lo[j] = 1;
-      hi[j] = n - 1;
+      // t_last +inf (unknown in the compact record, or a real +inf): the answer may be n
+      hi[j] = isinf(d[j].t_last) ? n : n - 1;
     }
   }
   // time buckets: [lo, hi] narrows to [bkt[j], bkt[j + 1]] (typically ~R entries, one or two
@@ -474,13 +514,15 @@ constexpr int kBulkMaxL = 16;
 
 // REC: the window gather reads the graph's 16-byte records (tgfx_graph::rec) instead of the
 // three columns: one 16-byte load per slot
+// DC: the compact 32-byte directory (one load per query instead of two)
 template <bool ASSEMBLE, bool IDX64, int W, int QL, int MINB, bool BULK = false, bool REC = false,
-          int UNR = 4>
+          int UNR = 4, bool DC = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
     const NodeDir* __restrict__ dir, const int64_t* __restrict__ nbr,
     const int64_t* __restrict__ eid, const double* __restrict__ ts, QueryIn in, int64_t Q,
     int64_t k, int l, int64_t self_idx, uint32_t magic, Outs o,
-    const uint4* __restrict__ rec = nullptr) {
+    const uint4* __restrict__ rec = nullptr, const DirC* __restrict__ dirc = nullptr,
+    const uint32_t* __restrict__ bkt = nullptr, int rshift = 0) {
   constexpr int GQ = 32 * QL;
   // BULK staging: per warp [3][32 * l] 32-bit words (node, edge, dt)
   extern __shared__ __align__(16) uint32_t s_out[];
@@ -504,7 +546,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       pres[j] = q < Q && fetch_query(in, q, u[j], t[j]);
     }
 #pragma unroll
-    for (int j = 0; j < QL; ++j) d[j] = load_dir(dir, u[j], pres[j]);  // bounds + bracket + buckets
+    for (int j = 0; j < QL; ++j)  // bounds + bracket + buckets
+      d[j] = DC ? load_dirc(dirc, bkt, rshift, u[j], pres[j]) : load_dir(dir, u[j], pres[j]);
     search_lines<W, QL>(ts, d, pres, t, m);
 #pragma unroll
     for (int j = 0; j < QL; ++j) {
@@ -1537,6 +1580,15 @@ bool launch_sample_inputs(const SampleInputsArgs& a, int* bad, cudaStream_t s) {
   return true;
 }
 
+// compact directory records for the bulk recent-k kernel (TGFX_DIRC, default 1)
+bool dirc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_DIRC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (a.g->indptr_bad)  // an imported T-CSR whose indptr no slice walk can trust
     throw Error(TGFX_EVALIDATION, "indptr not monotone");
@@ -1562,10 +1614,16 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                         reinterpret_cast<uintptr_t>(a.dt32)) & 15) == 0 &&
                       bulk_enabled();
     if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
+      // compact directory records: slice lengths fit u32 and the bucket size is a power of 2
+      const int64_t R = g->bkt_r;
+      int rshift = 0;
+      while (R > 0 && (int64_t(1) << rshift) < R) ++rshift;
+      const bool dc = g->dirc && g->m < (int64_t(1) << 32) && (R == 0 || (int64_t(1) << rshift) == R) &&
+                      dirc_enabled();
       if (g->rec) {
-#define TGFX_BULK_LAUNCH(REC, U)                                                               \
+#define TGFX_BULK_LAUNCH(REC, U, DCV)                                                          \
   do {                                                                                         \
-    const auto kern = k_recent_line<true, false, kProbeW, 1, 4, true, REC, U>;                 \
+    const auto kern = k_recent_line<true, false, kProbeW, 1, 4, true, REC, U, DCV>;            \
     static const bool attr = [&] {                                                             \
       TGFX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                      kWarps * 3 * 32 * ((kBulkMaxL + U - 1) / U * U) * 4));    \
@@ -1574,14 +1632,18 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     (void)attr;                                                                                \
     const size_t smu = static_cast<size_t>(kWarps) * 3 * 32 * ((l + U - 1) / U * U) * 4;       \
     kern<<<gq, kThreads, smu, s>>>(g->dir, g->nbr, g->eid, g->ts, in, a.q, a.k, l,             \
-                                   a.self_edge_index, magic, o, g->rec);                       \
+                                   a.self_edge_index, magic, o, g->rec, g->dirc, g->bkt,       \
+                                   rshift);                                                    \
   } while (0)
         // 2 slots per lane per load round (measured: 35.8 ms/step vs 37.6 for 4, 38.2 for 1)
-        TGFX_BULK_LAUNCH(true, 2);
+        if (dc)
+          TGFX_BULK_LAUNCH(true, 2, true);
+        else
+          TGFX_BULK_LAUNCH(true, 2, false);
         after_launch("k_recent_line");
         return;
       }
-      TGFX_BULK_LAUNCH(false, 2);
+      TGFX_BULK_LAUNCH(false, 2, false);
 #undef TGFX_BULK_LAUNCH
       after_launch("k_recent_line");
       return;
