@@ -527,6 +527,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
   // BULK staging: per warp [3][32 * l] 32-bit words (node, edge, dt)
   extern __shared__ __align__(16) uint32_t s_out[];
   __shared__ longlong2 s_st[kWarps][GQ];  // {window start, query time bits}: one LDS.128
+  // BULK: {window start << 5 | kb + 1, query time bits} -- a slot's whole staging read is one
+  // LDS.128 (kb <= 15 there); the self-loop token is stored by the query's own lane afterwards
+  __shared__ longlong2 s_bk[BULK ? kWarps : 1][BULK ? GQ : 1];
   __shared__ int64_t s_u[kWarps][GQ];
   __shared__ int s_kb[kWarps][GQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -567,6 +570,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       s_st[warp][qi] = make_longlong2(d[j].start + m[j] - kb, __double_as_longlong(t[j]));
       s_u[warp][qi] = u[j];
       s_kb[warp][qi] = kb;
+      if (BULK)
+        s_bk[warp][qi] = make_longlong2(((d[j].start + m[j] - kb) << 5) | (kb + 1),
+                                        __double_as_longlong(t[j]));
     }
     __syncwarp();
     const int64_t qbase = g * GQ;
@@ -592,18 +598,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
       for (int it0 = 0; it0 < QL * l; it0 += UNR) {
         uint32_t rn[UNR], re[UNR];
         double tv[UNR], tq[UNR];
-        uint32_t sf[UNR];  // self-slot node id + 1, or 0
         bool tk[UNR];
 #pragma unroll
         for (int uu = 0; uu < UNR; ++uu) {
           const bool valid = it0 + uu < QL * l;
           const int qr = valid ? qi : 0;  // padding slots run qi past the warp's 32 queries
-          const int kbq = s_kb[warp][qr];
-          const longlong2 st = s_st[warp][qr];
+          const longlong2 st = s_bk[warp][qr];
+          const int kbq = static_cast<int>(st.x & 31) - 1;
           tk[uu] = valid && j < kbq;
-          sf[uu] = (valid && j == kbq) ? static_cast<uint32_t>(s_u[warp][qr] + 1) : 0u;
           tq[uu] = __longlong_as_double(st.y);
-          const int64_t p = tk[uu] ? st.x + j : 0;
+          const int64_t p = tk[uu] ? (st.x >> 5) + j : 0;
           // volatile: keeps the loads here, unconditional, instead of sunk into phase B's
           // per-slot branches (which would serialise them again)
           if (REC) {
@@ -629,9 +633,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
 #pragma unroll
         for (int uu = 0; uu < UNR; ++uu) {
           const int s = lane + 32 * (it0 + uu);
-          sn[s] = tk[uu] ? rn[uu] + 1u : sf[uu];
-          se[s] = tk[uu] ? re[uu] + 1u : (sf[uu] ? static_cast<uint32_t>(self_idx) : 0u);
+          sn[s] = tk[uu] ? rn[uu] + 1u : 0u;
+          se[s] = tk[uu] ? re[uu] + 1u : 0u;
           sd[s] = tk[uu] ? __double2float_rn(tq[uu] - tv[uu]) : 0.0f;
+        }
+      }
+      __syncwarp();
+      // the self-loop token of each query (sequence.cpp:79-81), by the query's own lane
+#pragma unroll
+      for (int jq = 0; jq < QL; ++jq) {
+        const int qq = jq * 32 + lane;
+        const int kbq = s_kb[warp][qq];
+        if (kbq >= 0) {
+          sn[qq * width + kbq] = static_cast<uint32_t>(u[jq] + 1);
+          se[qq * width + kbq] = static_cast<uint32_t>(self_idx);
         }
       }
       __syncwarp();
