@@ -1379,7 +1379,8 @@ template <int KM, int CH, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_random_lane(
     const NodeDir* __restrict__ dir, const double* __restrict__ ts, const uint4* __restrict__ rec,
     QueryIn in, int64_t Q, int k, int l, int64_t self_idx, uint64_t seed, uint64_t stream_base,
-    Outs o) {
+    Outs o, const DirC* __restrict__ dirc = nullptr, const uint32_t* __restrict__ bkt = nullptr,
+    int rshift = 0) {
   extern __shared__ __align__(16) uint32_t s_rows[];  // per warp [3][32 * l]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t seed_mix = mix64(seed);
@@ -1395,7 +1396,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_random_lane(
     bool pres[1];
     pres[0] = q < Q && fetch_query(in, q, u[0], t[0]);
     NodeDir d[1];
-    d[0] = load_dir(dir, u[0], pres[0]);
+    d[0] = (dirc ? load_dirc(dirc, bkt, rshift, u[0], pres[0]) : load_dir(dir, u[0], pres[0]));
     search_lines<kProbeW, 1>(ts, d, pres, t, m);
     const uint32_t qm = static_cast<uint32_t>(m[0]);
     const bool floyd = pres[0] && qm > static_cast<uint32_t>(k);
@@ -1604,6 +1605,18 @@ bool dirc_enabled() {
   return on;
 }
 
+// the graph's compact directory when the samplers may use it (slice lengths fit u32, bucket
+// size a power of two), else nullptr; *rshift = log2 of the bucket size
+const DirC* compact_dir(const tgfx_graph* g, int* rshift) {
+  const int64_t R = g->bkt_r;
+  int sh = 0;
+  while (R > 0 && (int64_t(1) << sh) < R) ++sh;
+  *rshift = sh;
+  const bool ok = g->dirc && g->m < (int64_t(1) << 32) && (R == 0 || (int64_t(1) << sh) == R) &&
+                  dirc_enabled();
+  return ok ? g->dirc : nullptr;
+}
+
 void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (a.g->indptr_bad)  // an imported T-CSR whose indptr no slice walk can trust
     throw Error(TGFX_EVALIDATION, "indptr not monotone");
@@ -1630,11 +1643,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                       bulk_enabled();
     if (!g->search_exact && bulk) {  // line probes + bulk-copied rows (default for l <= 16)
       // compact directory records: slice lengths fit u32 and the bucket size is a power of 2
-      const int64_t R = g->bkt_r;
       int rshift = 0;
-      while (R > 0 && (int64_t(1) << rshift) < R) ++rshift;
-      const bool dc = g->dirc && g->m < (int64_t(1) << 32) && (R == 0 || (int64_t(1) << rshift) == R) &&
-                      dirc_enabled();
+      const bool dc = compact_dir(g, &rshift) != nullptr;
       if (g->rec) {
 #define TGFX_BULK_LAUNCH(REC, U, DCV)                                                          \
   do {                                                                                         \
@@ -1700,6 +1710,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
   if (lane_uniform && !g->search_exact && g->rec && assemble && !a.index64 && a.dt32 &&
       !a.dt64 && a.k <= 32 && l <= 32) {  // one query per lane (default for k <= 32, l <= 32)
     const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
+    int cshift = 0;
+    const DirC* cdir = compact_dir(g, &cshift);
 #define TGFX_RANDOM_LANE(KM)                                                                   \
   do {                                                                                         \
     static const bool attr = [] {                                                              \
@@ -1711,7 +1723,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     (void)attr;                                                                                \
     k_random_lane<KM, 4, (KM > 16 ? 2 : 3)><<<grid, kThreads, sm, s>>>(g->dir, g->ts, g->rec, in, a.q, \
                                                     static_cast<int>(a.k), l, a.self_edge_index, \
-                                                    a.seed, a.stream_base, o);                 \
+                                                    a.seed, a.stream_base, o, cdir, g->bkt,      \
+                                                    cshift);                                     \
   } while (0)
     if (a.k <= 8)
       TGFX_RANDOM_LANE(8);
