@@ -141,8 +141,12 @@ void scan_u32_to_i64(const uint32_t* in, int64_t n, int64_t* out, cudaStream_t s
 namespace {
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsRounds = 8;
-constexpr int kRsTile = kRsThreads * kRsRounds;  // 2048 keys per tile
+// keys per thread of a onesweep tile: 16 for 8-byte (key, value) pairs (4,096-key tiles: half
+// as many tiles, so half the decoupled look-back walks), 8 otherwise (static shared memory)
+template <typename K, typename V>
+constexpr int rs_rounds() {
+  return sizeof(K) + sizeof(V) <= 8 ? 16 : 8;
+}
 
 // all digit positions' global histograms in one pass: hist[pass * 256 + digit] (u64)
 template <typename K>
@@ -170,6 +174,8 @@ __global__ void __launch_bounds__(kRsThreads) k_onesweep(
     const K* __restrict__ keys_in, const V* __restrict__ vals_in, int64_t n, int shift,
     const int64_t* __restrict__ digit_base, unsigned long long* status, unsigned int* counter,
     K* __restrict__ keys_out, V* __restrict__ vals_out) {
+  constexpr int kRsRounds = rs_rounds<K, V>();
+  constexpr int kRsTile = kRsThreads * kRsRounds;
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ int64_t goff[256];
   __shared__ int64_t s_tile;
@@ -274,7 +280,7 @@ void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
   if (n <= 1) return;
   const int passes = std::min(static_cast<int>(sizeof(K)), (max_bits + 7) / 8);
   if (passes <= 0) return;
-  const int64_t ntiles = ceil_div(n, kRsTile);
+  const int64_t ntiles = ceil_div(n, static_cast<int64_t>(kRsThreads) * rs_rounds<K, V>());
   // workspace: histograms [passes][256] u64 | digit bases [256] i64 | status [ntiles][256] u64
   // | tile counter
   const size_t hb = sizeof(unsigned long long) * 256 * passes;
