@@ -54,28 +54,41 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;  // tile aggregate published
 constexpr unsigned long long kFlagInc = 2ull << 62;  // inclusive prefix published
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
+// The status words are self-contained (flag and value in one 64-bit word, written with one
+// store) and nothing else is read on the strength of them, so relaxed gpu-scope accesses are
+// enough: same-address coherence orders a tile's AGG before its INC.
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
 // exclusive prefix of tile `tile` for one value: walk back over published words until an
 // inclusive prefix (spins while a predecessor has published nothing yet -- predecessors took
-// their tile ids earlier from the same counter, so they are resident and make progress)
+// their tile ids earlier from the same counter, so they are resident and make progress).
+// Four words are loaded per step so a walk over aggregates costs a quarter of the round trips.
 __device__ __forceinline__ unsigned long long lookback(const unsigned long long* status,
                                                        int64_t tile, int64_t stride) {
+  constexpr int W = 4;
   unsigned long long excl = 0;
-  for (int64_t t = tile - 1; t >= 0;) {
-    const unsigned long long w = ld_acquire(status + t * stride);
-    const unsigned long long f = w & ~kValMask;
-    if (f == 0) continue;
-    excl += w & kValMask;
-    if (f == kFlagInc) break;
-    --t;
+  int64_t t = tile - 1;
+  while (t >= 0) {
+    unsigned long long w[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) w[j] = t - j >= 0 ? ld_acquire(status + (t - j) * stride) : kFlagInc;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if (done) continue;
+      const unsigned long long f = w[j] & ~kValMask;
+      if (f == 0) { done = true; continue; }   // not published yet: re-poll from t
+      excl += w[j] & kValMask;
+      --t;
+      if (f == kFlagInc) { done = true; t = -1; }
+    }
   }
   return excl;
 }
