@@ -12,7 +12,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "lib", "libtgfx.so")
+# TGFX_LIB: another build of the same library (A/B timing of two builds in one session)
+LIB_PATH = os.environ.get("TGFX_LIB") or os.path.join(HERE, "lib", "libtgfx.so")
 
 TGFX_OK, TGFX_EVALIDATION, TGFX_EFORMAT, TGFX_ECUDA, TGFX_ENOMEM, TGFX_EUNSUPPORTED = range(6)
 TGFX_RECENT, TGFX_RANDOM = 0, 1
