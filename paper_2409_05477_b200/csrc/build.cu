@@ -1243,8 +1243,38 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
   double xprev = __shfl_up_sync(kFull, x[P - 1], 1);
   if (lane == 31) wts[warp] = x[P - 1];
   int32_t first = v0;  // node of this thread's first entry
-  const bool hub = dir[v0].end > i1;
-  if (!hub) {
+  const NodeDir d0 = dir[v0];
+  const bool hub = d0.end > i1;
+  if (hub) {
+    // the whole tile lies in one slice (the hubs, most of the entries): 32-bit slice-relative
+    // indices, no node bookkeeping -- a dozen instructions per entry
+    __syncthreads();  // wts
+    if (!d0.nb) return;
+    if (lane == 0) xprev = warp ? wts[warp - 1] : (i0 > 0 ? ts[i0 - 1] : 0.0);
+    uint32_t* bkt = const_cast<uint32_t*>(d0.bkt);
+    const uint32_t nb = static_cast<uint32_t>(d0.nb);
+    const double nbm1 = static_cast<double>(nb - 1);
+    const auto bucket = [&](double t) -> int {  // bucket_of, with nb - 1 hoisted
+      const double xx = __dmul_rn(__dsub_rn(t, d0.t_first), d0.scale);
+      return static_cast<int>(xx < nbm1 ? static_cast<uint32_t>(xx) : nb - 1);
+    };
+    const uint32_t r0 = static_cast<uint32_t>(b0 - d0.start);
+    const uint32_t last = static_cast<uint32_t>(d0.end - d0.start - 1);
+    const int live = min(P, cnt - tid * P);  // entries of this thread
+    int jprev = (live > 0 && r0 > 0) ? bucket(xprev) : -1;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (k >= live) continue;
+      const uint32_t r = r0 + static_cast<uint32_t>(k);
+      const int jr = bucket(x[k]);
+      if (jr > jprev) bkt[jprev + 1] = r;
+      for (int j = jprev + 2; j <= jr; ++j) bkt[j] = r;
+      jprev = jr;
+      if (r == last) bkt[nb] = r + 1;
+    }
+    return;
+  }
+  {
     for (int q = tid; q < cnt; q += 256) mark[q] = -1;
     __syncthreads();
     for (int32_t u = v0 + 1 + tid; u <= v1; u += 256) {
@@ -1270,12 +1300,10 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
     if (lane == 0) ex = -1;
     for (int w = 0; w < warp; ++w) ex = max(ex, wmax[w]);
     first = max(v0, ex);  // node owning position tid*P (before this thread's own marks)
-  } else {
-    __syncthreads();
   }
   if (lane == 0) xprev = warp ? wts[warp - 1] : (i0 > 0 ? ts[i0 - 1] : 0.0);
   int32_t u = first;
-  NodeDir d = dir[u];
+  NodeDir d = first == v0 ? d0 : dir[u];
   int jprev = -1;  // bucket of the previous entry of the same slice
   {
     const int64_t i = b0;
@@ -1285,7 +1313,7 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
   for (int k = 0; k < P; ++k) {
     const int64_t i = b0 + k;
     if (i > i1) continue;
-    if (!hub) {
+    {
       const int32_t mk = mark[tid * P + k];
       if (mk >= 0 && mk != u) {  // a new slice starts here
         u = mk;
