@@ -1190,6 +1190,14 @@ bool bulk_enabled() {
   return on;
 }
 
+int recent_unr() {
+  static const int v = [] {
+    const char* e = getenv("TGFX_RECENT_UNR");
+    return e ? atoi(e) : 4;
+  }();
+  return v;
+}
+
 int grid_groups(int64_t Q) {
   const int64_t groups = ceil_div(std::max<int64_t>(Q, 1), 32);
   const int64_t blocks = ceil_div(groups, kWarps);
@@ -1660,9 +1668,15 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                                    a.self_edge_index, magic, o, g->rec, g->dirc, g->bkt,       \
                                    rshift);                                                    \
   } while (0)
-        // 2 slots per lane per load round (measured: 35.8 ms/step vs 37.6 for 4, 38.2 for 1)
-        if (dc)
+        // slots per lane per load round: 2 with the 64-byte directory (round 1: 35.8 ms/step
+        // against 37.6 for 4, 38.2 for 1); with the compact directory, TGFX_RECENT_UNR (round 2,
+        // GDELT step launch: 2 / 3 / 4 / 6 -> 1.373 / 1.329 / 1.309 / 1.390 ms)
+        if (dc && recent_unr() == 2)
           TGFX_BULK_LAUNCH(true, 2, true);
+        else if (dc && recent_unr() == 3)
+          TGFX_BULK_LAUNCH(true, 3, true);
+        else if (dc)
+          TGFX_BULK_LAUNCH(true, 4, true);
         else
           TGFX_BULK_LAUNCH(true, 2, false);
         after_launch("k_recent_line");
