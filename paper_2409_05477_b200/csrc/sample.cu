@@ -1726,16 +1726,17 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     const size_t sm = static_cast<size_t>(kWarps) * 3 * 32 * l * 4;
     int cshift = 0;
     const DirC* cdir = compact_dir(g, &cshift);
-#define TGFX_RANDOM_LANE(KM)                                                                   \
+#define TGFX_RANDOM_LANE(KM) TGFX_RANDOM_LANE_C(KM, 4, (KM > 16 ? 2 : 3))
+#define TGFX_RANDOM_LANE_C(KM, CH, MB)                                                         \
   do {                                                                                         \
     static const bool attr = [] {                                                              \
-      TGFX_CUDA(cudaFuncSetAttribute(k_random_lane<KM, 4, (KM > 16 ? 2 : 3)>,                  \
+      TGFX_CUDA(cudaFuncSetAttribute(k_random_lane<KM, CH, MB>,                                \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                      kWarps * 3 * 32 * 32 * 4));                               \
       return true;                                                                             \
     }();                                                                                       \
     (void)attr;                                                                                \
-    k_random_lane<KM, 4, (KM > 16 ? 2 : 3)><<<grid, kThreads, sm, s>>>(g->dir, g->ts, g->rec, in, a.q, \
+    k_random_lane<KM, CH, MB><<<grid, kThreads, sm, s>>>(g->dir, g->ts, g->rec, in, a.q,        \
                                                     static_cast<int>(a.k), l, a.self_edge_index, \
                                                     a.seed, a.stream_base, o, cdir, g->bkt,      \
                                                     cshift);                                     \
@@ -1744,11 +1745,13 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
       TGFX_RANDOM_LANE(8);
     else if (a.k <= 16)
       TGFX_RANDOM_LANE(16);
-    else if (a.k <= 24)
-      TGFX_RANDOM_LANE(24);
+    else if (a.k <= 24)  // loads in chunks of 8 (round 2, one 48 M-query GDELT uniform-20
+      TGFX_RANDOM_LANE_C(24, 8, 2);  // launch: chunks of 2 / 4 / 8 / 12 / 24 -> 19.5 / 19.2-19.5 /
+                                     // 18.6-18.8 / 20.1 / 23.6 ms; LastFM 0.85 -> 0.83 ms)
     else
       TGFX_RANDOM_LANE(32);
 #undef TGFX_RANDOM_LANE
+#undef TGFX_RANDOM_LANE_C
     after_launch("k_random_lane");
     return;
   }
