@@ -535,8 +535,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = ASSEMBLE ? l : static_cast<int>(k);
   const int64_t ngroups = ceil_div(Q, GQ);
+  // BULK launches cover every group with the grid (one group per warp, launch_sample checks):
+  // the loop then runs at most once and carries no counter (which was spilled at 64 registers)
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * kWarps + warp; g < ngroups;
-       g += static_cast<int64_t>(gridDim.x) * kWarps) {
+       g = BULK ? ngroups : g + static_cast<int64_t>(gridDim.x) * kWarps) {
     int64_t u[QL], m[QL];
     double t[QL];
     bool pres[QL];
@@ -1644,6 +1646,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
     // a group per warp (a persistent grid of 4 or 8 blocks per SM measured 22 % slower)
     const int gq = static_cast<int>(
         std::min<int64_t>(ceil_div(ceil_div(a.q, 32), kWarps), INT32_MAX));
+    if (ceil_div(a.q, 32) > static_cast<int64_t>(gq) * kWarps)  // > 5.5e11 queries in one call
+      throw Error(TGFX_EUNSUPPORTED, "too many queries for one launch");
     const bool bulk = assemble && !a.index64 && a.dt32 && !a.dt64 && l <= kBulkMaxL &&
                       ((reinterpret_cast<uintptr_t>(a.node_index) |
                         reinterpret_cast<uintptr_t>(a.edge_index) |
