@@ -1195,7 +1195,7 @@ bool bulk_enabled() {
 int recent_unr() {
   static const int v = [] {
     const char* e = getenv("TGFX_RECENT_UNR");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 0;
   }();
   return v;
 }
@@ -1673,12 +1673,17 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
                                    rshift);                                                    \
   } while (0)
         // slots per lane per load round: 2 with the 64-byte directory (round 1: 35.8 ms/step
-        // against 37.6 for 4, 38.2 for 1); with the compact directory, TGFX_RECENT_UNR (round 2,
-        // GDELT step launch: 2 / 3 / 4 / 6 -> 1.373 / 1.329 / 1.309 / 1.390 ms)
-        if (dc && recent_unr() == 2)
+        // against 37.6 for 4, 38.2 for 1); with the compact directory and no loop-carried
+        // spill (round 2, GDELT step launch, l = 11): 3 / 4 / 5 / 6 / 12 -> 1.277 / 1.254 /
+        // 1.617 / 1.235 / 1.405 ms -- 6 while it pads l to at most 12 slots, else 4
+        // (TGFX_RECENT_UNR overrides)
+        const int unr = recent_unr() ? recent_unr() : (l <= 12 ? 6 : 4);
+        if (dc && unr == 2)
           TGFX_BULK_LAUNCH(true, 2, true);
-        else if (dc && recent_unr() == 3)
+        else if (dc && unr == 3)
           TGFX_BULK_LAUNCH(true, 3, true);
+        else if (dc && unr == 6)
+          TGFX_BULK_LAUNCH(true, 6, true);
         else if (dc)
           TGFX_BULK_LAUNCH(true, 4, true);
         else
