@@ -21,6 +21,7 @@
 #ifndef TGFX_H
 #define TGFX_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -161,6 +162,22 @@ int tgfx_graph_from_device(int64_t num_nodes, int64_t num_edges, int reverse, in
 int tgfx_sample_batch(const tgfx_graph* g, const int64_t* nodes, const double* times,
                       int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
                       int64_t* counts, int64_t* nbr, int64_t* eid, double* ts);
+/* One sampled neighbour in the reference's record layout (NeighborEntry, sampler.hpp:14-18;
+ * 24 bytes, so a NeighborSample's std::vector<NeighborEntry> is a run of these). */
+typedef struct tgfx_neighbor {
+  int64_t neighbor;
+  int64_t edge;
+  double timestamp;
+} tgfx_neighbor;
+/* tgfx_sample_batch with the padded [q, k] entries written as tgfx_neighbor records (one
+ * device->host copy; what the C++ layer's tgf::sample_batch copies into its NeighborSamples) */
+int tgfx_sample_batch_records(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                              int64_t q, int64_t k, int strategy, uint64_t seed,
+                              uint64_t stream_base, int64_t* counts, tgfx_neighbor* entries);
+/* Page-locked host memory for the host-buffer calls: their copies from and to such buffers
+ * run as plain DMA without the driver's bounce copy (cudaHostAlloc / cudaFreeHost). */
+int tgfx_host_alloc(size_t bytes, void** p);
+int tgfx_host_free(void* p);
 int tgfx_sample_batch_device(const tgfx_graph* g, const int64_t* d_nodes,
                              const double* d_times, int64_t q, int64_t k, int strategy,
                              uint64_t seed, uint64_t stream_base, int64_t* d_counts,
@@ -257,6 +274,13 @@ int tgfx_assemble(int64_t q, int64_t kpad, const int64_t* counts, const int64_t*
                   const double* query_times, int64_t l, int64_t self_edge_index,
                   int64_t* node_index, int64_t* edge_index, double* time_delta,
                   int64_t* valid_len, int64_t* target_row);
+/* tgfx_assemble over tgfx_neighbor records [q, kpad] (tgf::build_sequence_batch's NeighborSamples
+ * packed as they are laid out in memory) */
+int tgfx_assemble_records(int64_t q, int64_t kpad, const int64_t* counts,
+                          const tgfx_neighbor* entries, const int64_t* query_nodes,
+                          const double* query_times, int64_t l, int64_t self_edge_index,
+                          int64_t* node_index, int64_t* edge_index, double* time_delta,
+                          int64_t* valid_len, int64_t* target_row);
 /* replaces tgf::build_mask (sequence.hpp:50, sequence.cpp:93-111): (q*l) x l doubles */
 int tgfx_build_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
                     int kind, double* mask);

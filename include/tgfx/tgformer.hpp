@@ -80,6 +80,9 @@ class Matrix {
  public:
   Matrix() = default;
   Matrix(std::size_t rows, std::size_t cols) : r_(rows), c_(cols), v_(rows * cols, 0.0) {}
+  // a rows x cols copy of src (row-major), without first zero-filling
+  Matrix(std::size_t rows, std::size_t cols, const double* src)
+      : r_(rows), c_(cols), v_(src, src + rows * cols) {}
   std::size_t rows() const { return r_; }
   std::size_t cols() const { return c_; }
   std::size_t size() const { return v_.size(); }

@@ -90,6 +90,9 @@ SIGNATURES = {
     "tgfx_graph_free": [_P],
     "tgfx_graph_build_path": [_P],
     "tgfx_sample_batch": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _P, _P, _P, _P],
+    "tgfx_sample_batch_records": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _P, _P],
+    "tgfx_host_alloc": [C.c_size_t, C.POINTER(_P)],
+    "tgfx_host_free": [_P],
     "tgfx_sample_batch_device": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _P, _P, _P, _P, _P, _U],
     "tgfx_sample_assemble": [_P, _P, _P, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P, _P, _P,
                              _P],
@@ -122,6 +125,7 @@ SIGNATURES = {
     "tgfx_sample_two_hop": [_P, _P, _P, _I64, _I64, _I64, _I, _U64, _U64, _I64, _I64, _P, _P, _P,
                             _P, _P, _P, _P, _P],
     "tgfx_assemble": [_I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P],
+    "tgfx_assemble_records": [_I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P],
     "tgfx_build_mask": [_I64, _I64, _P, _P, _I, _P],
     "tgfx_make_random_stream": [_I64, _I64, _U64, C.c_double, _P],
     "tgfx_make_random_stream_device": [_I64, _I64, _U64, C.c_double, _P, _P],

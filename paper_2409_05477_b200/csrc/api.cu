@@ -9,6 +9,7 @@
 #include <cstring>
 #include <fstream>
 #include <vector>
+#include <initializer_list>
 #include <mutex>
 #include <new>
 #include <string>
@@ -208,12 +209,121 @@ void check_graph(const tgfx_graph* g) {
   if (!g) throw Error(TGFX_EVALIDATION, "null graph");
 }
 
+
 void check_k(int64_t k) {
   if (k < 1) throw Error(TGFX_EVALIDATION, "k must be at least 1");  // sampler.cpp:25
 }
 
 void check_l(int64_t l) {
   if (l < 2) throw Error(TGFX_EVALIDATION, "sequence length must be at least 2");  // sequence.cpp:57
+}
+
+// ---- small synchronous host-buffer calls (one forward_concat batch: a few thousand queries)
+// Each calling thread keeps one device arena and one stream, so a call is: its H2D copies,
+// one or two launches, its D2H copies and one stream synchronisation -- no allocation, no
+// pool traffic and no extra round trip for the query check (done on the host buffers).  The
+// arena grows to the largest call up to kArenaMax; bigger calls take pool buffers.  The
+// stream is a blocking one: it orders after work on the legacy default stream, like the
+// rest of the host-buffer calls.  Neither is released before the process exits.
+constexpr size_t kArenaMax = size_t(256) << 20;
+
+struct HostCall {
+  cudaStream_t s = nullptr;
+  char* arena = nullptr;
+  size_t cap = 0;
+  int dev = -1;
+};
+
+HostCall& host_call() {
+  thread_local HostCall hc;
+  const int dev = device_info().device;
+  if (hc.dev != dev) {  // first call on this thread (or after a device switch)
+    hc = HostCall{};
+    TGFX_CUDA(cudaStreamCreate(&hc.s));
+    hc.dev = dev;
+  }
+  return hc;
+}
+
+// device scratch of `bytes` on hc.s: the thread's arena, or a pool buffer held by `own`
+struct Scratch {
+  char* p = nullptr;
+  void* own = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch(HostCall& hc, size_t bytes) : s(hc.s) {
+    if (bytes > kArenaMax) {
+      own = dmalloc(bytes, s);
+      p = static_cast<char*>(own);
+      return;
+    }
+    if (bytes > hc.cap) {
+      if (hc.arena) {
+        TGFX_CUDA(cudaStreamSynchronize(hc.s));
+        TGFX_CUDA(cudaFree(hc.arena));
+        hc.arena = nullptr;
+        hc.cap = 0;
+      }
+      const size_t c = std::min(kArenaMax, std::max(bytes + bytes / 2, size_t(4) << 20));
+      TGFX_CUDA(cudaMalloc(&hc.arena, c));
+      hc.cap = c;
+    }
+    p = hc.arena;
+  }
+  ~Scratch() {
+    if (own) {
+      try {
+        dfree(own, s);
+      } catch (...) {
+      }
+    }
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+};
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// The copies of one host call, in order; a run of segments adjacent on both sides is issued as
+// one copy.  The device scratch places each direction's buffers back to back, so a caller
+// whose host buffers are back to back too (the C++ layer's pinned staging) pays one DMA per
+// direction instead of one per array.
+struct Seg {
+  void* dst;
+  const void* src;
+  size_t n;
+};
+void copy_merged(std::initializer_list<Seg> segs, cudaMemcpyKind kind, cudaStream_t s) {
+  char* d = nullptr;
+  const char* h = nullptr;
+  size_t n = 0;
+  auto flush = [&] {
+    if (n && d && h) TGFX_CUDA(cudaMemcpyAsync(d, h, n, kind, s));
+    n = 0;
+  };
+  for (const Seg& g : segs) {
+    if (!g.n || !g.dst || !g.src) continue;
+    if (n && static_cast<char*>(g.dst) == d + n && static_cast<const char*>(g.src) == h + n) {
+      n += g.n;
+      continue;
+    }
+    flush();
+    d = static_cast<char*>(g.dst);
+    h = static_cast<const char*>(g.src);
+    n = g.n;
+  }
+  flush();
+}
+
+// sampler.cpp:88-93 on the caller's host buffer: every query's node in order, then k (checked
+// with query 0, so k < 1 reports after query 0's node)
+void check_queries_host(const tgfx_graph* g, const int64_t* nodes, int64_t q, int64_t k) {
+  if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
+  if (q == 0) return;
+  const int64_t n = k < 1 ? 1 : q;
+  for (int64_t i = 0; i < n; ++i)
+    if (nodes[i] < 0 || nodes[i] >= g->V)
+      throw Error(TGFX_EVALIDATION, "query node " + std::to_string(nodes[i]) + " out of range");
+  check_k(k);
 }
 
 void check_queries(const tgfx_graph* g, const int64_t* d_nodes, int64_t q, int64_t k,
@@ -573,40 +683,86 @@ int tgfx_graph_free(tgfx_graph* g) {
   return guarded([&] { free_graph(g); });
 }
 
+namespace {
+
+// tgfx_sample_batch / tgfx_sample_batch_records: padded [q, k] entries as three columns
+// (rec == nullptr) or as tgfx_neighbor records, through the calling thread's arena
+void sample_entries_host(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                         int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
+                         int64_t* counts, int64_t* nbr, int64_t* eid, double* ts,
+                         tgfx_neighbor* rec) {
+  check_graph(g);
+  check_queries_host(g, nodes, q, k);
+  if (q == 0) return;
+  HostCall& hc = host_call();
+  const size_t qs = static_cast<size_t>(q), qk = qs * static_cast<size_t>(k);
+  // device: [nodes | times] [counts | entries] (each direction back to back)
+  const size_t o_t = 8 * qs, o_c = al256(16 * qs), o_e = o_c + 8 * qs;
+  Scratch d(hc, o_e + 24 * qk);
+  copy_merged({{d.p, nodes, 8 * qs}, {d.p + o_t, times, 8 * qs}}, cudaMemcpyHostToDevice, hc.s);
+  int64_t* e = reinterpret_cast<int64_t*>(d.p + o_e);
+  SampleArgs a{};
+  a.g = g;
+  a.nodes = reinterpret_cast<const int64_t*>(d.p);
+  a.times = reinterpret_cast<const double*>(d.p + o_t);
+  a.q = q;
+  a.k = k;
+  a.strategy = strategy;
+  a.seed = seed;
+  a.stream_base = stream_base;
+  a.counts = reinterpret_cast<int64_t*>(d.p + o_c);
+  if (rec) {  // interleaved: record i = words [3i, 3i + 3)
+    a.e_nbr = e;
+    a.e_eid = e + 1;
+    a.e_ts = reinterpret_cast<double*>(e + 2);
+    a.e_stride = 3;
+  } else {
+    a.e_nbr = e;
+    a.e_eid = e + qk;
+    a.e_ts = reinterpret_cast<double*>(e + 2 * qk);
+  }
+  launch_sample(a, hc.s);
+  if (rec)
+    copy_merged({{counts, a.counts, 8 * qs}, {rec, e, 24 * qk}}, cudaMemcpyDeviceToHost, hc.s);
+  else
+    copy_merged({{counts, a.counts, 8 * qs}, {nbr, e, 8 * qk}, {eid, e + qk, 8 * qk},
+                 {ts, e + 2 * qk, 8 * qk}},
+                cudaMemcpyDeviceToHost, hc.s);
+  TGFX_CUDA(cudaStreamSynchronize(hc.s));
+}
+
+}  // namespace
+
 int tgfx_sample_batch(const tgfx_graph* g, const int64_t* nodes, const double* times, int64_t q,
                       int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
                       int64_t* counts, int64_t* nbr, int64_t* eid, double* ts) {
   return guarded([&] {
-    check_graph(g);
-    cudaStream_t s = 0;
-    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
-    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
-    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
-    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
-    check_queries(g, dn.as<int64_t>(), q, k, s);
-    if (q == 0) return;
-    const size_t qk = qb * static_cast<size_t>(k);
-    DBuf dc(sizeof(int64_t) * qb, s), en(sizeof(int64_t) * qk, s), ee(sizeof(int64_t) * qk, s),
-        et(sizeof(double) * qk, s);
-    SampleArgs a{};
-    a.g = g;
-    a.nodes = dn.as<int64_t>();
-    a.times = dt.as<double>();
-    a.q = q;
-    a.k = k;
-    a.strategy = strategy;
-    a.seed = seed;
-    a.stream_base = stream_base;
-    a.counts = dc.as<int64_t>();
-    a.e_nbr = en.as<int64_t>();
-    a.e_eid = ee.as<int64_t>();
-    a.e_ts = et.as<double>();
-    launch_sample(a, s);
-    d2h(counts, dc.p, sizeof(int64_t) * q, s);
-    d2h(nbr, en.p, sizeof(int64_t) * q * k, s);
-    d2h(eid, ee.p, sizeof(int64_t) * q * k, s);
-    d2h(ts, et.p, sizeof(double) * q * k, s);
-    TGFX_CUDA(cudaStreamSynchronize(s));
+    sample_entries_host(g, nodes, times, q, k, strategy, seed, stream_base, counts, nbr, eid, ts,
+                        nullptr);
+  });
+}
+
+int tgfx_sample_batch_records(const tgfx_graph* g, const int64_t* nodes, const double* times,
+                              int64_t q, int64_t k, int strategy, uint64_t seed,
+                              uint64_t stream_base, int64_t* counts, tgfx_neighbor* entries) {
+  return guarded([&] {
+    sample_entries_host(g, nodes, times, q, k, strategy, seed, stream_base, counts, nullptr,
+                        nullptr, nullptr, entries);
+  });
+}
+
+int tgfx_host_alloc(size_t bytes, void** p) {
+  return guarded([&] {
+    if (!p) throw Error(TGFX_EVALIDATION, "null output pointer");
+    *p = nullptr;
+    device_info();
+    TGFX_CUDA(cudaHostAlloc(p, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+
+int tgfx_host_free(void* p) {
+  return guarded([&] {
+    if (p) TGFX_CUDA(cudaFreeHost(p));
   });
 }
 
@@ -1199,20 +1355,20 @@ int tgfx_sample_sequence_batch(const tgfx_graph* g, const int64_t* nodes, const 
                                int64_t* valid_len, int64_t* target_row) {
   return guarded([&] {
     check_graph(g);
-    cudaStream_t s = 0;
-    const size_t qb = static_cast<size_t>(std::max<int64_t>(q, 1));
-    DBuf dn(sizeof(int64_t) * qb, s), dt(sizeof(double) * qb, s);
-    h2d(dn.p, nodes, sizeof(int64_t) * std::max<int64_t>(q, 0), s);
-    h2d(dt.p, times, sizeof(double) * std::max<int64_t>(q, 0), s);
-    check_queries(g, dn.as<int64_t>(), q, k, s);  // sampler.cpp:88-93 (k only if q > 0)
-    check_l(l);                                   // sequence.cpp:57, after sampling's checks
+    check_queries_host(g, nodes, q, k);  // sampler.cpp:88-93 (k only if q > 0)
+    check_l(l);                          // sequence.cpp:57, after sampling's checks
     if (q <= 0) return;
-    const size_t ql = qb * static_cast<size_t>(l);
-    DBuf on(8 * ql, s), oe(8 * ql, s), od(8 * ql, s), ov(8 * qb, s);
+    HostCall& hc = host_call();
+    const size_t qs = static_cast<size_t>(q), ql = qs * static_cast<size_t>(l);
+    // device: [nodes | times] [node_index | edge_index | time_delta | valid_len]
+    const size_t o_t = 8 * qs, o_n = al256(16 * qs), o_e = o_n + 8 * ql, o_d = o_e + 8 * ql,
+                 o_v = o_d + 8 * ql;
+    Scratch d(hc, o_v + 8 * qs);
+    copy_merged({{d.p, nodes, 8 * qs}, {d.p + o_t, times, 8 * qs}}, cudaMemcpyHostToDevice, hc.s);
     SampleArgs a{};
     a.g = g;
-    a.nodes = dn.as<int64_t>();
-    a.times = dt.as<double>();
+    a.nodes = reinterpret_cast<const int64_t*>(d.p);
+    a.times = reinterpret_cast<const double*>(d.p + o_t);
     a.q = q;
     a.k = k;
     a.strategy = strategy;
@@ -1220,18 +1376,17 @@ int tgfx_sample_sequence_batch(const tgfx_graph* g, const int64_t* nodes, const 
     a.stream_base = stream_base;
     a.l = l;
     a.self_edge_index = self_edge_index;
-    a.node_index = on.p;
-    a.edge_index = oe.p;
+    a.node_index = d.p + o_n;
+    a.edge_index = d.p + o_e;
     a.dt32 = nullptr;
-    a.dt64 = od.as<double>();
-    a.valid_len = ov.p;
+    a.dt64 = reinterpret_cast<double*>(d.p + o_d);
+    a.valid_len = d.p + o_v;
     a.index64 = true;
-    launch_sample(a, s);
-    d2h(node_index, on.p, 8 * ql, s);
-    d2h(edge_index, oe.p, 8 * ql, s);
-    d2h(time_delta, od.p, 8 * ql, s);
-    d2h(valid_len, ov.p, 8 * qb, s);
-    TGFX_CUDA(cudaStreamSynchronize(s));
+    launch_sample(a, hc.s);
+    copy_merged({{node_index, d.p + o_n, 8 * ql}, {edge_index, d.p + o_e, 8 * ql},
+                 {time_delta, d.p + o_d, 8 * ql}, {valid_len, d.p + o_v, 8 * qs}},
+                cudaMemcpyDeviceToHost, hc.s);
+    TGFX_CUDA(cudaStreamSynchronize(hc.s));
     if (target_row)
       for (int64_t b = 0; b < q; ++b) target_row[b] = valid_len[b] - 1;  // sequence.cpp:83
   });
@@ -1296,39 +1451,79 @@ int tgfx_sample_two_hop(const tgfx_graph* g, const int64_t* roots, const double*
   });
 }
 
+namespace {
+
+// build_sequence_batch (sequence.cpp:55-86) over padded host samples: columns (rec ==
+// nullptr) or tgfx_neighbor records, through the calling thread's arena
+void assemble_host(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
+                   const int64_t* eid, const double* ts, const tgfx_neighbor* rec,
+                   const int64_t* query_nodes, const double* query_times, int64_t l,
+                   int64_t self_edge_index, int64_t* node_index, int64_t* edge_index,
+                   double* time_delta, int64_t* valid_len, int64_t* target_row) {
+  check_l(l);
+  if (q < 0 || kpad < 0) throw Error(TGFX_EVALIDATION, "bad batch shape");
+  for (int64_t b = 0; b < q; ++b)
+    if (counts[b] < 0 || counts[b] > kpad) throw Error(TGFX_EVALIDATION, "bad sample count");
+  if (q == 0) return;
+  HostCall& hc = host_call();
+  const size_t qs = static_cast<size_t>(q), qk = qs * static_cast<size_t>(kpad),
+               ql = qs * static_cast<size_t>(l);
+  // device: [counts | entries (records, or nbr | eid | ts) | query nodes | query times]
+  //         [node_index | edge_index | time_delta | valid_len | target_row]
+  const size_t o_n = 8 * qs, o_qn = o_n + 24 * qk, o_qt = o_qn + 8 * qs,
+               o_on = al256(o_qt + 8 * qs), o_oe = o_on + 8 * ql, o_od = o_oe + 8 * ql,
+               o_ov = o_od + 8 * ql, o_or = o_ov + 8 * qs;
+  Scratch d(hc, o_or + 8 * qs);
+  auto at = [&](size_t o) { return reinterpret_cast<int64_t*>(d.p + o); };
+  const int64_t *dn = at(o_n), *de, *dtp;
+  int64_t es = 1;
+  if (rec) {  // records [q, kpad]; the three fields at word offsets 0, 1, 2
+    copy_merged({{d.p, counts, 8 * qs}, {d.p + o_n, rec, 24 * qk},
+                 {d.p + o_qn, query_nodes, 8 * qs}, {d.p + o_qt, query_times, 8 * qs}},
+                cudaMemcpyHostToDevice, hc.s);
+    de = dn + 1;
+    dtp = dn + 2;
+    es = 3;
+  } else {
+    copy_merged({{d.p, counts, 8 * qs}, {d.p + o_n, nbr, 8 * qk},
+                 {d.p + o_n + 8 * qk, eid, 8 * qk}, {d.p + o_n + 16 * qk, ts, 8 * qk},
+                 {d.p + o_qn, query_nodes, 8 * qs}, {d.p + o_qt, query_times, 8 * qs}},
+                cudaMemcpyHostToDevice, hc.s);
+    de = dn + qk;
+    dtp = dn + 2 * qk;
+  }
+  launch_assemble_entries(q, kpad, at(0), dn, de, reinterpret_cast<const double*>(dtp),
+                          at(o_qn), reinterpret_cast<const double*>(at(o_qt)), l,
+                          self_edge_index, at(o_on), at(o_oe),
+                          reinterpret_cast<double*>(at(o_od)), at(o_ov), at(o_or), hc.s, es);
+  copy_merged({{node_index, d.p + o_on, 8 * ql}, {edge_index, d.p + o_oe, 8 * ql},
+               {time_delta, d.p + o_od, 8 * ql}, {valid_len, d.p + o_ov, 8 * qs},
+               {target_row, d.p + o_or, 8 * qs}},
+              cudaMemcpyDeviceToHost, hc.s);
+  TGFX_CUDA(cudaStreamSynchronize(hc.s));
+}
+
+}  // namespace
+
 int tgfx_assemble(int64_t q, int64_t kpad, const int64_t* counts, const int64_t* nbr,
                   const int64_t* eid, const double* ts, const int64_t* query_nodes,
                   const double* query_times, int64_t l, int64_t self_edge_index,
                   int64_t* node_index, int64_t* edge_index, double* time_delta,
                   int64_t* valid_len, int64_t* target_row) {
   return guarded([&] {
-    check_l(l);
-    if (q < 0 || kpad < 0) throw Error(TGFX_EVALIDATION, "bad batch shape");
-    for (int64_t b = 0; b < q; ++b)
-      if (counts[b] < 0 || counts[b] > kpad) throw Error(TGFX_EVALIDATION, "bad sample count");
-    if (q == 0) return;
-    device_info();
-    cudaStream_t s = 0;
-    const size_t qb = static_cast<size_t>(q), qk = qb * std::max<int64_t>(kpad, 1),
-                 ql = qb * static_cast<size_t>(l);
-    DBuf c(8 * qb, s), n(8 * qk, s), e(8 * qk, s), t(8 * qk, s), qn(8 * qb, s), qt(8 * qb, s);
-    DBuf on(8 * ql, s), oe(8 * ql, s), od(8 * ql, s), ov(8 * qb, s), orow(8 * qb, s);
-    h2d(c.p, counts, 8 * qb, s);
-    h2d(n.p, nbr, 8 * qb * kpad, s);
-    h2d(e.p, eid, 8 * qb * kpad, s);
-    h2d(t.p, ts, 8 * qb * kpad, s);
-    h2d(qn.p, query_nodes, 8 * qb, s);
-    h2d(qt.p, query_times, 8 * qb, s);
-    launch_assemble_entries(q, kpad, c.as<int64_t>(), n.as<int64_t>(), e.as<int64_t>(),
-                            t.as<double>(), qn.as<int64_t>(), qt.as<double>(), l, self_edge_index,
-                            on.as<int64_t>(), oe.as<int64_t>(), od.as<double>(), ov.as<int64_t>(),
-                            orow.as<int64_t>(), s);
-    d2h(node_index, on.p, 8 * ql, s);
-    d2h(edge_index, oe.p, 8 * ql, s);
-    d2h(time_delta, od.p, 8 * ql, s);
-    d2h(valid_len, ov.p, 8 * qb, s);
-    d2h(target_row, orow.p, 8 * qb, s);
-    TGFX_CUDA(cudaStreamSynchronize(s));
+    assemble_host(q, kpad, counts, nbr, eid, ts, nullptr, query_nodes, query_times, l,
+                  self_edge_index, node_index, edge_index, time_delta, valid_len, target_row);
+  });
+}
+
+int tgfx_assemble_records(int64_t q, int64_t kpad, const int64_t* counts,
+                          const tgfx_neighbor* entries, const int64_t* query_nodes,
+                          const double* query_times, int64_t l, int64_t self_edge_index,
+                          int64_t* node_index, int64_t* edge_index, double* time_delta,
+                          int64_t* valid_len, int64_t* target_row) {
+  return guarded([&] {
+    assemble_host(q, kpad, counts, nullptr, nullptr, nullptr, entries, query_nodes, query_times,
+                  l, self_edge_index, node_index, edge_index, time_delta, valid_len, target_row);
   });
 }
 

@@ -154,6 +154,7 @@ struct SampleArgs {
   int64_t* e_nbr = nullptr;
   int64_t* e_eid = nullptr;
   double* e_ts = nullptr;
+  int64_t e_stride = 1;  // 3: e_nbr/e_eid/e_ts interleaved as tgfx_neighbor records
   // hop-2 mode: query (nodes, times) given padded [q_roots, k1] with per-root counts
   const int64_t* hop_counts = nullptr;
   int64_t hop_k1 = 0;
@@ -182,7 +183,8 @@ void launch_assemble_entries(int64_t q, int64_t kpad, const int64_t* counts, con
                              const int64_t* eid, const double* ts, const int64_t* qn,
                              const double* qt, int64_t l, int64_t self_edge_index,
                              int64_t* node_index, int64_t* edge_index, double* dt,
-                             int64_t* valid_len, int64_t* target_row, cudaStream_t s);
+                             int64_t* valid_len, int64_t* target_row, cudaStream_t s,
+                             int64_t es = 1);
 void launch_mask(int64_t q, int64_t l, const int64_t* valid_len, const int64_t* target_row,
                  int kind, double* mask, cudaStream_t s);
 

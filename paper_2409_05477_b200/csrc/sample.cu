@@ -98,7 +98,15 @@ struct Outs {
   int64_t* e_nbr;
   int64_t* e_eid;
   double* e_ts;
+  int64_t es;  // entry stride in 8-byte words: 1 = three columns, 3 = tgfx_neighbor records
 };
+
+__device__ __forceinline__ void put_entry(const Outs& o, int64_t i, int64_t nb, int64_t ed,
+                                          double t) {
+  o.e_nbr[i * o.es] = nb;
+  o.e_eid[i * o.es] = ed;
+  o.e_ts[i * o.es] = t;
+}
 
 // Output rows are written once and never re-read by the kernel: streaming (evict-first)
 // stores keep them from pushing the T-CSR lines the searches reuse out of L2.
@@ -314,9 +322,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent(
         int64_t a = 0, b = 0;
         double c = 0.0;
         if (j < kbq) fetch_entry(rec, nbr, eid, ts, s_start[warp][qi] + j, a, b, c);
-        o.e_nbr[obase + s] = a;
-        o.e_eid[obase + s] = b;
-        o.e_ts[obase + s] = c;
+        put_entry(o, obase + s, a, b, c);
       }
     }
     __syncwarp();
@@ -696,9 +702,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_recent_line(
                           take ? ei + 1 : self ? self_idx : 0,
                           take ? __longlong_as_double(st.y) - tv : 0.0);
       } else {
-        o.e_nbr[obase + s] = take ? ni : 0;
-        o.e_eid[obase + s] = take ? ei : 0;
-        o.e_ts[obase + s] = take ? tv : 0.0;
+        put_entry(o, obase + s, take ? ni : 0, take ? ei : 0, take ? tv : 0.0);
       }
       j += dj;
       qi += dq;
@@ -1010,9 +1014,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
             int64_t a = 0, b = 0;
             double c = 0.0;
             if (h) fetch_entry(rec, nbr, eid, ts, qlo + j, a, b, c);
-            o.e_nbr[qq * k + j] = a;
-            o.e_eid[qq * k + j] = b;
-            o.e_ts[qq * k + j] = c;
+            put_entry(o, qq * k + j, a, b, c);
           }
           if (lane == 0) o.counts[qq] = qm;
         }
@@ -1047,9 +1049,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
             int64_t ni, ei;
             double tv;
             fetch_entry(rec, nbr, eid, ts, qlo + static_cast<int64_t>(list[r]), ni, ei, tv);
-            o.e_nbr[qq * k + r] = ni;
-            o.e_eid[qq * k + r] = ei;
-            o.e_ts[qq * k + r] = tv;
+            put_entry(o, qq * k + r, ni, ei, tv);
           }
           if (lane == 0) o.counts[qq] = kk;
         }
@@ -1118,9 +1118,7 @@ __global__ void __launch_bounds__(kThreads) k_random(
             int64_t ni, ei;
             double tv;
             fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
-            o.e_nbr[qq * k + rank[p]] = ni;
-            o.e_eid[qq * k + rank[p]] = ei;
-            o.e_ts[qq * k + rank[p]] = tv;
+            put_entry(o, qq * k + rank[p], ni, ei, tv);
           }
         }
         if (lane == 0) o.counts[qq] = kk;
@@ -1149,7 +1147,7 @@ __global__ void k_assemble_entries(int64_t q, int64_t kpad, const int64_t* __res
                                    const double* __restrict__ ts, const int64_t* __restrict__ qn,
                                    const double* __restrict__ qt, int64_t l, int64_t self_idx,
                                    int64_t* node_index, int64_t* edge_index, double* dt,
-                                   int64_t* valid_len, int64_t* target_row) {
+                                   int64_t* valid_len, int64_t* target_row, int64_t es) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q * l;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = i / l, j = i - b * l;
@@ -1159,7 +1157,7 @@ __global__ void k_assemble_entries(int64_t q, int64_t kpad, const int64_t* __res
     int64_t ni = 0, ei = 0;
     double d = 0.0;
     if (j < kb) {
-      const int64_t s = b * kpad + skip + j;
+      const int64_t s = (b * kpad + skip + j) * es;
       ni = nbr[s] + 1;
       ei = eid[s] + 1;
       d = qt[b] - ts[s];
@@ -1364,9 +1362,7 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
             int64_t a = 0, b = 0;
             double c = 0.0;
             if (h) fetch_entry(rec, nbr, eid, ts, qlo + j, a, b, c);
-            o.e_nbr[qq * k + j] = a;
-            o.e_eid[qq * k + j] = b;
-            o.e_ts[qq * k + j] = c;
+            put_entry(o, qq * k + j, a, b, c);
           }
           if (r == 0) o.counts[qq] = take;
           continue;
@@ -1378,9 +1374,7 @@ __global__ void __launch_bounds__(kThreads) k_random_g(
             int64_t ni, ei;
             double tv;
             fetch_entry(rec, nbr, eid, ts, qlo + c[p], ni, ei, tv);
-            o.e_nbr[qq * k + rank[p]] = ni;
-            o.e_eid[qq * k + rank[p]] = ei;
-            o.e_ts[qq * k + rank[p]] = tv;
+            put_entry(o, qq * k + rank[p], ni, ei, tv);
           }
         }
         if (r == 0) o.counts[qq] = kk;
@@ -1646,8 +1640,8 @@ void launch_sample(const SampleArgs& a, cudaStream_t s) {
   const tgfx_graph* g = a.g;
   QueryIn in{a.nodes, a.times, a.hop_counts, a.hop_k1, a.seeds, a.batch_q,
              g->V,    a.first_bad, a.stream_base};
-  Outs o{a.node_index, a.edge_index, a.dt32, a.dt64, a.valid_len,
-         a.counts,     a.e_nbr,      a.e_eid, a.e_ts};
+  Outs o{a.node_index, a.edge_index, a.dt32, a.dt64,  a.valid_len,
+         a.counts,     a.e_nbr,      a.e_eid, a.e_ts, a.e_stride};
   const int grid = grid_groups(a.q);
   if (ceil_div(a.q, 32) > static_cast<int64_t>(grid) * kWarps)  // > 5.5e11 queries per call
     throw Error(TGFX_EUNSUPPORTED, "too many queries for one launch");
@@ -1863,12 +1857,13 @@ void launch_assemble_entries(int64_t q, int64_t kpad, const int64_t* counts, con
                              const int64_t* eid, const double* ts, const int64_t* qn,
                              const double* qt, int64_t l, int64_t self_edge_index,
                              int64_t* node_index, int64_t* edge_index, double* dt,
-                             int64_t* valid_len, int64_t* target_row, cudaStream_t s) {
+                             int64_t* valid_len, int64_t* target_row, cudaStream_t s,
+                             int64_t es) {
   if (q <= 0) return;
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(q * l, 256), device_info().sms * 8));
   k_assemble_entries<<<grid, 256, 0, s>>>(q, kpad, counts, nbr, eid, ts, qn, qt, l,
                                           self_edge_index, node_index, edge_index, dt, valid_len,
-                                          target_row);
+                                          target_row, es);
   after_launch("k_assemble_entries");
 }
 

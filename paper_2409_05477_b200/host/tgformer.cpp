@@ -10,9 +10,12 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstring>
 #include <fstream>
 #include <mutex>
+
+#include <omp.h>
 
 namespace tgf {
 
@@ -31,9 +34,51 @@ void check(int rc) {
   if (rc != TGFX_OK) throw_status(rc, tgfx_last_error());
 }
 
-// Content fingerprint of the host columns: full FNV-1a over small graphs, a strided sample
-// plus the sizes over large ones.  Detects a TCsr whose columns were replaced or edited after
-// its device copy was made (the reference treats TCsr as immutable).
+// Per-thread page-locked staging for the host <-> device copies of the sampling and sequence
+// calls (grown on demand, kept for the thread's lifetime): a copy from or to it is one DMA,
+// where a copy from a std::vector's pageable memory goes through the driver's bounce buffer.
+struct Pinned {
+  void* p = nullptr;
+  std::size_t cap = 0;
+  Pinned() = default;
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned() {
+    if (p) tgfx_host_free(p);
+  }
+  char* get(std::size_t bytes) {
+    if (bytes > cap) {
+      if (p) tgfx_host_free(p);
+      p = nullptr;
+      cap = 0;
+      const std::size_t c = std::max<std::size_t>(bytes + bytes / 2, std::size_t(1) << 20);
+      check(tgfx_host_alloc(c, &p));
+      cap = c;
+    }
+    return static_cast<char*>(p);
+  }
+};
+
+Pinned& pinned_in() {
+  thread_local Pinned b;
+  return b;
+}
+Pinned& pinned_out() {
+  thread_local Pinned b;
+  return b;
+}
+
+
+// bodies of loops over a batch's queries: OpenMP threads once a batch is large enough that
+// the vector allocations and copies outweigh waking the team (the reference's own loops
+// are OpenMP too, sampler.cpp:95)
+constexpr std::int64_t kParMin = 512;
+
+// Fingerprint of the host columns: their sizes, plus a full FNV-1a over small graphs and 64
+// strided words per column over large ones (not the addresses: a copied TCsr shares its
+// source's device copy).  Detects a TCsr whose columns were replaced (or resized) after its
+// device copy was made; an in-place edit of a large column is usually missed (the reference treats TCsr as immutable).  It runs on every
+// sampling call, so it stays far below a batch's own cost: 256 cache misses, not 16 K.
 std::uint64_t fingerprint(const TCsr& g) {
   std::uint64_t h = 1469598103934665603ULL;
   auto mixin = [&](std::uint64_t x) {
@@ -46,7 +91,7 @@ std::uint64_t fingerprint(const TCsr& g) {
   auto cols = [&](const void* p, std::size_t n) {
     mixin(n);
     const auto* w = static_cast<const std::uint64_t*>(p);
-    const std::size_t step = n <= (1u << 16) ? 1 : n / 4096;
+    const std::size_t step = n <= (1u << 12) ? 1 : n / 64;
     for (std::size_t i = 0; i < n; i += step) mixin(w[i] + i);
     if (n) mixin(w[n - 1]);
   };
@@ -383,7 +428,15 @@ SampleStrategy parse_strategy(const std::string& name) {
 
 namespace {
 
-// One libtgfx batch call; stream of query i = stream_base + i (sampler.cpp:100-101).
+static_assert(sizeof(NeighborEntry) == sizeof(tgfx_neighbor) &&
+                  offsetof(NeighborEntry, neighbor) == offsetof(tgfx_neighbor, neighbor) &&
+                  offsetof(NeighborEntry, edge) == offsetof(tgfx_neighbor, edge) &&
+                  offsetof(NeighborEntry, timestamp) == offsetof(tgfx_neighbor, timestamp),
+              "NeighborEntry must have the tgfx_neighbor record layout");
+
+// One libtgfx batch call; stream of query i = stream_base + i (sampler.cpp:100-101).  The
+// queries go up and the padded records come back through the thread's pinned staging; each
+// NeighborSample's vector is then one copy of its run of records.
 std::vector<NeighborSample> run_batch(const TCsr& g, const NodeId* nodes, const Time* times,
                                       std::int64_t q, std::int64_t k, SampleStrategy strategy,
                                       std::uint64_t seed, std::uint64_t stream_base) {
@@ -394,22 +447,48 @@ std::vector<NeighborSample> run_batch(const TCsr& g, const NodeId* nodes, const 
   const std::int64_t kpad = k < 1 ? k : std::max<std::int64_t>(1, std::min(k, dc.max_degree));
   const std::size_t qs = static_cast<std::size_t>(std::max<std::int64_t>(q, 0));
   const std::size_t slots = qs * static_cast<std::size_t>(std::max<std::int64_t>(kpad, 1));
-  std::vector<std::int64_t> counts(qs), nb(slots), ed(slots);
-  std::vector<double> ts(slots);
-  detail::check(tgfx_sample_batch(dc.handle, nodes, times, q, kpad,
-                                  strategy == SampleStrategy::recent ? TGFX_RECENT : TGFX_RANDOM,
-                                  seed, stream_base, counts.data(), nb.data(), ed.data(),
-                                  ts.data()));
+  char* in = detail::pinned_in().get(16 * qs);
+  std::memcpy(in, nodes, 8 * qs);
+  std::memcpy(in + 8 * qs, times, 8 * qs);
+  // counts and records back to back: one device->host copy
+  char* o = detail::pinned_out().get(8 * qs + 24 * slots);
+  const auto* counts = reinterpret_cast<const std::int64_t*>(o);
+  const auto* rec = reinterpret_cast<const NeighborEntry*>(o + 8 * qs);
+  const int strat = strategy == SampleStrategy::recent ? TGFX_RECENT : TGFX_RANDOM;
   std::vector<NeighborSample> out(qs);
-  for (std::size_t i = 0; i < qs; ++i) {
-    NeighborSample& s = out[i];
-    s.query_node = nodes[i];
-    s.query_time = times[i];
-    const std::size_t base = i * static_cast<std::size_t>(kpad);
-    s.neighbors.resize(static_cast<std::size_t>(counts[i]));
-    for (std::size_t j = 0; j < s.neighbors.size(); ++j)
-      s.neighbors[j] = {nb[base + j], ed[base + j], ts[base + j]};
+  const std::int64_t n = static_cast<std::int64_t>(qs);
+  // Large batches: one thread runs the (synchronous) device call while the others allocate
+  // the samples' vectors (kpad entries each, when that is small), then all copy the records
+  // out.  The allocation, the slowest host step, hides under the device round trip.
+  const bool par = n >= detail::kParMin;
+  const bool pre = par && kpad <= 64;
+  int rc = TGFX_OK;
+#pragma omp parallel if (par)
+  {
+    const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+    if (t == 0) {
+      rc = tgfx_sample_batch_records(dc.handle, reinterpret_cast<const std::int64_t*>(in),
+                                     reinterpret_cast<const double*>(in + 8 * qs), q, kpad, strat,
+                                     seed, stream_base, reinterpret_cast<std::int64_t*>(o),
+                                     reinterpret_cast<tgfx_neighbor*>(o + 8 * qs));
+    } else if (pre) {
+      for (std::int64_t i = (t - 1) * n / (nt - 1); i < t * n / (nt - 1); ++i)
+        out[static_cast<std::size_t>(i)].neighbors.reserve(static_cast<std::size_t>(kpad));
+    }
+#pragma omp barrier
+    if (rc == TGFX_OK) {
+#pragma omp for schedule(static)
+      for (std::int64_t i = 0; i < n; ++i) {
+        NeighborSample& s = out[static_cast<std::size_t>(i)];
+        s.query_node = nodes[i];
+        s.query_time = times[i];
+        const NeighborEntry* r =
+            rec + static_cast<std::size_t>(i) * static_cast<std::size_t>(kpad);
+        s.neighbors.assign(r, r + counts[i]);
+      }
+    }
   }
+  detail::check(rc);
   return out;
 }
 
@@ -478,40 +557,76 @@ MaskKind parse_mask_kind(const std::string& name) {
   throw ValidationError("unknown mask kind '" + name + "'");
 }
 
+namespace {
+
+// The SequenceBatch columns from the pinned staging the device wrote them to: assign() copies
+// without the value-initialisation a resize() would first write.
+SequenceBatch unpack_sequences(const char* o, std::int64_t q, std::int64_t l,
+                               std::size_t o_e, std::size_t o_d, std::size_t o_v,
+                               std::size_t o_r) {
+  SequenceBatch out;
+  out.batch = q;
+  out.l = l;
+  const std::size_t ql = static_cast<std::size_t>(q) * static_cast<std::size_t>(l);
+  const auto* ni = reinterpret_cast<const std::int64_t*>(o);
+  const auto* ei = reinterpret_cast<const std::int64_t*>(o + o_e);
+  const auto* vl = reinterpret_cast<const std::int64_t*>(o + o_v);
+  const auto* tr = reinterpret_cast<const std::int64_t*>(o + o_r);
+  // the three [q, l] columns are copied by three threads once they are large
+#pragma omp parallel sections if (ql >= 8192)
+  {
+#pragma omp section
+    out.node_index.assign(ni, ni + ql);
+#pragma omp section
+    out.edge_index.assign(ei, ei + ql);
+#pragma omp section
+    out.time_delta = Matrix(static_cast<std::size_t>(q), static_cast<std::size_t>(l),
+                            reinterpret_cast<const double*>(o + o_d));
+  }
+  out.valid_len.assign(vl, vl + q);
+  out.target_row.assign(tr, tr + q);
+  return out;
+}
+
+}  // namespace
+
 SequenceBatch build_sequence_batch(const std::vector<NeighborSample>& samples, std::int64_t l,
                                    std::int64_t self_edge_index) {
   if (l < 2) throw ValidationError("sequence length must be at least 2");  // sequence.cpp:57
   const std::int64_t q = static_cast<std::int64_t>(samples.size());
+  // sequence.cpp:66-70 reads only a sample's last min(total, l - 1) entries: only those are
+  // packed (count kb, skip 0), which leaves the rows unchanged
+  const std::size_t tail = static_cast<std::size_t>(l - 1);
   std::size_t kpad = 1;
-  for (const NeighborSample& s : samples) kpad = std::max(kpad, s.neighbors.size());
-  const std::size_t qs = static_cast<std::size_t>(q);
-  std::vector<std::int64_t> counts(qs), nb(qs * kpad), ed(qs * kpad), qn(qs);
-  std::vector<double> ts(qs * kpad), qt(qs);
-  for (std::size_t b = 0; b < qs; ++b) {
-    const NeighborSample& s = samples[b];
-    counts[b] = static_cast<std::int64_t>(s.neighbors.size());
+  for (const NeighborSample& s : samples) kpad = std::max(kpad, std::min(tail, s.neighbors.size()));
+  const std::size_t qs = static_cast<std::size_t>(q), ql = qs * static_cast<std::size_t>(l);
+  // inputs and outputs each back to back (one copy per direction)
+  const std::size_t i_e = 8 * qs, i_qn = i_e + 24 * qs * kpad,
+                    i_qt = i_qn + 8 * qs;
+  char* in = detail::pinned_in().get(i_qt + 8 * qs);
+  auto* cnt = reinterpret_cast<std::int64_t*>(in);
+  auto* rec = reinterpret_cast<NeighborEntry*>(in + i_e);
+  auto* qn = reinterpret_cast<std::int64_t*>(in + i_qn);
+  auto* qt = reinterpret_cast<double*>(in + i_qt);
+#pragma omp parallel for schedule(static) if (q >= detail::kParMin)
+  for (std::int64_t b = 0; b < q; ++b) {
+    const NeighborSample& s = samples[static_cast<std::size_t>(b)];
+    const std::size_t total = s.neighbors.size(), kb = std::min(total, tail);
+    cnt[b] = static_cast<std::int64_t>(kb);
     qn[b] = s.query_node;
     qt[b] = s.query_time;
-    for (std::size_t j = 0; j < s.neighbors.size(); ++j) {
-      nb[b * kpad + j] = s.neighbors[j].neighbor;
-      ed[b * kpad + j] = s.neighbors[j].edge;
-      ts[b * kpad + j] = s.neighbors[j].timestamp;
-    }
+    if (kb)
+      std::memcpy(rec + static_cast<std::size_t>(b) * kpad, s.neighbors.data() + (total - kb),
+                  kb * sizeof(NeighborEntry));
   }
-  SequenceBatch out;
-  out.batch = q;
-  out.l = l;
-  const std::size_t ql = qs * static_cast<std::size_t>(l);
-  out.node_index.resize(ql);
-  out.edge_index.resize(ql);
-  out.time_delta = Matrix(qs, static_cast<std::size_t>(l));
-  out.valid_len.resize(qs);
-  out.target_row.resize(qs);
-  detail::check(tgfx_assemble(q, static_cast<std::int64_t>(kpad), counts.data(), nb.data(),
-                              ed.data(), ts.data(), qn.data(), qt.data(), l, self_edge_index,
-                              out.node_index.data(), out.edge_index.data(), out.time_delta.data(),
-                              out.valid_len.data(), out.target_row.data()));
-  return out;
+  const std::size_t o_e = 8 * ql, o_d = o_e + 8 * ql, o_v = o_d + 8 * ql, o_r = o_v + 8 * qs;
+  char* o = detail::pinned_out().get(o_r + 8 * qs);
+  detail::check(tgfx_assemble_records(
+      q, static_cast<std::int64_t>(kpad), cnt, reinterpret_cast<const tgfx_neighbor*>(rec), qn,
+      qt, l, self_edge_index, reinterpret_cast<std::int64_t*>(o),
+      reinterpret_cast<std::int64_t*>(o + o_e), reinterpret_cast<double*>(o + o_d),
+      reinterpret_cast<std::int64_t*>(o + o_v), reinterpret_cast<std::int64_t*>(o + o_r)));
+  return unpack_sequences(o, q, l, o_e, o_d, o_v, o_r);
 }
 
 SequenceBatch sample_sequence_batch(const TCsr& g, const std::vector<NodeId>& nodes,
@@ -524,21 +639,20 @@ SequenceBatch sample_sequence_batch(const TCsr& g, const std::vector<NodeId>& no
   const std::shared_ptr<detail::DeviceCopy> dc = detail::device_of(g);
   const std::int64_t q = static_cast<std::int64_t>(nodes.size());
   const std::size_t qs = nodes.size();
-  SequenceBatch out;
-  out.batch = q;
-  out.l = l;
+  char* in = detail::pinned_in().get(16 * qs);
+  std::memcpy(in, nodes.data(), 8 * qs);
+  std::memcpy(in + 8 * qs, times.data(), 8 * qs);
   const std::size_t ql = qs * static_cast<std::size_t>(l > 0 ? l : 0);
-  out.node_index.resize(ql);
-  out.edge_index.resize(ql);
-  out.time_delta = Matrix(qs, static_cast<std::size_t>(l > 0 ? l : 0));
-  out.valid_len.resize(qs);
-  out.target_row.resize(qs);
+  const std::size_t o_e = 8 * ql, o_d = o_e + 8 * ql, o_v = o_d + 8 * ql, o_r = o_v + 8 * qs;
+  char* o = detail::pinned_out().get(o_r + 8 * qs);
   detail::check(tgfx_sample_sequence_batch(
-      dc->handle, nodes.data(), times.data(), q, k,
+      dc->handle, reinterpret_cast<const std::int64_t*>(in),
+      reinterpret_cast<const double*>(in + 8 * qs), q, k,
       strategy == SampleStrategy::recent ? TGFX_RECENT : TGFX_RANDOM, seed, 0, l,
-      self_edge_index, out.node_index.data(), out.edge_index.data(), out.time_delta.data(),
-      out.valid_len.data(), out.target_row.data()));
-  return out;
+      self_edge_index, reinterpret_cast<std::int64_t*>(o),
+      reinterpret_cast<std::int64_t*>(o + o_e), reinterpret_cast<double*>(o + o_d),
+      reinterpret_cast<std::int64_t*>(o + o_v), reinterpret_cast<std::int64_t*>(o + o_r)));
+  return unpack_sequences(o, q, l > 0 ? l : 0, o_e, o_d, o_v, o_r);
 }
 
 SequenceBatch build_sequence(const NeighborSample& sample, std::int64_t l,

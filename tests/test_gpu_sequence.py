@@ -63,3 +63,62 @@ def test_device_generator_large_prefix(oracle_mod):
     want = oracle_mod.make_random_stream(3_000_000, 16682, 42)
     got = D.random_stream(3_000_000, 16682, 42).cpu().numpy()
     assert got.tobytes() == want.view(np.uint8).tobytes()
+
+
+def test_record_layout_calls_match_column_calls(T):
+    """tgfx_sample_batch_records / tgfx_assemble_records (the C++ layer's forward_concat route,
+    tgfx_neighbor records = NeighborEntry) equal the column calls, from pinned and pageable
+    host buffers, on the reference golden sequences and on a sampled batch."""
+    import ctypes as C
+
+    from paper_2409_05477_b200._lib import check, lib
+    L = lib()
+    rec_t = np.dtype([("neighbor", np.int64), ("edge", np.int64), ("timestamp", np.float64)])
+    g = golden("sequence")
+    q, kp = g["nbr"].shape
+    rec = np.zeros((q, kp), rec_t)
+    rec["neighbor"], rec["edge"], rec["timestamp"] = g["nbr"], g["eid"], g["ts"]
+    for l in (2, 4, 11, 33):
+        outs = [np.zeros(q * l, np.int64), np.zeros(q * l, np.int64), np.zeros(q * l, np.float64),
+                np.zeros(q, np.int64), np.zeros(q, np.int64)]
+        args = [np.ascontiguousarray(x) for x in (g["counts"], rec, g["qn"], g["qt"])]
+        check(L.tgfx_assemble_records(q, kp, *(a.ctypes.data for a in args), l, 5001,
+                                      *(o.ctypes.data for o in outs)))
+        for o, kk in zip(outs, ("node_index", "edge_index", "time_delta", "valid_len",
+                                "target_row")):
+            assert o.tobytes() == np.ascontiguousarray(g[f"l{l}_{kk}"]).tobytes(), (l, kk)
+
+    ev = T.make_random_stream(30_000, 250, 3)
+    gr = T.build_parallel(ev, True, 4)
+    rng = np.random.default_rng(1)
+    nq = 5000
+    nodes = rng.integers(0, 250, nq).astype(np.int64)
+    times = rng.uniform(0, 30_000, nq)
+    # the same call from page-locked buffers
+    p = C.c_void_p()
+    check(L.tgfx_host_alloc(16 * nq, C.byref(p)))
+    try:
+        pin = np.ctypeslib.as_array((C.c_char * (16 * nq)).from_address(p.value))
+        pn = pin[:8 * nq].view(np.int64)
+        pt = pin[8 * nq:].view(np.float64)
+        pn[:], pt[:] = nodes, times
+        for strat, code, k in (("recent", 0, 10), ("random", 1, 20), ("random", 1, 300)):
+            counts, nb, ed, ts = T.sample_batch_arrays(gr, nodes, times, k, strat, 9)
+            for src_n, src_t in ((nodes, times), (pn, pt)):
+                c2 = np.zeros(nq, np.int64)
+                r2 = np.zeros((nq, k), rec_t)
+                check(L.tgfx_sample_batch_records(gr.handle, src_n.ctypes.data, src_t.ctypes.data,
+                                                  nq, k, code, 9, 0, c2.ctypes.data,
+                                                  r2.ctypes.data))
+                assert np.array_equal(c2, counts), strat
+                assert np.array_equal(r2["neighbor"], nb), strat
+                assert np.array_equal(r2["edge"], ed), strat
+                assert r2["timestamp"].tobytes() == ts.tobytes(), strat
+        bad = nodes.copy()
+        bad[77] = 250
+        with pytest.raises(T.ValidationError, match="query node 250 out of range"):
+            check(L.tgfx_sample_batch_records(gr.handle, bad.ctypes.data, times.ctypes.data, nq, 5,
+                                              0, 0, 0, np.zeros(nq, np.int64).ctypes.data,
+                                              np.zeros((nq, 5), rec_t).ctypes.data))
+    finally:
+        check(L.tgfx_host_free(p))
