@@ -11,6 +11,7 @@
 #include <vector>
 #include <initializer_list>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <string>
 
@@ -1219,21 +1220,76 @@ int tgfx_sample_assemble_batched_device(const tgfx_graph* g, const int64_t* d_no
 }
 
 // Host-buffer sample_assemble, pipelined: the output rows (136 B/query at l = 11) dwarf the
-// inputs (16 B/query), so the call is bound by device->host copies.  Node ids go up first
-// (every query is validated before any output is written, sampler.cpp:88-93); then the
-// queries are processed in sub-chunks on two streams, so the times upload of one sub-chunk,
-// the kernel of the next and the row download of the previous overlap on the copy engines.
+// inputs (16 B/query), so the call is bound by its device->host copies, and the copy engine
+// should start early and never idle.  The queries are processed in sub-chunks on the calling
+// thread's two lanes (stream + device buffers, kept across calls): a sub-chunk's node and
+// time upload, its kernel, and the previous sub-chunk's row download overlap on the copy
+// engines.  sampler.cpp:88-93 validates every query before anything is sampled and nothing
+// is returned on failure: here host threads scan the node ids while the first two sub-chunks
+// already sample into device buffers (a bad node is an absent query to the kernels, so that
+// is safe), and no row reaches the caller's buffers before the scan has passed.
+namespace {
+
+struct AsmLanes {
+  static constexpr int kN = 2;
+  cudaStream_t st[kN] = {nullptr, nullptr};
+  char* buf[kN] = {nullptr, nullptr};
+  size_t cap[kN] = {0, 0};
+  cudaEvent_t after_legacy = nullptr;  // orders the lanes after the legacy default stream
+  int dev = -1;
+};
+
+AsmLanes& asm_lanes() {
+  thread_local AsmLanes L;
+  const int dev = device_info().device;
+  if (L.dev != dev) {
+    L = AsmLanes{};
+    for (cudaStream_t& st : L.st) TGFX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    TGFX_CUDA(cudaEventCreateWithFlags(&L.after_legacy, cudaEventDisableTiming));
+    L.dev = dev;
+  }
+  return L;
+}
+
+int64_t asm_sub_queries() {
+  static const int64_t v = [] {
+    const char* e = getenv("TGFX_ASM_SUB");  // A/B: queries per sub-chunk
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(4) << 20;
+  }();
+  return v;
+}
+
+// index of the first node outside [0, V) in nodes[0, q), or -1; threads over ranges for big q
+int64_t first_bad_node_host(const int64_t* nodes, int64_t q, int64_t V) {
+  auto scan = [&](int64_t a, int64_t b) -> int64_t {
+    for (int64_t i = a; i < b; ++i)
+      if (static_cast<uint64_t>(nodes[i]) >= static_cast<uint64_t>(V)) return i;
+    return -1;
+  };
+  const int T = q >= (int64_t(1) << 20)
+                    ? static_cast<int>(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())))
+                    : 1;
+  if (T == 1) return scan(0, q);
+  std::vector<int64_t> first(static_cast<size_t>(T), -1);
+  std::vector<std::thread> th;
+  th.reserve(static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] { first[static_cast<size_t>(t)] = scan(q * t / T, q * (t + 1) / T); });
+  for (std::thread& x : th) x.join();
+  for (int64_t f : first)
+    if (f >= 0) return f;
+  return -1;
+}
+
+}  // namespace
+
 int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double* times,
                          int64_t q, int64_t k, int strategy, uint64_t seed, uint64_t stream_base,
                          int64_t l, int64_t self_edge_index, int32_t* node_index,
                          int32_t* edge_index, float* dt32, double* dt64, int32_t* valid_len) {
   return guarded([&] {
     check_graph(g);
-    cudaStream_t s = 0;
-    // sampler.cpp:88-93 validates every query before sampling (query 0's node, then k, then
-    // the rest) and nothing is written on failure.  Query 0 and k are checked on the host; the
-    // other nodes on the device while the first sub-chunks already sample (into device
-    // buffers only); the rows are copied out only once every query has passed.
+    // query 0's node, then k (checked with query 0), then the others (sampler.cpp:88-93)
     if (q < 0) throw Error(TGFX_EVALIDATION, "negative query count");
     if (q > 0 && (nodes[0] < 0 || nodes[0] >= g->V))
       throw Error(TGFX_EVALIDATION, "query node " + std::to_string(nodes[0]) + " out of range");
@@ -1241,97 +1297,86 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     check_l(l);
     check_int32_outputs(g, self_edge_index);
     if (q == 0) return;
-    DBuf dn(sizeof(int64_t) * static_cast<size_t>(q), s);
-    DBuf first(sizeof(unsigned long long), s);
-    const unsigned long long none = ~0ull;
-    TGFX_CUDA(cudaMemcpyAsync(first.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
-    h2d(dn.p, nodes, sizeof(int64_t) * q, s);
-    // bad nodes are also replaced by node 0 in this device copy, so sampling can start on it
-    // before the host has seen the verdict
-    find_bad_async(g, dn.as<int64_t>(), q, 0, static_cast<unsigned long long*>(first.p), s);
-    unsigned long long bad = none;
-    TGFX_CUDA(cudaMemcpyAsync(&bad, first.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    cudaEvent_t nodes_ready = nullptr;
-    TGFX_CUDA(cudaEventCreateWithFlags(&nodes_ready, cudaEventDisableTiming));
-    TGFX_CUDA(cudaEventRecord(nodes_ready, s));
-    constexpr int kStreams = 2;
-    const int64_t sub = std::min<int64_t>(q, int64_t(1) << 22);  // 4 M queries per sub-chunk
+    AsmLanes& L = asm_lanes();
+    const int64_t sub = std::min<int64_t>(q, asm_sub_queries());
     const size_t sl = static_cast<size_t>(sub) * static_cast<size_t>(l);
-    struct Lane {
-      cudaStream_t st = nullptr;
-      void *t = nullptr, *on = nullptr, *oe = nullptr, *o32 = nullptr, *o64 = nullptr,
-           *ov = nullptr;
-    } lanes[kStreams];
-    auto release = [&] {
-      for (Lane& ln : lanes) {
-        if (!ln.st) continue;
-        cudaStreamSynchronize(ln.st);
-        for (void* p : {ln.t, ln.on, ln.oe, ln.o32, ln.o64, ln.ov}) {
-          try {
-            dfree(p, ln.st);  // dmalloc'd: big blocks go back to the size cache
-          } catch (...) {
-          }
+    // lane layout: [nodes | times] [node_index | edge_index | dt32 | dt64 | valid_len]
+    const size_t o_t = 8 * static_cast<size_t>(sub), o_n = al256(16 * static_cast<size_t>(sub)),
+                 o_e = o_n + al256(4 * sl), o_f = o_e + al256(4 * sl),
+                 o_d = o_f + (dt32 ? al256(4 * sl) : 0), o_v = o_d + (dt64 ? al256(8 * sl) : 0),
+                 need = o_v + 4 * static_cast<size_t>(sub);
+    for (int i = 0; i < AsmLanes::kN; ++i)
+      if (L.cap[i] < need) {
+        if (L.buf[i]) {
+          TGFX_CUDA(cudaStreamSynchronize(L.st[i]));
+          TGFX_CUDA(cudaFree(L.buf[i]));
+          L.buf[i] = nullptr;
+          L.cap[i] = 0;
         }
-        cudaStreamSynchronize(ln.st);
-        cudaStreamDestroy(ln.st);
-        ln.st = nullptr;
+        TGFX_CUDA(cudaMalloc(&L.buf[i], need));
+        L.cap[i] = need;
       }
-      cudaStreamSynchronize(s);
-      if (nodes_ready) cudaEventDestroy(nodes_ready);
-      nodes_ready = nullptr;
+    // like every host-buffer call, after the work already queued on the legacy default stream
+    TGFX_CUDA(cudaEventRecord(L.after_legacy, 0));
+    for (cudaStream_t st : L.st) TGFX_CUDA(cudaStreamWaitEvent(st, L.after_legacy, 0));
+    // the scan of nodes[1, q) runs on host threads beside the first sub-chunks
+    int64_t bad = -1;
+    std::thread checker;
+    if (q > 1) checker = std::thread([&] {
+      const int64_t f = first_bad_node_host(nodes + 1, q - 1, g->V);
+      bad = f < 0 ? -1 : f + 1;
+    });
+    auto join = [&] {
+      if (checker.joinable()) checker.join();
+    };
+    // sub-chunk i covers queries [c0(i), c0(i + 1)): the first is small (1/8 of the others) so
+    // the first row download starts after a short upload and kernel, then full sub-chunks
+    const int64_t head = std::max<int64_t>(1, sub / 8);
+    const int64_t nsub = q <= head ? 1 : 1 + ceil_div(q - head, sub);
+    auto c0_of = [&](int64_t i) { return i == 0 ? int64_t(0) : std::min(q, head + (i - 1) * sub); };
+    auto c1_of = [&](int64_t i) { return i + 1 >= nsub ? q : c0_of(i + 1); };
+    auto compute = [&](int64_t i) {  // upload + sampling of sub-chunk i on its lane
+      const int ln = static_cast<int>(i % AsmLanes::kN);
+      char* d = L.buf[ln];
+      const int64_t c0 = c0_of(i), c = c1_of(i) - c0;
+      h2d(d, nodes + c0, 8 * static_cast<size_t>(c), L.st[ln]);
+      h2d(d + o_t, times + c0, 8 * static_cast<size_t>(c), L.st[ln]);
+      SampleArgs a{};
+      a.g = g;
+      a.nodes = reinterpret_cast<const int64_t*>(d);
+      a.times = reinterpret_cast<const double*>(d + o_t);
+      a.q = c;
+      a.k = k;
+      a.strategy = strategy;
+      a.seed = seed;
+      a.stream_base = stream_base + static_cast<uint64_t>(c0);
+      a.l = l;
+      a.self_edge_index = self_edge_index;
+      a.node_index = d + o_n;
+      a.edge_index = d + o_e;
+      a.dt32 = dt32 ? reinterpret_cast<float*>(d + o_f) : nullptr;
+      a.dt64 = dt64 ? reinterpret_cast<double*>(d + o_d) : nullptr;
+      a.valid_len = d + o_v;
+      launch_sample(a, L.st[ln]);
+    };
+    auto copy_out = [&](int64_t i) {  // rows of sub-chunk i to the caller's buffers
+      const int ln = static_cast<int>(i % AsmLanes::kN);
+      const char* d = L.buf[ln];
+      const int64_t c0 = c0_of(i), c = c1_of(i) - c0;
+      const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
+      const size_t r0 = static_cast<size_t>(c0) * static_cast<size_t>(l);
+      d2h(node_index + r0, d + o_n, 4 * cl, L.st[ln]);
+      d2h(edge_index + r0, d + o_e, 4 * cl, L.st[ln]);
+      if (dt32) d2h(dt32 + r0, d + o_f, 4 * cl, L.st[ln]);
+      if (dt64) d2h(dt64 + r0, d + o_d, 8 * cl, L.st[ln]);
+      d2h(valid_len + c0, d + o_v, 4 * static_cast<size_t>(c), L.st[ln]);
     };
     try {
-      for (Lane& ln : lanes) {
-        TGFX_CUDA(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
-        TGFX_CUDA(cudaStreamWaitEvent(ln.st, nodes_ready, 0));
-        ln.t = dmalloc(sizeof(double) * sub, ln.st);
-        ln.on = dmalloc(sizeof(int32_t) * sl, ln.st);
-        ln.oe = dmalloc(sizeof(int32_t) * sl, ln.st);
-        if (dt32) ln.o32 = dmalloc(sizeof(float) * sl, ln.st);
-        if (dt64) ln.o64 = dmalloc(sizeof(double) * sl, ln.st);
-        ln.ov = dmalloc(sizeof(int32_t) * sub, ln.st);
-      }
-      const int64_t nsub = ceil_div(q, sub);
-      auto compute = [&](int64_t i) {  // times upload + sampling of sub-chunk i on its lane
-        Lane& ln = lanes[i % kStreams];
-        const int64_t c0 = i * sub, c = std::min(sub, q - c0);
-        h2d(ln.t, times + c0, sizeof(double) * c, ln.st);
-        SampleArgs a{};
-        a.g = g;
-        a.nodes = dn.as<int64_t>() + c0;
-        a.times = static_cast<const double*>(ln.t);
-        a.q = c;
-        a.k = k;
-        a.strategy = strategy;
-        a.seed = seed;
-        a.stream_base = stream_base + static_cast<uint64_t>(c0);
-        a.l = l;
-        a.self_edge_index = self_edge_index;
-        a.node_index = ln.on;
-        a.edge_index = ln.oe;
-        a.dt32 = static_cast<float*>(ln.o32);
-        a.dt64 = static_cast<double*>(ln.o64);
-        a.valid_len = ln.ov;
-        launch_sample(a, ln.st);
-      };
-      auto copy_out = [&](int64_t i) {  // rows of sub-chunk i to the caller's buffers
-        Lane& ln = lanes[i % kStreams];
-        const int64_t c0 = i * sub, c = std::min(sub, q - c0);
-        const size_t cl = static_cast<size_t>(c) * static_cast<size_t>(l);
-        const size_t r0 = static_cast<size_t>(c0) * static_cast<size_t>(l);
-        d2h(node_index + r0, ln.on, sizeof(int32_t) * cl, ln.st);
-        d2h(edge_index + r0, ln.oe, sizeof(int32_t) * cl, ln.st);
-        if (dt32) d2h(dt32 + r0, ln.o32, sizeof(float) * cl, ln.st);
-        if (dt64) d2h(dt64 + r0, ln.o64, sizeof(double) * cl, ln.st);
-        d2h(valid_len + c0, ln.ov, sizeof(int32_t) * c, ln.st);
-      };
-      // the first sub-chunks sample while the host waits for the node check; nothing reaches
-      // the caller's buffers before it has passed
-      const int64_t pre = std::min<int64_t>(nsub, kStreams);
+      const int64_t pre = std::min<int64_t>(nsub, AsmLanes::kN);
       for (int64_t i = 0; i < pre; ++i) compute(i);
-      TGFX_CUDA(cudaStreamSynchronize(s));  // the node check -> bad
-      if (bad != none) {
-        release();
+      join();
+      if (bad >= 0) {
+        for (cudaStream_t st : L.st) cudaStreamSynchronize(st);
         throw Error(TGFX_EVALIDATION,
                     "query node " + std::to_string(nodes[bad]) + " out of range");
       }
@@ -1339,12 +1384,12 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
         if (i >= pre) compute(i);
         copy_out(i);
       }
-      for (Lane& ln : lanes) TGFX_CUDA(cudaStreamSynchronize(ln.st));
+      for (cudaStream_t st : L.st) TGFX_CUDA(cudaStreamSynchronize(st));
     } catch (...) {
-      release();
+      join();
+      for (cudaStream_t st : L.st) cudaStreamSynchronize(st);
       throw;
     }
-    release();
   });
 }
 
