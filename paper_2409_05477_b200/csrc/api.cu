@@ -206,6 +206,100 @@ void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
   if (bytes && h) TGFX_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
 }
 
+// ---- large copies from / to pageable host memory (a std::vector's columns, a caller's
+// malloc'd event array).  cudaMemcpy from pageable memory runs through the driver's bounce
+// buffer at ~11 GB/s on the pool's hosts; here host threads copy 64 MB chunks into a pinned
+// double buffer while the copy engine moves the previous chunk (DMA at ~55 GB/s).
+constexpr size_t kRingChunk = size_t(64) << 20;
+constexpr size_t kRingMin = size_t(256) << 20;  // smaller copies go straight through
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy split over up to 16 host threads (1 MB pieces at least)
+void par_memcpy(void* dst, const void* src, size_t n) {
+  const int T = static_cast<int>(std::min<size_t>(
+      std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())),
+      std::max<size_t>(1, n >> 20)));
+  if (T <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([=] {
+      const size_t a = n * t / T, b = n * (t + 1) / T;
+      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+  for (std::thread& x : th) x.join();
+}
+
+struct Ring {
+  char* pin[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int dev = -1;
+};
+
+Ring& ring() {
+  thread_local Ring r;
+  const int dev = device_info().device;
+  if (r.dev != dev) {
+    r = Ring{};
+    for (int i = 0; i < 2; ++i) {
+      TGFX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r.pin[i]), kRingChunk,
+                              cudaHostAllocPortable));
+      TGFX_CUDA(cudaEventCreateWithFlags(&r.done[i], cudaEventDisableTiming));
+    }
+    r.dev = dev;
+  }
+  return r;
+}
+
+// host -> device; returns once the host buffer may be reused (like a pageable cudaMemcpyAsync)
+void h2d_big(void* d, const void* h, size_t bytes, cudaStream_t s) {
+  if (bytes < kRingMin || host_pinned(h)) return h2d(d, h, bytes, s);
+  Ring& r = ring();
+  for (size_t off = 0, i = 0; off < bytes; off += kRingChunk, ++i) {
+    const size_t n = std::min(kRingChunk, bytes - off);
+    char* pin = r.pin[i & 1];
+    TGFX_CUDA(cudaEventSynchronize(r.done[i & 1]));  // its previous DMA has read it
+    par_memcpy(pin, static_cast<const char*>(h) + off, n);
+    TGFX_CUDA(cudaMemcpyAsync(static_cast<char*>(d) + off, pin, n, cudaMemcpyHostToDevice, s));
+    TGFX_CUDA(cudaEventRecord(r.done[i & 1], s));
+  }
+  TGFX_CUDA(cudaStreamSynchronize(s));
+}
+
+// device -> host, complete on return
+void d2h_big(void* h, const void* d, size_t bytes, cudaStream_t s) {
+  if (!h || bytes < kRingMin || host_pinned(h)) {
+    d2h(h, d, bytes, s);
+    return;
+  }
+  Ring& r = ring();
+  const size_t nch = (bytes + kRingChunk - 1) / kRingChunk;
+  auto issue = [&](size_t i) {
+    const size_t off = i * kRingChunk, n = std::min(kRingChunk, bytes - off);
+    TGFX_CUDA(cudaMemcpyAsync(r.pin[i & 1], static_cast<const char*>(d) + off, n,
+                              cudaMemcpyDeviceToHost, s));
+    TGFX_CUDA(cudaEventRecord(r.done[i & 1], s));
+  };
+  for (size_t i = 0; i < std::min<size_t>(2, nch); ++i) issue(i);
+  for (size_t i = 0; i < nch; ++i) {
+    const size_t off = i * kRingChunk, n = std::min(kRingChunk, bytes - off);
+    TGFX_CUDA(cudaEventSynchronize(r.done[i & 1]));
+    par_memcpy(static_cast<char*>(h) + off, r.pin[i & 1], n);
+    if (i + 2 < nch) issue(i + 2);
+  }
+}
+
 void check_graph(const tgfx_graph* g) {
   if (!g) throw Error(TGFX_EVALIDATION, "null graph");
 }
@@ -404,7 +498,7 @@ int build_host(const tgfx_event* events, int64_t n, int64_t V, int reverse, tgfx
     device_info();
     const double t0 = now_ms();
     DBuf dev(sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 1)), s);
-    h2d(dev.p, events, sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 0)), s);
+    h2d_big(dev.p, events, sizeof(tgfx_event) * static_cast<size_t>(std::max<int64_t>(n, 0)), s);
     if (trace_on()) TGFX_CUDA(cudaStreamSynchronize(s));
     const double t1 = now_ms();
     g = new_graph(n, V, reverse, s);
@@ -649,10 +743,10 @@ int tgfx_graph_export(const tgfx_graph* g, int64_t* indptr, int64_t* nbr, int64_
     check_graph(g);
     cudaStream_t s = 0;
     ensure_columns(g, s);
-    d2h(indptr, g->indptr, sizeof(int64_t) * (g->V + 1), s);
-    d2h(nbr, g->nbr, sizeof(int64_t) * g->m, s);
-    d2h(eid, g->eid, sizeof(int64_t) * g->m, s);
-    d2h(ts, g->ts, sizeof(double) * g->m, s);
+    d2h_big(indptr, g->indptr, sizeof(int64_t) * (g->V + 1), s);
+    d2h_big(nbr, g->nbr, sizeof(int64_t) * g->m, s);
+    d2h_big(eid, g->eid, sizeof(int64_t) * g->m, s);
+    d2h_big(ts, g->ts, sizeof(double) * g->m, s);
     TGFX_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <fstream>
 #include <mutex>
+#include <type_traits>
 
 #include <omp.h>
 
@@ -254,6 +255,24 @@ void TCsr::validate() const {
 
 namespace {
 
+// A column of n entries for export_graph: on large columns every thread first faults in its
+// share of the (reserved, not yet constructed) pages, so resize() -- which value-initialises,
+// i.e. memsets -- runs over resident memory.  Faulting the ~9 GB of fresh pages of a
+// GDELT-sized T-CSR on one thread took seconds; the element type is trivial, so writing the
+// reserved bytes before resize() constructs the elements has no observable effect.
+template <typename T>
+void sized_column(std::vector<T>& v, std::size_t n) {
+  static_assert(std::is_trivially_default_constructible_v<T>, "trivial column type");
+  v.reserve(n);
+  const std::int64_t bytes = static_cast<std::int64_t>(n * sizeof(T));
+  if (bytes >= (std::int64_t(64) << 20)) {
+    volatile char* p = reinterpret_cast<volatile char*>(v.data());
+#pragma omp parallel for schedule(static)
+    for (std::int64_t off = 0; off < bytes; off += 4096) p[off] = 0;
+  }
+  v.resize(n);
+}
+
 TCsr export_graph(tgfx_graph* h, bool reverse) {
   TCsr g;
   std::int64_t V = 0, E = 0, m = 0;
@@ -262,10 +281,10 @@ TCsr export_graph(tgfx_graph* h, bool reverse) {
   g.num_nodes = V;
   g.num_edges = E;
   g.reverse = reverse;
-  g.indptr.resize(static_cast<std::size_t>(V) + 1);
-  g.neighbor_ids.resize(static_cast<std::size_t>(m));
-  g.edge_ids.resize(static_cast<std::size_t>(m));
-  g.timestamps.resize(static_cast<std::size_t>(m));
+  sized_column(g.indptr, static_cast<std::size_t>(V) + 1);
+  sized_column(g.neighbor_ids, static_cast<std::size_t>(m));
+  sized_column(g.edge_ids, static_cast<std::size_t>(m));
+  sized_column(g.timestamps, static_cast<std::size_t>(m));
   detail::check(tgfx_graph_export(h, g.indptr.data(), g.neighbor_ids.data(), g.edge_ids.data(),
                                   g.timestamps.data()));
   detail::attach(g, h);
