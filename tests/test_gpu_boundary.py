@@ -200,3 +200,35 @@ def test_fused_query_check():
     tr = D.sample_assemble(g, bad[:9000], times[:9000], 10, "recent", 9, 11, E + 1, trusted=True)
     torch.cuda.synchronize()
     assert int(tr["valid_len"][40]) == 0
+
+
+def test_host_buffer_sample_assemble_sub_chunks(T):
+    """tgfx_sample_assemble with host buffers over several sub-chunks (a short head sub-chunk,
+    then full ones, alternating between two lanes): rows equal the device-buffer call on the
+    same queries (uniform-k included, so every sub-chunk's RNG stream offset is checked), and a
+    bad node in a late sub-chunk raises the reference's error with the caller's buffers left
+    untouched (sampler.cpp:88-93 validates every query before anything is returned)."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V = 400_000, 3000
+    ev = D.random_stream(E, V, 21)
+    g = D.build(ev, V, True)
+    nodes, times = D.make_queries(ev, 0, E, 600, V)  # 1.2 M queries: head + 1 full sub-chunk
+    hn, ht = nodes.cpu().numpy(), times.cpu().numpy()
+    th = g
+    for strat, k, l in (("recent", 10, 11), ("random", 20, 21)):
+        want = D.sample_assemble(g, nodes, times, k, strat, 9, l, E + 1, stream_base=77)
+        got = T.sample_assemble(th, hn, ht, k, strat, 9, l, E + 1, stream_base=77)
+        for key in ("node_index", "edge_index", "time_delta", "valid_len"):
+            assert np.array_equal(got[key], want[key].cpu().numpy()), (strat, key)
+    from paper_2409_05477_b200._lib import ValidationError, check, lib
+    bad = hn.copy()
+    bad[1_000_003] = V + 5
+    q, l = len(bad), 11
+    outs = [np.full(q * l, 7, np.int32), np.full(q * l, 7, np.int32),
+            np.full(q * l, 7.0, np.float32), np.full(q, 7, np.int32)]
+    with pytest.raises(ValidationError, match=f"query node {V + 5} out of range"):
+        check(lib().tgfx_sample_assemble(th.handle, bad.ctypes.data, ht.ctypes.data, q, 10, 0, 9,
+                                         0, l, E + 1, outs[0].ctypes.data, outs[1].ctypes.data,
+                                         outs[2].ctypes.data, None, outs[3].ctypes.data))
+    assert all((o == 7).all() for o in outs)
