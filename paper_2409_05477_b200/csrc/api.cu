@@ -231,13 +231,18 @@ void par_memcpy(void* dst, const void* src, size_t n) {
     std::memcpy(dst, src, n);
     return;
   }
+  auto piece = [=](int t) {
+    const size_t a = n * t / T, b = n * (t + 1) / T;
+    std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+  };
   std::vector<std::thread> th;
   th.reserve(static_cast<size_t>(T));
-  for (int t = 0; t < T; ++t)
-    th.emplace_back([=] {
-      const size_t a = n * t / T, b = n * (t + 1) / T;
-      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
-    });
+  int started = 0;
+  try {  // pieces no thread could be started for are copied here
+    for (; started < T; ++started) th.emplace_back(piece, started);
+  } catch (...) {
+  }
+  for (int t = started; t < T; ++t) piece(t);
   for (std::thread& x : th) x.join();
 }
 
@@ -1367,8 +1372,15 @@ int64_t first_bad_node_host(const int64_t* nodes, int64_t q, int64_t V) {
   std::vector<int64_t> first(static_cast<size_t>(T), -1);
   std::vector<std::thread> th;
   th.reserve(static_cast<size_t>(T));
-  for (int t = 0; t < T; ++t)
-    th.emplace_back([&, t] { first[static_cast<size_t>(t)] = scan(q * t / T, q * (t + 1) / T); });
+  int started = 0;
+  try {  // the ranges no thread could be started for are scanned here
+    for (; started < T; ++started)
+      th.emplace_back([&, started] {
+        first[static_cast<size_t>(started)] = scan(q * started / T, q * (started + 1) / T);
+      });
+  } catch (...) {
+  }
+  for (int t = started; t < T; ++t) first[static_cast<size_t>(t)] = scan(q * t / T, q * (t + 1) / T);
   for (std::thread& x : th) x.join();
   for (int64_t f : first)
     if (f >= 0) return f;
@@ -1416,10 +1428,17 @@ int tgfx_sample_assemble(const tgfx_graph* g, const int64_t* nodes, const double
     // the scan of nodes[1, q) runs on host threads beside the first sub-chunks
     int64_t bad = -1;
     std::thread checker;
-    if (q > 1) checker = std::thread([&] {
+    auto check_rest = [&] {
       const int64_t f = first_bad_node_host(nodes + 1, q - 1, g->V);
       bad = f < 0 ? -1 : f + 1;
-    });
+    };
+    if (q > 1) {
+      try {
+        checker = std::thread(check_rest);
+      } catch (...) {  // no thread: check before sampling instead of beside it
+        check_rest();
+      }
+    }
     auto join = [&] {
       if (checker.joinable()) checker.join();
     };
