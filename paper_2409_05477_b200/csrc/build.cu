@@ -1014,19 +1014,29 @@ __global__ void k_entry_keys(const tgfx_event* __restrict__ ev, int64_t m, K* ke
   }
 }
 
+// each output position gathers its entry's event; with `rec` the entry goes out as the
+// sampler's 16-byte gather record + ts (the int64 columns are widened on demand, as after the
+// small-V scatter), else as the three reference columns
 template <int R>
 __global__ void k_gather_entries(const tgfx_event* __restrict__ ev,
                                  const uint32_t* __restrict__ val, int64_t m, int64_t* nbr,
-                                 int64_t* eid, double* ts) {
+                                 int64_t* eid, double* ts, uint4* __restrict__ rec) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m;
        p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t j = val[p];
     const int64_t e = R == 2 ? (j >> 1) : j;
     const bool side = R == 2 && (j & 1);
     const Ev x = load_event(ev, e);
-    nbr[p] = side ? x.src : x.dst;
-    eid[p] = x.eid;
+    const int64_t other = side ? x.src : x.dst;
     ts[p] = x.t;
+    if (rec) {
+      const unsigned long long tb = static_cast<unsigned long long>(__double_as_longlong(x.t));
+      rec[p] = make_uint4(static_cast<uint32_t>(other), static_cast<uint32_t>(x.eid),
+                          static_cast<uint32_t>(tb), static_cast<uint32_t>(tb >> 32));
+    } else {
+      nbr[p] = other;
+      eid[p] = x.eid;
+    }
   }
 }
 
@@ -1813,10 +1823,12 @@ void build_large_k(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
   radix_sort_pairs<K, uint32_t>(k, v, kalt, valt, m, bits, s);
   k_indptr_lb<K><<<static_cast<unsigned>(ceil_div(V + 1, 256)), 256, 0, s>>>(k, m, V, g->indptr);
   after_launch("k_indptr_lb");
+  uint4* rec = ensure_rec(g, s);
+  g->cols_valid = rec == nullptr;
   if (g->reverse)
-    k_gather_entries<2><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts);
+    k_gather_entries<2><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts, rec);
   else
-    k_gather_entries<1><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts);
+    k_gather_entries<1><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts, rec);
   after_launch("k_gather_entries");
   dfree(key, s);
   dfree(kalt, s);
