@@ -151,6 +151,18 @@ void scan_u32_to_i64(const uint32_t* in, int64_t n, int64_t* out, cudaStream_t s
 }
 
 // ------------------------------------------------------------------ radix sort
+// onesweep tile shape and residency (1/16-scale MAG build, 3 passes of 162 M 8-byte pairs;
+// round 2): 16 keys per thread at 128 registers left 2 tiles per SM (occupancy limited by
+// registers and by the default shared-memory carveout) -> 11.6 ms; capped at 4 tiles per SM
+// (64 registers, 40 B of spills) with an 80 % carveout -> 10.3 ms.  Also measured: 3 tiles
+// per SM 11.4, 5 / 6 per SM 10.4 / 10.6, 8 keys per thread at 6 / 8 per SM 11.5 / 11.6,
+// 12 keys per thread at 5 per SM 11.0, 2 tiles per SM with a 100 % carveout 16.8 ms.
+#ifndef TGFX_OS_ROUNDS
+#define TGFX_OS_ROUNDS 16
+#endif
+#ifndef TGFX_OS_MINB
+#define TGFX_OS_MINB 4
+#endif
 namespace {
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
@@ -158,7 +170,7 @@ constexpr int kRsWarps = kRsThreads / 32;
 // as many tiles, so half the decoupled look-back walks), 8 otherwise (static shared memory)
 template <typename K, typename V>
 constexpr int rs_rounds() {
-  return sizeof(K) + sizeof(V) <= 8 ? 16 : 8;
+  return sizeof(K) + sizeof(V) <= 8 ? TGFX_OS_ROUNDS : 8;
 }
 
 // all digit positions' global histograms in one pass: hist[pass * 256 + digit] (u64)
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(kRsThreads) k_onesweep_hist(const K* __restric
 
 // one onesweep pass: digit (key >> shift) & 0xff; digit_base[256] = the digit's global start
 template <typename K, typename V>
-__global__ void __launch_bounds__(kRsThreads) k_onesweep(
+__global__ void __launch_bounds__(kRsThreads, TGFX_OS_MINB) k_onesweep(
     const K* __restrict__ keys_in, const V* __restrict__ vals_in, int64_t n, int shift,
     const int64_t* __restrict__ digit_base, unsigned long long* status, unsigned int* counter,
     K* __restrict__ keys_out, V* __restrict__ vals_out) {
@@ -322,6 +334,12 @@ void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
     }
     TGFX_CUDA(cudaMemcpyAsync(dbase, b, sizeof b, cudaMemcpyHostToDevice, s));
     TGFX_CUDA(cudaMemsetAsync(status, 0, sb + 16, s));
+    static const bool carve = [] {  // room for TGFX_OS_MINB resident tiles' shared memory
+      TGFX_CUDA(cudaFuncSetAttribute(k_onesweep<K, V>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 80));
+      return true;
+    }();
+    (void)carve;
     k_onesweep<K, V><<<static_cast<unsigned>(ntiles), kRsThreads, 0, s>>>(
         keys, vals, n, 8 * p, dbase, status, counter, keys_alt, vals_alt);
     after_launch("k_onesweep");
