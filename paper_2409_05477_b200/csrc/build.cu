@@ -1225,13 +1225,12 @@ __global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict_
   const int cnt = static_cast<int>(i1 - i0 + 1);
   const int64_t b0 = i0 + static_cast<int64_t>(tid) * P;
   double x[P];
-  if (b0 + P - 1 <= i1) {  // 64-byte aligned: four 16-byte loads
+  if (b0 + P - 1 <= i1) {  // 64-byte aligned: two 32-byte loads (one L1 wavefront per sector)
 #pragma unroll
-    for (int k = 0; k < P; k += 2) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(ts + b0 + k));
-      x[k] = v.x;
-      x[k + 1] = v.y;
-    }
+    for (int k = 0; k < P; k += 4)
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(x[k]), "=d"(x[k + 1]), "=d"(x[k + 2]), "=d"(x[k + 3])
+                   : "l"(ts + b0 + k));
   } else {
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = b0 + k <= i1 ? ts[b0 + k] : 0.0;
