@@ -264,6 +264,73 @@ __global__ void k_coldflags(const int64_t* __restrict__ deg, int32_t V, int64_t 
   if ((threadIdx.x & 31) == 0 && u < ((V + 31) & ~31)) coldbits[u >> 5] = b;
 }
 
+// Hot labels for the one-pass scatter (TGFX_SCATTER_VARIANT=50): the highest-degree non-cold
+// nodes, at most 255, get labels 0..L-1 in node order; every other node 255.  One block: a
+// degree threshold T is bisected until at most 255 non-cold nodes have degree >= T.
+__global__ void __launch_bounds__(1024) k_hot_labels(const int64_t* __restrict__ deg, int32_t V,
+                                                     const uint32_t* __restrict__ coldbits,
+                                                     uint8_t* __restrict__ hot) {
+  __shared__ int s_cnt;
+  __shared__ int s_wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto is_cand = [&](int u, int64_t T) {
+    return !((coldbits[u >> 5] >> (u & 31)) & 1u) && deg[u] >= T;
+  };
+  auto count = [&](int64_t T) {
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    int c = 0;
+    for (int u = tid; u < V; u += 1024) c += is_cand(u, T) ? 1 : 0;
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0 && c) atomicAdd(&s_cnt, c);
+    __syncthreads();
+    const int r = s_cnt;
+    __syncthreads();
+    return r;
+  };
+  int64_t lo = 0, hi = 0;  // smallest T with count(T) <= 255 lies in (lo, hi]
+  {
+    int64_t mx = 0;
+    for (int u = tid; u < V; u += 1024) mx = max(mx, static_cast<int64_t>(deg[u]));
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    __shared__ int64_t s_mx[32];
+    if (lane == 0) s_mx[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      int64_t m = 0;
+      for (int w = 0; w < 32; ++w) m = max(m, s_mx[w]);
+      s_mx[0] = m;
+    }
+    __syncthreads();
+    hi = s_mx[0] + 1;
+  }
+  if (count(0) <= 255) {
+    hi = 0;
+  } else {
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (count(mid) <= 255) hi = mid; else lo = mid;
+    }
+  }
+  const int64_t T = hi;
+  // labels in node order: each thread a contiguous node range, block exclusive scan of counts
+  const int per = (V + 1023) / 1024;
+  const int u0 = min(V, tid * per), u1 = min(V, u0 + per);
+  int c = 0;
+  for (int u = u0; u < u1; ++u) c += is_cand(u, T) ? 1 : 0;
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += s_wsum[w];
+  int next = before + x - c;
+  for (int u = u0; u < u1; ++u) hot[u] = is_cand(u, T) ? static_cast<uint8_t>(next++) : 255;
+}
+
 // K3: stable scatter ("ticketed warps") ---------------------------------------------------
 // Each CTA owns a contiguous chunk and its per-node cursors (shared memory).  The chunk is cut
 // into warp tiles of kTkRounds x 32 consecutive entries, taken by the CTA's warps round-robin.
@@ -968,6 +1035,278 @@ __global__ void __launch_bounds__(kBT, 2) k_scatter_big(
   }
 }
 
+// K3 one-pass variant (TGFX_SCATTER_VARIANT=50).  The hub nodes (k_hot_labels: <= 255 of
+// them, ~81 % of the GDELT-shaped entries) are ranked by ONE block-wide stable pass over their
+// 8-bit label; everything else (label 255) ends up as one run at the tile's end, still in
+// stream order, and the block's last warp sorts just that run by node (two warp-local 8-bit
+// passes) while the other seven place the hub runs: a hub run's tile offset is its label's
+// scanned start, so no run-head search is needed there.  Same shared memory as variant 43;
+// scur holds each node's cursor with its cold flag in bit 31 (positions < 2^31).
+template <int R, int TE, int S>
+__global__ void __launch_bounds__(kBT, 2) k_scatter_hot(
+    const tgfx_event* __restrict__ ev, int64_t n, int32_t V, int64_t chunk_ev,
+    uint32_t* __restrict__ off, const uint32_t* __restrict__ coldbits,
+    const uint8_t* __restrict__ hot, ulonglong2* __restrict__ cold_img,
+    double* __restrict__ ts_out, uint4* __restrict__ rec_out, int64_t* __restrict__ nbr_out,
+    int64_t* __restrict__ eid_out) {
+  constexpr int NE = TE * R;
+  constexpr int KPT = NE / kBT;
+  constexpr int kW = kBT / 32;
+  constexpr int kHubT = (kW - 1) * 32;           // hub-run threads (warps 0..kW-2)
+  constexpr int HMAX = (NE + kHubT - 1) / kHubT;  // hub positions per thread
+  constexpr int kCB = 8;                          // cold-sort rounds per MATCH batch
+  static_assert(KPT * kBT == NE && NE <= 65536 && kW == 8, "tile shape");
+  extern __shared__ __align__(128) unsigned char sm[];
+  tgfx_event* stage = reinterpret_cast<tgfx_event*>(sm);
+  uint32_t* keys0 = reinterpret_cast<uint32_t*>(sm + static_cast<size_t>(S) * TE * 32);
+  uint32_t* keys1 = keys0 + NE;
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(keys1 + NE);  // [kW][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wcnt + kW * 256);
+  int* scr = reinterpret_cast<int*>(bars + S);
+  uint32_t* scur = reinterpret_cast<uint32_t*>(scr + 64);  // [vpad] cursor | cold << 31
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  if (e0 >= e1) return;
+  const int64_t ntiles = ceil_div(e1 - e0, TE);
+  const uint32_t* crow = off + static_cast<int64_t>(blockIdx.x) * V;
+  for (int i = tid; i < V; i += kBT) scur[i] = crow[i] | (((coldbits[i >> 5] >> (i & 31)) & 1u) << 31);
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < S && q < ntiles; ++q) {
+      const int64_t b = e0 + static_cast<int64_t>(q) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[q], bytes);
+      bulk_g2s(stage + q * TE, ev + b, bytes, &bars[q]);
+    }
+  }
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int sidx = static_cast<int>(it % S);
+    const int64_t tb = e0 + it * TE;
+    const int ent = static_cast<int>(min(static_cast<int64_t>(TE), e1 - tb)) * R;
+    const tgfx_event* sev = stage + sidx * TE;
+    mbar_wait(&bars[sidx], static_cast<uint32_t>((it / S) & 1));
+    uint32_t key[KPT], dig[KPT], rank[KPT];
+    unsigned peers[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int j = warp * 32 * KPT + k * 32 + lane;
+      uint32_t node = static_cast<uint32_t>(V);  // sentinel: label 255, sorts after every node
+      if (j < ent) node = hot_node_of<R>(sev, j);
+      key[k] = (node << 16) | static_cast<uint32_t>(j);
+      dig[k] = node < static_cast<uint32_t>(V) ? __ldg(hot + node) : 255u;
+    }
+    // ---- one block-wide stable counting pass by label (as one pass of k_scatter_big)
+    uint16_t* wc = wcnt + warp * 256;
+    reinterpret_cast<uint4*>(wc)[lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) peers[k] = __match_any_sync(kFull, dig[k]);
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const uint32_t b = wc[dig[k]];
+      __syncwarp();
+      if (lane == __ffs(peers[k]) - 1) wc[dig[k]] = static_cast<uint16_t>(b + __popc(peers[k]));
+      __syncwarp();
+      rank[k] = b + __popc(peers[k] & lanemask_lt());
+    }
+    __syncthreads();
+    {
+      constexpr int kDT = 4;
+      constexpr int kNT = 256 / kDT;
+      uint2 v[kW];
+      uint32_t tot = 0;
+      if (tid < kNT) {
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+          v[w] = *reinterpret_cast<const uint2*>(wcnt + w * 256 + kDT * tid);
+          tot += (v[w].x & 0xffffu) + (v[w].x >> 16) + (v[w].y & 0xffffu) + (v[w].y >> 16);
+        }
+      }
+      uint32_t x = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31 && warp == 0) scr[0] = static_cast<int>(x);
+      __syncthreads();
+      if (tid < kNT) {
+        uint32_t run = (warp == 1 ? static_cast<uint32_t>(scr[0]) : 0u) + x - tot;
+        uint32_t o[kW][kDT];
+#pragma unroll
+        for (int dd = 0; dd < kDT; ++dd) {
+#pragma unroll
+          for (int w = 0; w < kW; ++w) {
+            const uint32_t word = dd < 2 ? v[w].x : v[w].y;
+            const uint32_t c = (word >> (16 * (dd & 1))) & 0xffffu;
+            o[w][dd] = run;
+            run += c;
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < kW; ++w)
+          *reinterpret_cast<uint2*>(wcnt + w * 256 + kDT * tid) =
+              make_uint2(o[w][0] | (o[w][1] << 16), o[w][2] | (o[w][3] << 16));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) keys1[wc[dig[k]] + rank[k]] = key[k];
+    __syncthreads();
+    // keys1: hub runs by label in [0, c0), the rest [c0, NE) in stream order.  wcnt row 0 =
+    // each label's tile start (the scan is in (label, warp) order).
+    const int c0 = wcnt[255];
+    if (warp < kW - 1) {
+      // ---- hub runs: position = cursor + offset from the label's start
+      const int ht = warp * 32 + lane;
+      uint32_t hk[HMAX], hp[HMAX], hc[HMAX];
+      int hl[HMAX];
+#pragma unroll
+      for (int i = 0; i < HMAX; ++i) {
+        const int sp = ht + kHubT * i;
+        hl[i] = -1;
+        if (sp < c0) {
+          const uint32_t k2 = keys1[sp];
+          const uint32_t u = k2 >> 16;
+          const uint32_t d = __ldg(hot + u);
+          const int r0 = wcnt[d];
+          const uint32_t c = scur[u];
+          hk[i] = k2;
+          hc[i] = c;
+          hp[i] = (c & 0x7fffffffu) + static_cast<uint32_t>(sp - r0);
+          if (sp == r0) hl[i] = static_cast<int>(wcnt[d + 1]) - r0;  // run length (head only)
+        }
+      }
+      named_bar_sync(1, kHubT);  // every hub cursor read before any is bumped
+#pragma unroll
+      for (int i = 0; i < HMAX; ++i) {
+        const int sp = ht + kHubT * i;
+        if (sp < c0) {
+          const uint32_t u = hk[i] >> 16;
+          if (hl[i] >= 0) scur[u] = hc[i] + static_cast<uint32_t>(hl[i]);
+          write_entry_known<R>(sev, static_cast<int>(hk[i] & 0xffffu), hp[i], u,
+                               (hc[i] >> 31) != 0, cold_img, ts_out, rec_out, nbr_out, eid_out);
+        }
+      }
+    } else {
+      // ---- the rest: one warp sorts [c0, NE) by node (two warp-local stable 8-bit passes)
+      const int ncr = NE - c0;
+      uint16_t* cnt = wcnt + (kW - 1) * 256;  // this warp's counter row
+      uint16_t* rk = wcnt + 256;              // ranks: rows 1..kW-2 (hub warps read row 0 only)
+      uint32_t* P = keys1 + c0;
+      uint32_t* Q = keys0 + c0;
+      for (int sh = 16; sh < 32; sh += 8) {
+        reinterpret_cast<uint4*>(cnt)[lane] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        for (int c0r = 0; c0r < ncr; c0r += 32 * kCB) {
+          // kCB rounds' MATCH.ANYs issued back to back (their ~400-cycle latencies overlap),
+          // then the counter chain round by round
+          uint32_t dd[kCB];
+          unsigned pe[kCB];
+#pragma unroll
+          for (int q = 0; q < kCB; ++q) {
+            const int i = c0r + q * 32 + lane;
+            dd[q] = i < ncr ? (P[i] >> sh) & 0xffu : 256u;
+          }
+#pragma unroll
+          for (int q = 0; q < kCB; ++q) pe[q] = __match_any_sync(kFull, dd[q]);
+#pragma unroll
+          for (int q = 0; q < kCB; ++q) {
+            const int i = c0r + q * 32 + lane;
+            const bool valid = i < ncr;
+            const uint32_t b = valid ? cnt[dd[q]] : 0u;
+            __syncwarp();
+            if (valid && lane == __ffs(pe[q]) - 1)
+              cnt[dd[q]] = static_cast<uint16_t>(b + __popc(pe[q]));
+            __syncwarp();
+            if (valid) rk[i] = static_cast<uint16_t>(b + __popc(pe[q] & lanemask_lt()));
+          }
+        }
+        __syncwarp();
+        {  // exclusive scan of the 256 counters, 8 per lane
+          uint4 w4 = reinterpret_cast<const uint4*>(cnt)[lane];
+          uint32_t c8[8] = {w4.x & 0xffffu, w4.x >> 16, w4.y & 0xffffu, w4.y >> 16,
+                            w4.z & 0xffffu, w4.z >> 16, w4.w & 0xffffu, w4.w >> 16};
+          uint32_t t = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) t += c8[q];
+          uint32_t xs = t;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, xs, o);
+            if (lane >= o) xs += y;
+          }
+          uint32_t r = xs - t, e8[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            e8[q] = r;
+            r += c8[q];
+          }
+          __syncwarp();
+          reinterpret_cast<uint4*>(cnt)[lane] =
+              make_uint4(e8[0] | (e8[1] << 16), e8[2] | (e8[3] << 16), e8[4] | (e8[5] << 16),
+                         e8[6] | (e8[7] << 16));
+          __syncwarp();
+        }
+        for (int c = 0; c < ncr; c += 32) {
+          const int i = c + lane;
+          if (i < ncr) {
+            const uint32_t k2 = P[i];
+            Q[cnt[(k2 >> sh) & 0xffu] + rk[i]] = k2;
+          }
+        }
+        __syncwarp();
+        uint32_t* t2 = P;
+        P = Q;
+        Q = t2;
+      }
+      // P: sorted by node; Q: head cursors.  Runs: the head reads the cursor, every entry
+      // finds its head by a max-scan (carried across rounds), the tail bumps the cursor.
+      int carry = -1;
+      for (int c = 0; c < ncr; c += 32) {
+        const int i = c + lane;
+        const bool valid = i < ncr;
+        const uint32_t k2 = valid ? P[i] : 0xffffffffu;
+        const uint32_t u = k2 >> 16;
+        const bool real = valid && u < static_cast<uint32_t>(V);
+        const bool head = real && (i == 0 || (P[i - 1] >> 16) != u);
+        if (head) Q[i] = scur[u];
+        int xh = head ? i : -1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, xh, o);
+          if (lane >= o) xh = max(xh, y);
+        }
+        xh = max(xh, carry);
+        carry = __shfl_sync(kFull, xh, 31);
+        __syncwarp();
+        if (real) {
+          const uint32_t cur = Q[xh];
+          const uint32_t pos = (cur & 0x7fffffffu) + static_cast<uint32_t>(i - xh);
+          const bool tail = i == ncr - 1 || (P[i + 1] >> 16) != u;
+          if (tail) scur[u] = cur + static_cast<uint32_t>(i - xh + 1);
+          write_entry_known<R>(sev, static_cast<int>(k2 & 0xffffu), pos, u, (cur >> 31) != 0,
+                               cold_img, ts_out, rec_out, nbr_out, eid_out);
+        }
+      }
+    }
+    __syncthreads();  // stage consumed; cursor stores ordered before the next tile's loads
+    if (tid == 0 && it + S < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t b = e0 + (it + S) * TE;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(TE), e1 - b) * 32);
+      mbar_arrive_tx(&bars[sidx], bytes);
+      bulk_g2s(stage + sidx * TE, ev + b, bytes, &bars[sidx]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ general path helpers
 __device__ __forceinline__ uint64_t time_key(double t) {
   // total order of doubles consistent with operator< for non-NaN; -0.0 keyed as +0.0
@@ -1489,6 +1828,7 @@ int big_bps_t(int64_t V) {
 }
 
 int big_bps(int R, int v, int64_t V) {
+  if (v == 50) v = 43;  // k_scatter_hot: variant 43's tile shape and shared memory
 #define X(ID, TE, S, SC) \
   if (v == ID) return R == 2 ? big_bps_t<2, TE, S, SC>(V) : big_bps_t<1, TE, S, SC>(V);
   TGFX_BIG_SHAPES(X)
@@ -1499,6 +1839,10 @@ int big_bps(int R, int v, int64_t V) {
 // the big-tile variant this build uses, 0 if none (node ids 0..V must fit the 16-bit key field)
 int big_variant(int R, int64_t V) {
   int v = scatter_variant();
+  if (v == 50) {  // one-pass hot-label scatter: variant 43's shared memory; else 43's fallbacks
+    if (V <= 65534 && t_build_m < (int64_t(1) << 31) && big_bps(R, 43, V) >= 2) return 50;
+    v = 43;
+  }
   if (v < 40 || v > 45 || V > 65534 || t_build_m >= (int64_t(1) << 32)) return 0;
   if (v == 43 && big_bps(R, 43, V) < 2) {
     // shared-memory cursors would leave one CTA per SM: the 256-event tile kernel when its
@@ -1667,18 +2011,24 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
   const int64_t vpad = (static_cast<int64_t>(V) + 31) & ~31LL;
   // small workspace: cold bitmask [vpad/32] u32 | cdelta [V] i64 | ncold i64
   const int64_t cb = (4 * (vpad / 32) + 15) & ~15LL;
-  char* small = static_cast<char*>(ws_get(g->ws_small, g->ws_small_bytes, cb + 8 * (vpad + 2), s));
+  char* small = static_cast<char*>(
+      ws_get(g->ws_small, g->ws_small_bytes, cb + 8 * (vpad + 2) + vpad, s));
   uint32_t* coldbits = reinterpret_cast<uint32_t*>(small);
   int64_t* cdelta = reinterpret_cast<int64_t*>(small + cb);
   int64_t* ncold_d = cdelta + vpad;
+  uint8_t* hot = reinterpret_cast<uint8_t*>(small + cb + 8 * (vpad + 2));  // variant 50 labels
   const int R = g->reverse ? 2 : 1;
-  const int bigv = big_variant(R, V);
+  int bigv = big_variant(R, V);
   if (V > 0) {
     k_colsum<<<vb, tb, 0, s>>>(cnt, C, V, g->indptr);
     after_launch("k_colsum");
     k_coldflags<<<static_cast<int>(ceil_div(vpad, tb)), tb, 0, s>>>(g->indptr, V,
                                                                      cold_theta() * C, coldbits);
     after_launch("k_coldflags");
+    if (bigv == 50) {  // degrees are still in indptr here
+      k_hot_labels<<<1, 1024, 0, s>>>(g->indptr, V, coldbits, hot);
+      after_launch("k_hot_labels");
+    }
   }
   k_indptr_scan<<<1, 1024, 0, s>>>(g->indptr, V, coldbits, cdelta, ncold_d);
   after_launch("k_indptr_scan");
@@ -1704,6 +2054,27 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
     while ((int64_t(1) << bits) <= V) ++bits;  // node ids 0..V (V = tail sentinel)
     const int passes = (bits + 7) / 8;
     const int cflag = std::max(g->m, ncold) < (int64_t(1) << 31) ? 1 : 0;
+    if (bigv == 50 && cflag) {
+      static const bool attr = [&] {
+        TGFX_CUDA(cudaFuncSetAttribute(k_scatter_hot<2, 512, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(device_info().smem_optin)));
+        TGFX_CUDA(cudaFuncSetAttribute(k_scatter_hot<1, 512, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(device_info().smem_optin)));
+        return true;
+      }();
+      (void)attr;
+      if (g->reverse)
+        k_scatter_hot<2, 512, 2><<<C, kBT, big_smem<2, 512, 2, true>(V), s>>>(
+            d_ev, g->n, V, chunk_ev, cnt, coldbits, hot, img, g->ts, rec, g->nbr, g->eid);
+      else
+        k_scatter_hot<1, 512, 2><<<C, kBT, big_smem<1, 512, 2, true>(V), s>>>(
+            d_ev, g->n, V, chunk_ev, cnt, coldbits, hot, img, g->ts, rec, g->nbr, g->eid);
+      after_launch("k_scatter_hot");
+    } else if (bigv == 50) {
+      bigv = 43;
+    }
 #define X(ID, TE, S, SC)                                                                       \
     if (bigv == ID) {                                                                          \
       if (g->reverse)                                                                          \
@@ -1715,9 +2086,11 @@ void build_fast(tgfx_graph* g, const tgfx_event* d_ev, int C, int64_t chunk_ev, 
             d_ev, g->n, V, chunk_ev, passes, cnt, coldbits, img, g->ts, rec, g->nbr, g->eid,   \
             cflag);                                                                             \
     }
-    TGFX_BIG_SHAPES(X)
+    if (bigv != 50) {
+      TGFX_BIG_SHAPES(X)
+      after_launch("k_scatter_big");
+    }
 #undef X
-    after_launch("k_scatter_big");
     if (ncold > 0) {
       k_cold_u<<<resident_grid(k_cold_u, 256, 0, ncold), 256, 0, s>>>(img, ncold, cdelta, g->nbr,
                                                                       g->eid, g->ts, rec);

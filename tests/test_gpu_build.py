@@ -191,3 +191,29 @@ def test_rebuild_refreshes_lazily_widened_columns(oracle_mod):
         assert np.array_equal(out["edge_index"].cpu().numpy(), want["edge_index"])
         assert np.array_equal(out["time_delta64"].cpu().numpy(), want["time_delta"])
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("variant", ["50", "45", "10"])
+def test_scatter_variants_build_the_same_tcsr(variant):
+    """The A/B scatter variants (TGFX_SCATTER_VARIANT, read once per process, so each runs in
+    its own process) build the default's T-CSR bit for bit on a GDELT-like shape (Zipf hubs,
+    cold tail, reverse = 1): 50 = one pass over hub labels + a warp-sorted remainder."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, hashlib; sys.path.insert(0, %r)\n"
+        "from paper_2409_05477_b200 import device as D\n"
+        "ev = D.random_stream(3_000_000, 16682, 42)\n"
+        "g = D.build(ev, 16682, True)\n"
+        "h = hashlib.sha256()\n"
+        "for t in D.graph_tensors(g): h.update(t.cpu().numpy().tobytes())\n"
+        "print(h.hexdigest())\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = {}
+    for v in ("43", variant):
+        env = dict(os.environ, TGFX_SCATTER_VARIANT=v)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = r.stdout.strip().splitlines()[-1]
+    assert out[variant] == out["43"]
