@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
+#include <thread>
+#include <vector>
 
 #include "doctest.h"
 #include "tgformer/sampler.hpp"
@@ -277,4 +279,39 @@ TEST_CASE("forward_concat route: large batches (threaded unpack) equal small one
     CHECK(dev.valid_len == want.valid_len);
   }
   CHECK(tgf::build_sequence_batch({}, 4, 1).batch == 0);
+}
+
+TEST_CASE("concurrent readers: threads sampling one TCsr get the single-threaded results") {
+  // a TCsr is safe for concurrent readers; each calling thread has its own device
+  // arena, stream and pinned staging in the host layer
+  const tgf::EventStream st = tgf::make_random_stream(50000, 300, 12);
+  const tgf::TCsr g = tgf::build_parallel(st, true, 4);
+  std::vector<tgf::NodeId> nodes;
+  std::vector<tgf::Time> times;
+  for (int i = 0; i < 50000; i += 10) {
+    nodes.push_back(st.events[i].dst);
+    times.push_back(st.events[i].timestamp);
+  }
+  const auto want_s = tgf::sample_batch(g, nodes, times, 10, tgf::SampleStrategy::random, 3);
+  const auto want = tgf::build_sequence_batch(want_s, 11, 50001);
+  const auto want_f = tgf::sample_sequence_batch(g, nodes, times, 10,
+                                                 tgf::SampleStrategy::random, 3, 11, 50001);
+  std::vector<int> ok(8, 0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < 8; ++t)
+    th.emplace_back([&, t] {
+      bool good = true;
+      for (int rep = 0; rep < 5; ++rep) {
+        const auto s = tgf::sample_batch(g, nodes, times, 10, tgf::SampleStrategy::random, 3);
+        const auto q = tgf::build_sequence_batch(s, 11, 50001);
+        const auto f = tgf::sample_sequence_batch(g, nodes, times, 10,
+                                                  tgf::SampleStrategy::random, 3, 11, 50001);
+        good = good && q.node_index == want.node_index && q.edge_index == want.edge_index &&
+               q.time_delta == want.time_delta && q.valid_len == want.valid_len &&
+               f.node_index == want_f.node_index && f.time_delta == want_f.time_delta;
+      }
+      ok[t] = good ? 1 : 0;
+    });
+  for (auto& x : th) x.join();
+  for (int t = 0; t < 8; ++t) CHECK(ok[t] == 1);
 }
