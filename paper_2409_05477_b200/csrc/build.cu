@@ -1365,7 +1365,16 @@ __global__ void k_gather_entries(const tgfx_event* __restrict__ ev,
     const uint32_t j = val[p];
     const int64_t e = R == 2 ? (j >> 1) : j;
     const bool side = R == 2 && (j & 1);
-    const Ev x = load_event(ev, e);
+    Ev x;  // the event's one 32-byte sector in one load
+    {
+      long long a0, a1, a2, a3;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.s64 {%0, %1, %2, %3}, [%4];"
+                   : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(ev + e));
+      x.eid = a0;
+      x.src = a1;
+      x.dst = a2;
+      x.t = __longlong_as_double(a3);
+    }
     const int64_t other = side ? x.src : x.dst;
     ts[p] = x.t;
     if (rec) {
