@@ -141,6 +141,107 @@ __global__ void __launch_bounds__(kHistThreads) k_hist(const tgfx_event* __restr
   }
 }
 
+// the large-V sort input made by k_flags_keys
+struct LargePre {
+  uint32_t* key;
+  uint32_t* val;
+  unsigned long long* hist;  // [passes][256]
+};
+
+// Large-V flags pass (k_hist's checks: endpoints, (t, eid) order, NaN, eid range) that also
+// emits the sort input of build_large_k -- key = the entry's node, val = its emission index --
+// and the keys' 8-bit digit histograms for all `passes` digit positions: the event stream is
+// read once instead of three times (flags, keys, histograms).  The keys are used only when
+// the stream turns out (t, eid)-sorted.
+template <int R>
+__global__ void __launch_bounds__(kHistThreads) k_flags_keys(const tgfx_event* __restrict__ ev,
+                                                             int64_t n, int64_t V, int64_t Vd,
+                                                             int64_t chunk_ev, int passes,
+                                                             uint32_t* __restrict__ key,
+                                                             uint32_t* __restrict__ val,
+                                                             unsigned long long* __restrict__ dh,
+                                                             BuildFlags* flags) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += kHistThreads) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * chunk_ev;
+  const int64_t e1 = min(n, e0 + chunk_ev);
+  bool unsorted = false, nan = false;
+  unsigned long long bad = ~0ull;
+  long long mx = LLONG_MIN, mn = LLONG_MAX;
+  constexpr int U = 4;
+  for (int64_t b = e0; b < e1; b += U * kHistThreads) {
+    Ev xs[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = b + k * kHistThreads + threadIdx.x;
+      xs[k] = e < e1 ? load_event(ev, e) : Ev{0, 0, 0, 0.0};
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = b + k * kHistThreads + threadIdx.x;
+      const bool valid = e < e1;
+      const Ev x = xs[k];
+      double tn = __shfl_down_sync(kFull, x.t, 1);
+      long long en = __shfl_down_sync(kFull, (long long)x.eid, 1);
+      if (valid && e + 1 < n && (lane == 31 || e + 1 >= e1)) {
+        const Ev y = load_event(ev, e + 1);
+        tn = y.t;
+        en = y.eid;
+      }
+      if (valid && e + 1 < n) {
+        const bool ok = (x.t < tn) || (x.t == tn && x.eid <= en);  // NaN -> not ok
+        unsorted |= !ok;
+      }
+      const bool ok_s = valid && x.src >= 0 && x.src < V;
+      const bool ok_d = valid && x.dst >= 0 && x.dst < Vd;
+      if (valid && !(ok_s && ok_d)) bad = min(bad, (unsigned long long)e);
+      if (valid) {
+        nan |= x.t != x.t;
+        mx = max(mx, (long long)x.eid);
+        mn = min(mn, (long long)x.eid);
+        // the entries of event e: j = R e (+ 1 for the reverse side), in emission order
+        const uint32_t us = static_cast<uint32_t>(x.src), ud = static_cast<uint32_t>(x.dst);
+        if (R == 2) {
+          reinterpret_cast<uint2*>(key)[e] = make_uint2(us, ud);
+          reinterpret_cast<uint2*>(val)[e] =
+              make_uint2(static_cast<uint32_t>(2 * e), static_cast<uint32_t>(2 * e + 1));
+        } else {
+          key[e] = us;
+          val[e] = static_cast<uint32_t>(e);
+        }
+        if (ok_s && ok_d) {
+          for (int p = 0; p < passes; ++p) {
+            atomicAdd(&h[p][(us >> (8 * p)) & 0xffu], 1u);
+            if (R == 2) atomicAdd(&h[p][(ud >> (8 * p)) & 0xffu], 1u);
+          }
+        }
+      }
+    }
+  }
+  unsorted = __any_sync(kFull, unsorted);
+  nan = __any_sync(kFull, nan);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad = min(bad, __shfl_xor_sync(kFull, bad, o));
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+  }
+  if (lane == 0) {
+    if (unsorted) atomicOr(&flags->unsorted, 1);
+    if (nan) atomicOr(&flags->has_nan, 1);
+    if (bad != ~0ull) atomicMin(&flags->bad_index, bad);
+    if (mx != LLONG_MIN) atomicMax(&flags->max_eid, mx);
+    if (mn != LLONG_MAX) atomicMin(&flags->min_eid, mn);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kHistThreads) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(dh + i, static_cast<unsigned long long>(c));
+  }
+}
+
 // K2a: degree of u = column sum of the chunk table (written to indptr[u] as a temporary)
 __global__ void k_colsum(const uint32_t* __restrict__ cnt, int C, int32_t V, int64_t* deg) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1791,6 +1892,15 @@ int64_t cold_theta() {
   return theta;
 }
 
+// TGFX_LARGE_FUSE=0: the large-V build's keys and histograms in their own passes (A/B)
+bool large_fuse_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TGFX_LARGE_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int scatter_variant() {
   static int v = [] {
     const char* e = getenv("TGFX_SCATTER_VARIANT");
@@ -2184,24 +2294,33 @@ __global__ void k_indptr_lb(const K* __restrict__ keys, int64_t m, int64_t V,
 
 // large V: (node, emission index) pairs sorted by node (stable LSD, 32-bit keys while node ids
 // fit), indptr from the sorted keys, then each output position gathers its event
-template <typename K>
-void build_large_k(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
-  const int64_t V = g->V, m = g->m;
-  const int grid = grid_for(m, 256);
-  K* key = static_cast<K*>(dmalloc(sizeof(K) * m, s));
-  K* kalt = static_cast<K*>(dmalloc(sizeof(K) * m, s));
-  uint32_t* val = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
-  uint32_t* valt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
-  if (g->reverse)
-    k_entry_keys<2, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
-  else
-    k_entry_keys<1, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
-  after_launch("k_entry_keys");
+// node-id bits the large-V sort orders by (its digit passes: (bits + 7) / 8)
+int large_key_bits(int64_t V) {
   int bits = 1;
   while (bits < 63 && (int64_t(1) << bits) < V) ++bits;
+  return bits;
+}
+
+// pre: the sort input and its digit histograms from k_flags_keys (32-bit keys), or null
+template <typename K>
+void build_large_k(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, const LargePre* pre) {
+  const int64_t V = g->V, m = g->m;
+  const int grid = grid_for(m, 256);
+  K* key = pre ? reinterpret_cast<K*>(pre->key) : static_cast<K*>(dmalloc(sizeof(K) * m, s));
+  K* kalt = static_cast<K*>(dmalloc(sizeof(K) * m, s));
+  uint32_t* val = pre ? pre->val : static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
+  uint32_t* valt = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * m, s));
+  if (!pre) {
+    if (g->reverse)
+      k_entry_keys<2, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
+    else
+      k_entry_keys<1, K><<<grid, 256, 0, s>>>(d_ev, m, key, val);
+    after_launch("k_entry_keys");
+  }
+  const int bits = large_key_bits(V);
   K* k = key;
   uint32_t* v = val;
-  radix_sort_pairs<K, uint32_t>(k, v, kalt, valt, m, bits, s);
+  radix_sort_pairs<K, uint32_t>(k, v, kalt, valt, m, bits, s, pre ? pre->hist : nullptr);
   k_indptr_lb<K><<<static_cast<unsigned>(ceil_div(V + 1, 256)), 256, 0, s>>>(k, m, V, g->indptr);
   after_launch("k_indptr_lb");
   uint4* rec = ensure_rec(g, s);
@@ -2211,13 +2330,16 @@ void build_large_k(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
   else
     k_gather_entries<1><<<grid, 256, 0, s>>>(d_ev, v, m, g->nbr, g->eid, g->ts, rec);
   after_launch("k_gather_entries");
-  dfree(key, s);
+  if (!pre) {  // pre's buffers belong to the caller
+    dfree(key, s);
+    dfree(val, s);
+  }
   dfree(kalt, s);
-  dfree(val, s);
   dfree(valt, s);
 }
 
-void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
+void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s,
+                 const LargePre* pre = nullptr) {
   const int64_t V = g->V, m = g->m;
   if (m >= (int64_t(1) << 32)) throw Error(TGFX_EUNSUPPORTED, "more than 2^32 entries");
   if (m == 0) {
@@ -2225,9 +2347,9 @@ void build_large(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s) {
     return;
   }
   if (V <= 0xffffffffLL)
-    build_large_k<uint32_t>(g, d_ev, s);
+    build_large_k<uint32_t>(g, d_ev, s, pre);
   else
-    build_large_k<uint64_t>(g, d_ev, s);
+    build_large_k<uint64_t>(g, d_ev, s, nullptr);
 }
 
 }  // namespace
@@ -2340,10 +2462,48 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
     C = grid_for(n, kHistThreads, 4);
     chunk_ev = std::max<int64_t>(1, ceil_div(std::max<int64_t>(n, 1), C));
   }
-  run_flags_pass(g, d_ev, C, chunk_ev, cnt, fast && V > 0, s);
-  read_flags(g, s);
+  // large-V builds of a sorted stream: the flags pass also writes the sort input
+  LargePre pre{};
+  const bool fuse = !fast && g->m > 0 && g->m < (int64_t(1) << 32) && V <= 0xffffffffLL &&
+                    large_fuse_enabled();
+  if (fuse) {
+    const int passes = std::min(4, (large_key_bits(V) + 7) / 8);
+    pre.key = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->m, s));
+    pre.val = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t) * g->m, s));
+    pre.hist = static_cast<unsigned long long*>(dmalloc(sizeof(unsigned long long) * 1024, s));
+    TGFX_CUDA(cudaMemsetAsync(pre.hist, 0, sizeof(unsigned long long) * 1024, s));
+    k_init_flags<<<1, 1, 0, s>>>(g->dflags);
+    after_launch("k_init_flags");
+    const int64_t Vd = g->reverse ? V : g->other_limit;
+    if (g->reverse)
+      k_flags_keys<2><<<C, kHistThreads, 0, s>>>(d_ev, n, V, Vd, chunk_ev, passes, pre.key,
+                                                 pre.val, pre.hist, g->dflags);
+    else
+      k_flags_keys<1><<<C, kHistThreads, 0, s>>>(d_ev, n, V, Vd, chunk_ev, passes, pre.key,
+                                                 pre.val, pre.hist, g->dflags);
+    after_launch("k_flags_keys");
+  } else {
+    run_flags_pass(g, d_ev, C, chunk_ev, cnt, fast && V > 0, s);
+  }
+  auto drop_pre = [&] {
+    if (pre.key) {
+      dfree(pre.key, s);
+      dfree(pre.val, s);
+      dfree(pre.hist, s);
+      pre = LargePre{};
+    }
+  };
+  try {
+    read_flags(g, s);
+  } catch (...) {
+    drop_pre();
+    throw;
+  }
   const double t1 = trace_ms(s);
-  if (g->hflags->bad_index != ~0ull) throw_bad_endpoint(g, d_ev, s);
+  if (g->hflags->bad_index != ~0ull) {
+    drop_pre();
+    throw_bad_endpoint(g, d_ev, s);
+  }
   g->max_eid = n ? g->hflags->max_eid : -1;
   g->min_eid = n ? g->hflags->min_eid : 0;
   const tgfx_event* src = d_ev;
@@ -2351,6 +2511,7 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
   g->path = fast ? 0 : 2;
   g->search_exact = g->hflags->has_nan ? 1 : 0;
   if (g->hflags->unsorted) {
+    drop_pre();  // the keys of the unsorted stream are not the sort input
     tmp = sorted_copy(d_ev, n, s);
     src = tmp;
     if (fast) {
@@ -2358,10 +2519,17 @@ void build_graph(tgfx_graph* g, const tgfx_event* d_ev, cudaStream_t s, bool tru
       run_flags_pass(g, src, C, chunk_ev, cnt, V > 0, s);
     }
   }
-  if (fast)
-    build_fast(g, src, C, chunk_ev, cnt, s);
-  else
-    build_large(g, src, s);
+  try {
+    if (fast)
+      build_fast(g, src, C, chunk_ev, cnt, s);
+    else
+      build_large(g, src, s, pre.key ? &pre : nullptr);
+  } catch (...) {
+    drop_pre();
+    if (tmp) dfree(tmp, s);
+    throw;
+  }
+  drop_pre();
   if (tmp) dfree(tmp, s);
   const double t2 = trace_ms(s);
   build_node_dir(g, s);

@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kRsThreads, TGFX_OS_MINB) k_onesweep(
 
 template <typename K, typename V>
 void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
-                      int max_bits, cudaStream_t s) {
+                      int max_bits, cudaStream_t s, const unsigned long long* pre_hist) {
   if (n <= 1) return;
   const int passes = std::min(static_cast<int>(sizeof(K)), (max_bits + 7) / 8);
   if (passes <= 0) return;
@@ -315,12 +315,14 @@ void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
   int64_t* dbase = reinterpret_cast<int64_t*>(ws + hb);
   unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + hb + 2048);
   unsigned int* counter = reinterpret_cast<unsigned int*>(ws + hb + 2048 + sb);
-  TGFX_CUDA(cudaMemsetAsync(hist, 0, hb, s));
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, kRsThreads), 8 * 148));
-  k_onesweep_hist<K><<<grid, kRsThreads, 0, s>>>(keys, n, passes, hist);
-  after_launch("k_onesweep_hist");
+  if (!pre_hist) {
+    TGFX_CUDA(cudaMemsetAsync(hist, 0, hb, s));
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, kRsThreads), 8 * 148));
+    k_onesweep_hist<K><<<grid, kRsThreads, 0, s>>>(keys, n, passes, hist);
+    after_launch("k_onesweep_hist");
+  }
   std::vector<unsigned long long> h(256 * passes);
-  TGFX_CUDA(cudaMemcpyAsync(h.data(), hist, hb, cudaMemcpyDeviceToHost, s));
+  TGFX_CUDA(cudaMemcpyAsync(h.data(), pre_hist ? pre_hist : hist, hb, cudaMemcpyDeviceToHost, s));
   TGFX_CUDA(cudaStreamSynchronize(s));
   for (int p = 0; p < passes; ++p) {
     const unsigned long long* hp = h.data() + 256 * p;
@@ -351,10 +353,13 @@ void radix_sort_pairs(K*& keys, V*& vals, K* keys_alt, V* vals_alt, int64_t n,
 }
 
 template void radix_sort_pairs<uint64_t, uint32_t>(uint64_t*&, uint32_t*&, uint64_t*, uint32_t*,
-                                                   int64_t, int, cudaStream_t);
+                                                   int64_t, int, cudaStream_t,
+                                                   const unsigned long long*);
 template void radix_sort_pairs<uint64_t, uint64_t>(uint64_t*&, uint64_t*&, uint64_t*, uint64_t*,
-                                                   int64_t, int, cudaStream_t);
+                                                   int64_t, int, cudaStream_t,
+                                                   const unsigned long long*);
 template void radix_sort_pairs<uint32_t, uint32_t>(uint32_t*&, uint32_t*&, uint32_t*, uint32_t*,
-                                                   int64_t, int, cudaStream_t);
+                                                   int64_t, int, cudaStream_t,
+                                                   const unsigned long long*);
 
 }  // namespace tgfx
