@@ -217,3 +217,23 @@ def test_scatter_variants_build_the_same_tcsr(variant):
         assert r.returncode == 0, r.stderr[-2000:]
         out[v] = r.stdout.strip().splitlines()[-1]
     assert out[variant] == out["43"]
+
+
+def test_pageable_host_round_trip_through_the_staging_ring(T):
+    """Host-buffer build from a pageable 640 MB event array and export into pageable 320 MB
+    columns (both above the 256 MB threshold of the pinned staging ring: host threads fill and
+    drain 64 MB chunks beside the DMA) equal the device-buffer build's columns bit for bit."""
+    import torch
+    from paper_2409_05477_b200 import device as D
+    E, V = 20_000_000, 16682
+    st = T.make_random_stream(E, V, 5)  # host (pageable) events
+    assert st.events.nbytes >= 256 << 20
+    g = T.build_parallel(st, True, 8)
+    dev_ev = torch.from_numpy(st.events.view(np.uint8).reshape(-1)).cuda()
+    gd = D.build(dev_ev, V, True)
+    ip, nb, ed, ts = (t.cpu().numpy() for t in D.graph_tensors(gd))
+    assert g.neighbor_ids.nbytes >= 256 << 20
+    assert np.array_equal(g.indptr, ip)
+    assert np.array_equal(g.neighbor_ids, nb)
+    assert np.array_equal(g.edge_ids, ed)
+    assert g.timestamps.tobytes() == ts.view(np.float64).tobytes()
