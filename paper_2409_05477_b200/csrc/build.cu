@@ -1655,7 +1655,7 @@ __global__ void __launch_bounds__(256) k_bucket_fill(const int64_t* __restrict__
 // predecessor bucket is the previous entry's (a register) and the write loop runs per thread.
 // The node of every entry comes from the tile's head marks (one max-scan per tile) instead of
 // a per-entry search of indptr; tiles inside one slice (the hubs) skip even that.
-__global__ void __launch_bounds__(256) k_bucket_fill8(const int64_t* __restrict__ indptr,
+__global__ void __launch_bounds__(256, 6) k_bucket_fill8(const int64_t* __restrict__ indptr,
                                                       const int64_t* __restrict__ nbr,
                                                       const int64_t* __restrict__ eid,
                                                       const double* __restrict__ ts,
