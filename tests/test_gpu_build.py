@@ -237,3 +237,20 @@ def test_pageable_host_round_trip_through_the_staging_ring(T):
     assert np.array_equal(g.neighbor_ids, nb)
     assert np.array_equal(g.edge_ids, ed)
     assert g.timestamps.tobytes() == ts.view(np.float64).tobytes()
+
+
+def test_large_v_fused_key_pass_errors_and_reuse(T, oracle_mod):
+    """Large-V path (V > 45,000): the flags pass that also writes the sort keys reports the
+    first bad endpoint with the reference's text, and the graph built right after from a valid
+    stream (same allocator, buffers reused) is bit-exact."""
+    V = 200_000
+    ev = oracle_mod.make_random_stream(300_000, V, 31)
+    bad = ev.copy()
+    bad["dst"][123_456] = V + 3
+    for rev in (False, True):
+        with pytest.raises(T.ValidationError, match="event %d endpoint out of range"
+                           % int(bad["edge_id"][123_456])):
+            T.build_parallel(T.EventStream(bad, V), rev, 4)
+        got = T.build_parallel(T.EventStream(ev, V), rev, 4)
+        assert got.build_path == 2
+        assert_same(got, oracle_mod.build(ev, V, rev), rev)
